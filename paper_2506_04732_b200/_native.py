@@ -1,0 +1,249 @@
+"""ctypes binding of ``libt2s2.so`` (include/t2s2.h).
+
+This is the binding a reference maintainer would add to ``pkg/src/ttss``
+(see INTEGRATION.md).  There is no fallback: if the library or a CUDA
+device is missing, every entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import MarchStepError, ShapeError
+
+__all__ = [
+    "NativeUnavailable",
+    "lib",
+    "context",
+    "DeviceTrain",
+    "SolverConfigC",
+    "SolveReportC",
+    "StepReportC",
+    "check",
+    "LIB_PATH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libt2s2.so")
+MAX_SWEEPS = 1024
+
+T2S2_OK = 0
+T2S2_ERR_ARG = 1
+T2S2_ERR_CUDA = 2
+T2S2_ERR_SHAPE = 3
+T2S2_ERR_VALUE = 4
+T2S2_ERR_STAGNATION = 5
+T2S2_ERR_CAPACITY = 6
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA engine (libt2s2.so) could not be loaded or initialised."""
+
+
+class SolverConfigC(ctypes.Structure):
+    _fields_ = [
+        ("max_sweeps", ctypes.c_int),
+        ("residual_tol", ctypes.c_double),
+        ("rounding_tol", ctypes.c_double),
+        ("enrichment_rank", ctypes.c_int),
+        ("max_rank", ctypes.c_int),
+        ("local_solver", ctypes.c_int),
+        ("local_direct_size", ctypes.c_int),
+        ("inner_tol_factor", ctypes.c_double),
+        ("stagnation_window", ctypes.c_int),
+        ("stagnation_drop", ctypes.c_double),
+    ]
+
+
+class SolveReportC(ctypes.Structure):
+    _fields_ = [
+        ("n_sweeps", ctypes.c_int),
+        ("residuals", ctypes.c_double * MAX_SWEEPS),
+        ("ranks", ctypes.c_int * MAX_SWEEPS),
+        ("compression", ctypes.c_double * MAX_SWEEPS),
+        ("wall_time", ctypes.c_double),
+        ("converged", ctypes.c_int),
+        ("stagnated", ctypes.c_int),
+    ]
+
+
+class StepReportC(ctypes.Structure):
+    _fields_ = [
+        ("step", ctypes.c_int),
+        ("max_rank", ctypes.c_int),
+        ("compression", ctypes.c_double),
+        ("residual", ctypes.c_double),
+        ("sweeps", ctypes.c_int),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_D = ctypes.c_double
+_IP = ctypes.POINTER(ctypes.c_int)
+_DP = ctypes.POINTER(ctypes.c_double)
+
+_SIGNATURES = {
+    "t2s2_context_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "t2s2_context_destroy": (None, [_P]),
+    "t2s2_last_error": (ctypes.c_char_p, [_P]),
+    "t2s2_synchronize": (_I, [_P]),
+    "t2s2_train_upload": (_I, [_P, _I, _IP, _IP, _IP, _DP, ctypes.POINTER(_P)]),
+    "t2s2_train_upload_device": (_I, [_P, _I, _IP, _IP, _IP, _P, ctypes.POINTER(_P)]),
+    "t2s2_train_shape": (_I, [_P, _IP, _IP, _IP, _IP, ctypes.POINTER(ctypes.c_size_t)]),
+    "t2s2_train_download": (_I, [_P, _P, _DP, ctypes.c_size_t]),
+    "t2s2_train_free": (None, [_P]),
+    "t2s2_round": (_I, [_P, _P, _D, _I, ctypes.POINTER(_P)]),
+    "t2s2_norm": (_I, [_P, _P, _DP]),
+    "t2s2_dot": (_I, [_P, _P, _P, _DP]),
+    "t2s2_add": (_I, [_P, _P, _P, _D, _D, ctypes.POINTER(_P)]),
+    "t2s2_scale": (_I, [_P, _P, _D, ctypes.POINTER(_P)]),
+    "t2s2_apply": (_I, [_P, _P, _P, ctypes.POINTER(_P)]),
+    "t2s2_full": (_I, [_P, _P, _DP, ctypes.c_size_t]),
+    "t2s2_solve": (_I, [_P, _P, _P, _P, ctypes.POINTER(SolverConfigC), ctypes.POINTER(_P),
+                        ctypes.POINTER(SolveReportC)]),
+    "t2s2_residual": (_I, [_P, _P, _P, _P, _D, _DP]),
+    "t2s2_march": (_I, [_P, _P, _P, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _D,
+                        ctypes.POINTER(SolverConfigC), _I, ctypes.POINTER(_P),
+                        ctypes.POINTER(StepReportC), _IP]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lock = threading.Lock()
+_lib = None
+_ctx = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libt2s2.so and declare its prototypes (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `make` or __graft_entry__.build()"
+            )
+        try:
+            lib = ctypes.CDLL(path)
+        except OSError as exc:
+            raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    return load_library()
+
+
+def context():
+    """The process-wide engine context on device ``T2S2_DEVICE`` (default 0)."""
+    global _ctx
+    if _ctx is not None:
+        return _ctx
+    l = lib()
+    with _lock:
+        if _ctx is None:
+            dev = int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+            h = _P()
+            rc = l.t2s2_context_create(dev, ctypes.byref(h))
+            if rc != T2S2_OK:
+                raise NativeUnavailable(f"t2s2_context_create(device={dev}) failed with code {rc}"
+                                        " (no CUDA device?)")
+            _ctx = h
+    return _ctx
+
+
+def check(rc, step=None):
+    if rc == T2S2_OK:
+        return
+    msg = lib().t2s2_last_error(context()).decode(errors="replace")
+    if rc == T2S2_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == T2S2_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == T2S2_ERR_STAGNATION:
+        raise MarchStepError(step if step is not None else -1, msg)
+    raise RuntimeError(f"t2s2 error {rc}: {msg}")
+
+
+def _iarr(vals):
+    a = (ctypes.c_int * len(vals))(*[int(v) for v in vals])
+    return a
+
+
+class DeviceTrain:
+    """Owning handle of a device-resident train (vector or operator)."""
+
+    __slots__ = ("handle",)
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    @classmethod
+    def upload(cls, cores, is_op):
+        cores = [np.ascontiguousarray(c, dtype=np.float64) for c in cores]
+        d = len(cores)
+        rows = _iarr([c.shape[1] for c in cores])
+        cols = _iarr([c.shape[2] for c in cores]) if is_op else None
+        ranks = _iarr([1] + [c.shape[-1] for c in cores])
+        flat = np.concatenate([c.ravel() for c in cores]) if d else np.zeros(0)
+        flat = np.ascontiguousarray(flat)
+        h = _P()
+        check(lib().t2s2_train_upload(context(), d, rows, cols, ranks,
+                                      flat.ctypes.data_as(_DP), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def upload_device(cls, ptr, d, rows, cols, ranks):
+        h = _P()
+        check(lib().t2s2_train_upload_device(context(), d, _iarr(rows),
+                                             _iarr(cols) if cols is not None else None,
+                                             _iarr(ranks), _P(ptr), ctypes.byref(h)))
+        return cls(h)
+
+    def shape(self):
+        d = ctypes.c_int()
+        check(lib().t2s2_train_shape(self.handle, ctypes.byref(d), None, None, None, None))
+        n = d.value
+        rows, cols, ranks = (ctypes.c_int * n)(), (ctypes.c_int * n)(), (ctypes.c_int * (n + 1))()
+        total = ctypes.c_size_t()
+        check(lib().t2s2_train_shape(self.handle, None, rows, cols, ranks, ctypes.byref(total)))
+        return list(rows), list(cols), list(ranks), total.value
+
+    @property
+    def ranks(self):
+        return tuple(self.shape()[2])
+
+    def download(self):
+        rows, cols, ranks, total = self.shape()
+        buf = np.empty(total, dtype=np.float64)
+        check(lib().t2s2_train_download(context(), self.handle, buf.ctypes.data_as(_DP), total))
+        is_op = any(c > 0 for c in cols)
+        cores, off = [], 0
+        for l in range(len(rows)):
+            shape = ((ranks[l], rows[l], cols[l], ranks[l + 1]) if is_op
+                     else (ranks[l], rows[l], ranks[l + 1]))
+            size = int(np.prod(shape))
+            cores.append(buf[off: off + size].reshape(shape).copy())
+            off += size
+        return cores, is_op
+
+    def free(self):
+        if self.handle:
+            lib().t2s2_train_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

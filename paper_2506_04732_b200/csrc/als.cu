@@ -1,0 +1,528 @@
+// Rank-adaptive alternating TT solver on the device
+// (reference: pkg/src/ttss/tt_solver.py).
+//
+// Sweep structure, candidate logic and truncation follow the reference
+// exactly; every contraction, local matrix, factorisation and SVD runs on
+// the GPU.  The host reads back only the scalars that steer control flow:
+// candidate scores, singular values for the rank decisions, the residual.
+#include <chrono>
+#include <cmath>
+
+#include "als.h"
+#include "blas.h"
+#include "linalg.h"
+#include "tt.h"
+
+namespace t2s2 {
+namespace {
+
+int grid_of(long long n) {
+  long long g = (n + 255) / 256;
+  if (g < 1) g = 1;
+  if (g > 2368) g = 2368;
+  return (int)g;
+}
+
+// Column-major Galerkin block B[(x,m,y),(X,n,Y)] = sum_ab pal[x,a,X] ac[a,m,n,b] par[y,b,Y]
+// (tt_solver.py:213-216).
+__global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
+                                       const double* __restrict__ pal,
+                                       const double* __restrict__ ac,
+                                       const double* __restrict__ par, double* __restrict__ B) {
+  const long long N = (long long)rx * n * ry;
+  const long long total = N * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e % N, col = e / N;
+    const int y = (int)(row % ry), m = (int)((row / ry) % n), x = (int)(row / ((long long)ry * n));
+    const int Y = (int)(col % ry), nn = (int)((col / ry) % n), X = (int)(col / ((long long)ry * n));
+    double s = 0.0;
+    for (int a = 0; a < ra; ++a) {
+      const double pl = pal[((long long)x * ra + a) * rx + X];
+      if (pl == 0.0) continue;
+      const double* acp = ac + (((long long)a * n + m) * n + nn) * rb;
+      const double* prp = par + (long long)y * rb * ry + Y;
+      double t = 0.0;
+      for (int b = 0; b < rb; ++b) t = fma(acp[b], prp[(long long)b * ry], t);
+      s = fma(pl, t, s);
+    }
+    B[e] = s;
+  }
+}
+
+__global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) *flag = 1;
+}
+
+bool all_finite(const DTensor& t) {
+  int* flag = reinterpret_cast<int*>(allocator().alloc(1));
+  T2S2_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream()));
+  nonfinite_kernel<<<grid_of((long long)t.size()), 256, 0, stream()>>>(t.p, (long long)t.size(),
+                                                                         flag);
+  T2S2_CHECK_LAUNCH();
+  int h = 0;
+  T2S2_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  allocator().release(reinterpret_cast<double*>(flag));
+  return h == 0;
+}
+
+DTensor ones(std::vector<int> shape) {
+  DTensor t(std::move(shape));
+  dfill(t.p, 1.0, t.size());
+  return t;
+}
+
+// -- interface recurrences (tt_solver.py:98-151) -----------------------------
+
+DTensor step_a_left(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
+  DTensor t = tensordot(phi, {0}, xc, {0});    // (a, z, m, X)
+  t = tensordot(t, {0, 2}, ac, {0, 1});        // (z, X, n, A)
+  return tensordot(t, {0, 2}, xc, {0, 1});     // (X, A, Z)
+}
+
+DTensor step_a_right(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
+  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, m, A, Z)
+  t = tensordot(ac, {1, 3}, t, {1, 2});        // (a, n, x, Z)
+  t = tensordot(t, {1, 3}, xc, {1, 2});        // (a, x, z)
+  return permute(t, {1, 0, 2});
+}
+
+DTensor step_n_left(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
+  DTensor t = tensordot(phi, {0}, xc, {0});    // (a1, a2, z, n1, X)
+  t = tensordot(t, {0, 3}, ac, {0, 2});        // (a2, z, X, k, A1)
+  t = tensordot(t, {0, 3}, ac, {0, 1});        // (z, X, A1, n2, A2)
+  return tensordot(t, {0, 3}, xc, {0, 1});     // (X, A1, A2, Z)
+}
+
+DTensor step_n_right(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
+  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, n1, A1, A2, Z)
+  t = tensordot(ac, {2, 3}, t, {1, 2});        // (a1, k, x, A2, Z)
+  t = tensordot(ac, {1, 3}, t, {1, 3});        // (a2, n2, a1, x, Z)
+  t = tensordot(t, {1, 4}, xc, {1, 2});        // (a2, a1, x, z)
+  return permute(t, {2, 1, 0, 3});
+}
+
+DTensor step_g_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
+  DTensor t = tensordot(phi, {0}, xc, {0});    // (a, b, n, X)
+  t = tensordot(t, {0, 2}, ac, {0, 2});        // (b, X, k, A)
+  return tensordot(t, {0, 2}, bc, {0, 1});     // (X, A, B)
+}
+
+DTensor step_g_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
+  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, n, A, B)
+  t = tensordot(ac, {2, 3}, t, {1, 2});        // (a, k, x, B)
+  t = tensordot(t, {1, 3}, bc, {1, 2});        // (a, x, b)
+  return permute(t, {1, 0, 2});
+}
+
+DTensor step_b_left(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
+  DTensor t = tensordot(phi, {0}, xc, {0});    // (b, m, X)
+  return tensordot(t, {0, 1}, bc, {0, 1});     // (X, B)
+}
+
+DTensor step_b_right(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
+  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, m, B)
+  return tensordot(t, {1, 2}, bc, {1, 2});     // (x, b)
+}
+
+// -- local systems (tt_solver.py:155-246) -------------------------------------
+
+DTensor galerkin_rhs(const DTensor& pbl, const DTensor& bc, const DTensor& pbr) {
+  DTensor t = tensordot(pbl, {1}, bc, {0});    // (x, m, c)
+  return tensordot(t, {2}, pbr, {1});          // (x, m, y)
+}
+
+DTensor normal_rhs(const DTensor& pgl, const DTensor& ac, const DTensor& bc, const DTensor& pgr) {
+  DTensor t = tensordot(pgl, {2}, bc, {0});    // (x, a, k, B)
+  t = tensordot(t, {1, 2}, ac, {0, 1});        // (x, B, m, A)
+  return tensordot(t, {1, 3}, pgr, {2, 1});    // (x, m, y)
+}
+
+DTensor normal_apply(const DTensor& pnl, const DTensor& ac, const DTensor& pnr, const DTensor& u) {
+  DTensor t = tensordot(pnl, {3}, u, {0});     // (x, a1, a2, n, w)
+  t = tensordot(t, {2, 3}, ac, {0, 2});        // (x, a1, w, k, A2)
+  t = tensordot(t, {1, 3}, ac, {0, 1});        // (x, w, A2, m, A1)
+  return tensordot(t, {1, 4, 2}, pnr, {3, 1, 2});  // (x, m, y)
+}
+
+// Column-major normal-equation block N[(x,m,y),(z,n,w)] (tt_solver.py:239-246).
+DTensor normal_matrix(const DTensor& pnl, const DTensor& ac, const DTensor& pnr) {
+  DTensor g = tensordot(ac, {1}, ac, {1});     // (a, m, P, b, n, Q)
+  DTensor t = tensordot(pnl, {1, 2}, g, {0, 3});  // (x, z, m, P, n, Q)
+  t = tensordot(t, {3, 5}, pnr, {1, 2});       // (x, z, m, n, y, w)
+  return permute(t, {1, 3, 5, 0, 2, 4});       // (z, n, w | x, m, y): column-major
+}
+
+DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& par) {
+  const int rx = pal.dim(0), ra = pal.dim(1), n = ac.dim(1), rb = ac.dim(3), ry = par.dim(0);
+  const long long N = (long long)rx * n * ry;
+  DTensor B({(int)N, (int)N});
+  galerkin_matrix_kernel<<<grid_of(N * N), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
+                                                                par.p, B.p);
+  T2S2_CHECK_LAUNCH();
+  return B;
+}
+
+// Dense direct solve of a column-major N x N system; false if singular.
+bool dense_solve(DTensor& M, const DTensor& rhs, DTensor& out) {
+  const int N = M.dim(0);
+  int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
+  int* info = reinterpret_cast<int*>(allocator().alloc(1));
+  lu_factor(N, M.p, ipiv, info);
+  out = rhs.clone();
+  lu_solve(N, M.p, ipiv, out.p);
+  int h = 0;
+  T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  allocator().release(reinterpret_cast<double*>(ipiv));
+  allocator().release(reinterpret_cast<double*>(info));
+  return h == 0;
+}
+
+// -- splits with enrichment (tt_solver.py:261-302) ------------------------------
+
+struct Split {
+  DTensor core, carry;
+  int extra = 0;
+};
+
+std::vector<double> host_vec(const DTensor& s) {
+  std::vector<double> h(s.size());
+  to_host(h.data(), s.p, s.size());
+  return h;
+}
+
+double vec_norm(const std::vector<double>& s) {
+  double a = 0.0;
+  for (double v : s) a += v * v;
+  return std::sqrt(a);
+}
+
+int count_significant(const std::vector<double>& zs) {
+  const double lead = zs.empty() ? 0.0 : zs[0];
+  const double thr = 1e-14 * (lead > 1e-300 ? lead : 1e-300);
+  int nz = 0;
+  for (double v : zs) nz += v > thr;
+  return nz;
+}
+
+Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& cfg, int d) {
+  const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
+  DTensor U, s, Vt;
+  svd_thin(m, r1, u.p, U, s, Vt);
+  const int kk = s.dim(0);
+  std::vector<double> hs = host_vec(s);
+  const double delta = cfg.rounding_tol * vec_norm(hs) / std::sqrt((double)(d - 1 > 1 ? d - 1 : 1));
+  int keep = tail_keep(hs, delta);
+  if (keep > cfg.max_rank) keep = cfg.max_rank;
+  Split out;
+  out.carry = DTensor({keep, r1});
+  dcopy(out.carry.p, Vt.p, (size_t)keep * r1);
+  scale_rows(out.carry.p, keep, r1, r1, s.p);
+  DTensor zu;
+  int zk = 0;
+  if (cfg.enrichment_rank > 0 && keep < cfg.max_rank && grad) {
+    DTensor basis({m, keep});
+    copy2d(basis.p, keep, U.p, kk, m, keep);
+    const int gc = (int)(grad->size() / m);
+    DTensor z = grad->clone();
+    DTensor tmp({keep, gc});
+    gemm(true, false, keep, gc, m, 1.0, basis.p, keep, z.p, gc, 0.0, tmp.p, gc);
+    gemm(false, false, m, gc, keep, -1.0, basis.p, keep, tmp.p, gc, 1.0, z.p, gc);
+    DTensor zs, zvt;
+    svd_thin(m, gc, z.p, zu, zs, zvt);
+    zk = zs.dim(0);
+    std::vector<double> hz = host_vec(zs);
+    int nz = count_significant(hz);
+    int extra = cfg.enrichment_rank;
+    if (cfg.max_rank - keep < extra) extra = cfg.max_rank - keep;
+    if (nz < extra) extra = nz;
+    out.extra = extra > 0 ? extra : 0;
+  }
+  out.core = DTensor({r0, n, keep + out.extra});
+  copy2d(out.core.p, keep + out.extra, U.p, kk, m, keep);
+  if (out.extra > 0) copy2d(out.core.p + keep, keep + out.extra, zu.p, zk, m, out.extra);
+  return out;
+}
+
+Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& cfg, int d) {
+  const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), cols = n * r1;
+  DTensor U, s, Vt;
+  svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
+  const int kk = s.dim(0);
+  std::vector<double> hs = host_vec(s);
+  const double delta = cfg.rounding_tol * vec_norm(hs) / std::sqrt((double)(d - 1 > 1 ? d - 1 : 1));
+  int keep = tail_keep(hs, delta);
+  if (keep > cfg.max_rank) keep = cfg.max_rank;
+  Split out;
+  out.carry = DTensor({r0, keep});
+  copy2d(out.carry.p, keep, U.p, kk, r0, keep);
+  scale_cols(out.carry.p, r0, keep, keep, s.p);
+  DTensor zvt;
+  if (cfg.enrichment_rank > 0 && keep < cfg.max_rank && grad) {
+    const int gr = (int)(grad->size() / cols);
+    DTensor z = grad->clone();
+    DTensor tmp({gr, keep});
+    gemm(false, true, gr, keep, cols, 1.0, z.p, cols, Vt.p, cols, 0.0, tmp.p, keep);
+    gemm(false, false, gr, cols, keep, -1.0, tmp.p, keep, Vt.p, cols, 1.0, z.p, cols);
+    DTensor zu, zs;
+    svd_thin(gr, cols, z.p, zu, zs, zvt);
+    std::vector<double> hz = host_vec(zs);
+    int nz = count_significant(hz);
+    int extra = cfg.enrichment_rank;
+    if (cfg.max_rank - keep < extra) extra = cfg.max_rank - keep;
+    if (nz < extra) extra = nz;
+    out.extra = extra > 0 ? extra : 0;
+  }
+  out.core = DTensor({keep + out.extra, n, r1});
+  dcopy(out.core.p, Vt.p, (size_t)keep * cols);
+  if (out.extra > 0) dcopy(out.core.p + (size_t)keep * cols, zvt.p, (size_t)out.extra * cols);
+  return out;
+}
+
+// -- residual (tt_solver.py:305-329) ----------------------------------------------
+
+double measure_residual(const Train& A, const std::vector<DTensor>& x, const Train& rhs,
+                        double bnorm) {
+  const int d = A.d();
+  DTensor phi = ones({1, 1, 1, 1});
+  for (int l = 0; l < d; ++l) phi = step_n_left(phi, x[l], A.cores[l]);
+  const double axax = scalar_to_host(phi.p);
+  DTensor psi = ones({1, 1, 1});
+  for (int l = 0; l < d; ++l) psi = step_g_left(psi, x[l], A.cores[l], rhs.cores[l]);
+  const double axb = scalar_to_host(psi.p);
+  const double est_sq = axax - 2.0 * axb + bnorm * bnorm;
+  const double est = std::sqrt(est_sq > 0.0 ? est_sq : 0.0) / bnorm;
+  if (est_sq <= 0.0 || est < 1e-6) {
+    Train xt;
+    xt.rows = rhs.rows;
+    for (auto& c : x) xt.cores.push_back(c.clone());
+    Train diff = tt_add(tt_apply(A, xt), rhs, 1.0, -1.0);
+    return tt_norm(diff) / bnorm;
+  }
+  return est;
+}
+
+// -- sweep state -------------------------------------------------------------------
+
+struct Sweep {
+  const Train& A;
+  const Train& rhs;
+  const SolverConfig& cfg;
+  int d;
+  int gal_rejects = 0;
+  int gal_cap;
+  std::vector<DTensor> la, ln, lg, lb, ra, rn, rg, rb;
+  Sweep(const Train& a, const Train& b, const SolverConfig& c)
+      : A(a), rhs(b), cfg(c), d(a.d()), gal_cap(2 * a.d()),
+        la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1) {}
+
+  double score(const DTensor& u, const DTensor& nu, const DTensor& c_ls) {
+    // u^T N u - 2 c^T u (tt_solver.py:332-334)
+    return ddot(u.p, nu.p, u.size()) - 2.0 * ddot(c_ls.p, u.p, u.size());
+  }
+
+  // Guarded update of core l (tt_solver.py:337-422).
+  void update(int l, std::vector<DTensor>& cores, double current_res, DTensor& best,
+              DTensor& grad, int& choice) {
+    const DTensor& ac = A.cores[l];
+    const DTensor& bc = rhs.cores[l];
+    const DTensor& u_old = cores[l];
+    const long long size = (long long)u_old.size();
+    DTensor c_gal = galerkin_rhs(lb[l], bc, rb[l + 1]);
+    DTensor c_ls = normal_rhs(lg[l], ac, bc, rg[l + 1]);
+    DTensor nu_old = normal_apply(ln[l], ac, rn[l + 1], u_old);
+    const double q_old = score(u_old, nu_old, c_ls);
+    const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
+    T2S2_REQUIRE(direct, kErrCapacity,
+                 "local system of size " + std::to_string(size) +
+                     " exceeds local_direct_size; iterative local solver not available");
+    const bool try_gal = gal_rejects < gal_cap;
+    bool have_gal = false;
+    DTensor u_gal;
+    if (try_gal) {
+      DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+      have_gal = dense_solve(B, c_gal, u_gal);
+      if (have_gal) have_gal = all_finite(u_gal);
+    }
+    double best_q = q_old;
+    choice = 0;
+    DTensor nu_best;
+    if (have_gal) {
+      u_gal.view(u_old.shape);
+      DTensor nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
+      const double q_gal = score(u_gal, nu_gal, c_ls);
+      if (q_gal <= best_q) {
+        best_q = q_gal;
+        choice = 1;
+        best = std::move(u_gal);
+        nu_best = std::move(nu_gal);
+        gal_rejects = 0;
+      } else if (try_gal) {
+        gal_rejects += 1;
+      }
+    }
+    if (choice == 0) {
+      DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
+      Nm.view({(int)size, (int)size});
+      DTensor u_ls;
+      bool ok = dense_solve(Nm, c_ls, u_ls);
+      if (ok && all_finite(u_ls)) {
+        u_ls.view(u_old.shape);
+        DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
+        const double q_ls = score(u_ls, nu_ls, c_ls);
+        if (q_ls <= best_q) {
+          best_q = q_ls;
+          choice = 2;
+          best = std::move(u_ls);
+          nu_best = std::move(nu_ls);
+        }
+      }
+    }
+    if (choice == 0) {
+      best = u_old.clone();
+      nu_best = std::move(nu_old);
+    }
+    // projected residual gradient N u - c steers the enrichment
+    grad = std::move(nu_best);
+    daxpy(-1.0, c_ls.p, grad.p, grad.size());
+  }
+};
+
+}  // namespace
+
+Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverConfig& cfg,
+                SolveReport& rep) {
+  T2S2_REQUIRE(A.is_op() && !rhs.is_op() && A.cols == rhs.rows && A.rows == rhs.rows, kErrShape,
+               "operator and right-hand side shapes do not match");
+  T2S2_REQUIRE(x0.rows == rhs.rows, kErrShape, "initial guess has wrong mode sizes");
+  auto t0 = std::chrono::steady_clock::now();
+  const double bnorm = tt_norm(rhs);
+  T2S2_REQUIRE(bnorm != 0.0, kErrValue, "rhs must be nonzero");
+  Train x = tt_round(x0, cfg.rounding_tol, cfg.max_rank);
+  const int d = x.d();
+  std::vector<DTensor> cores = std::move(x.cores);
+  double best_res = INFINITY;
+  std::vector<DTensor> best_cores;
+  for (auto& c : cores) best_cores.push_back(c.clone());
+  double current_res = 1.0;
+  Sweep sw(A, rhs, cfg);
+
+  for (int sweep = 0; sweep < cfg.max_sweeps; ++sweep) {
+    right_orthonormalize(cores);
+    sw.ra[d] = ones({1, 1, 1});
+    sw.rn[d] = ones({1, 1, 1, 1});
+    sw.rg[d] = ones({1, 1, 1});
+    sw.rb[d] = ones({1, 1});
+    for (int l = d - 1; l > 0; --l) {
+      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l]);
+      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l]);
+      sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
+      sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
+    }
+    sw.la[0] = ones({1, 1, 1});
+    sw.ln[0] = ones({1, 1, 1, 1});
+    sw.lg[0] = ones({1, 1, 1});
+    sw.lb[0] = ones({1, 1});
+
+    for (int l = 0; l < d; ++l) {
+      DTensor u, grad;
+      int choice;
+      sw.update(l, cores, current_res, u, grad, choice);
+      rep.choices.push_back(choice);
+      if (l == d - 1) {
+        cores[l] = std::move(u);
+        break;
+      }
+      Split sp = split_forward(u, &grad, cfg, d);
+      cores[l] = std::move(sp.core);
+      const DTensor& nx = cores[l + 1];
+      const int keep = sp.carry.dim(0), r1 = sp.carry.dim(1);
+      const int rest = (int)(nx.size() / r1);
+      DTensor nn({keep + sp.extra, nx.dim(1), nx.dim(2)});
+      gemm(false, false, keep, rest, r1, 1.0, sp.carry.p, r1, nx.p, rest, 0.0, nn.p, rest);
+      if (sp.extra > 0) dfill(nn.p + (size_t)keep * rest, 0.0, (size_t)sp.extra * rest);
+      cores[l + 1] = std::move(nn);
+      sw.la[l + 1] = step_a_left(sw.la[l], cores[l], A.cores[l]);
+      sw.ln[l + 1] = step_n_left(sw.ln[l], cores[l], A.cores[l]);
+      sw.lg[l + 1] = step_g_left(sw.lg[l], cores[l], A.cores[l], rhs.cores[l]);
+      sw.lb[l + 1] = step_b_left(sw.lb[l], cores[l], rhs.cores[l]);
+    }
+    for (int l = d - 1; l >= 0; --l) {
+      DTensor u, grad;
+      int choice;
+      sw.update(l, cores, current_res, u, grad, choice);
+      rep.choices.push_back(choice);
+      if (l == 0) {
+        cores[l] = std::move(u);
+        break;
+      }
+      Split sp = split_backward(u, &grad, cfg, d);
+      cores[l] = std::move(sp.core);
+      const DTensor& pv = cores[l - 1];
+      const int r0 = sp.carry.dim(0), keep = sp.carry.dim(1);
+      const int rows = (int)(pv.size() / r0);
+      const int nk = keep + sp.extra;
+      DTensor np({pv.dim(0), pv.dim(1), nk});
+      if (sp.extra > 0) dfill(np.p, 0.0, np.size());
+      gemm(false, false, rows, keep, r0, 1.0, pv.p, r0, sp.carry.p, keep, 0.0, np.p, nk);
+      cores[l - 1] = std::move(np);
+      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l]);
+      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l]);
+      sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
+      sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
+    }
+    current_res = measure_residual(A, cores, rhs, bnorm);
+    rep.residuals.push_back(current_res);
+    int mr = 1;
+    double stored = 0.0, dense = 1.0;
+    for (int l = 0; l < d; ++l) {
+      mr = cores[l].dim(-1) > mr ? cores[l].dim(-1) : mr;
+      stored += (double)cores[l].size();
+      dense *= (double)cores[l].dim(1);
+    }
+    rep.ranks.push_back(mr);
+    rep.compression.push_back(stored / dense);
+    if (current_res < best_res) {
+      best_res = current_res;
+      best_cores.clear();
+      for (auto& c : cores) best_cores.push_back(c.clone());
+    }
+    if (current_res <= cfg.residual_tol) {
+      rep.converged = true;
+      break;
+    }
+    const int w = cfg.stagnation_window;
+    const int nh = (int)rep.residuals.size();
+    if (nh > w) {
+      double past = INFINITY, now = INFINITY;
+      for (int i = 0; i < nh; ++i) {
+        if (i < nh - w) past = rep.residuals[i] < past ? rep.residuals[i] : past;
+        now = rep.residuals[i] < now ? rep.residuals[i] : now;
+      }
+      const double denom = past > 1e-300 ? past : 1e-300;
+      if (past <= 0.0 || (past - now) / denom < cfg.stagnation_drop) {
+        rep.stagnated = true;
+        break;
+      }
+    }
+  }
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  Train out;
+  out.rows = rhs.rows;
+  out.cores = std::move(best_cores);
+  return out;
+}
+
+double tt_residual(const Train& A, const Train& x, const Train& rhs, double tol) {
+  const double bnorm = tt_norm(rhs);
+  T2S2_REQUIRE(bnorm != 0.0, kErrValue, "rhs must be nonzero");
+  Train diff = tt_round(tt_add(tt_apply(A, x), rhs, 1.0, -1.0), 0.01 * tol, 0);
+  return tt_norm(diff) / bnorm;
+}
+
+}  // namespace t2s2

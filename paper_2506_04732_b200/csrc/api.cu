@@ -1,0 +1,334 @@
+// C ABI of the engine (include/t2s2.h): context management, train
+// upload/download and the hot-path entry points.
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "../../include/t2s2.h"
+#include "als.h"
+#include "blas.h"
+#include "tt.h"
+
+struct t2s2_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  t2s2::Allocator alloc;
+  std::string last_error;
+};
+
+struct t2s2_train {
+  t2s2_context* ctx = nullptr;  // owner: buffers are freed on its stream
+  t2s2::Train t;
+};
+
+namespace t2s2 {
+namespace {
+thread_local t2s2_context* g_ctx = nullptr;
+
+struct Bind {  // makes ctx current for the duration of an API call
+  t2s2_context* prev;
+  explicit Bind(t2s2_context* c) : prev(g_ctx) {
+    g_ctx = c;
+    cudaSetDevice(c->device);
+  }
+  ~Bind() { g_ctx = prev; }
+};
+}  // namespace
+
+Allocator& allocator() { return g_ctx->alloc; }
+cudaStream_t stream() { return g_ctx->stream; }
+
+}  // namespace t2s2
+
+using namespace t2s2;
+
+namespace {
+
+template <class F>
+int guarded(t2s2_context* ctx, F&& f) {
+  if (!ctx) return T2S2_ERR_ARG;
+  Bind b(ctx);
+  try {
+    f();
+    return T2S2_OK;
+  } catch (const Error& e) {
+    ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->last_error = e.what();
+    return T2S2_ERR_ARG;
+  }
+}
+
+Train make_train(int d, const int* rows, const int* cols, const int* ranks, const double* src,
+                 cudaMemcpyKind kind) {
+  T2S2_REQUIRE(d >= 1 && rows && ranks && src, kErrArg, "bad train arguments");
+  T2S2_REQUIRE(ranks[0] == 1 && ranks[d] == 1, kErrShape, "boundary ranks must be 1");
+  Train t;
+  size_t off = 0;
+  for (int l = 0; l < d; ++l) {
+    T2S2_REQUIRE(rows[l] >= 1 && ranks[l] >= 1 && ranks[l + 1] >= 1 && (!cols || cols[l] >= 1),
+                 kErrShape, "mode sizes and ranks must be positive");
+    t.rows.push_back(rows[l]);
+    std::vector<int> shape = cols ? std::vector<int>{ranks[l], rows[l], cols[l], ranks[l + 1]}
+                                  : std::vector<int>{ranks[l], rows[l], ranks[l + 1]};
+    if (cols) t.cols.push_back(cols[l]);
+    DTensor c(shape);
+    T2S2_CUDA(cudaMemcpyAsync(c.p, src + off, c.size() * sizeof(double), kind, stream()));
+    off += c.size();
+    t.cores.push_back(std::move(c));
+  }
+  return t;
+}
+
+t2s2_train* wrap(Train&& t) {
+  auto* h = new t2s2_train;
+  h->ctx = g_ctx;
+  h->t = std::move(t);
+  return h;
+}
+
+SolverConfig to_cfg(const t2s2_solver_config* c) {
+  SolverConfig s;
+  if (!c) return s;
+  s.max_sweeps = c->max_sweeps;
+  s.residual_tol = c->residual_tol;
+  s.rounding_tol = c->rounding_tol;
+  s.enrichment_rank = c->enrichment_rank;
+  s.max_rank = c->max_rank;
+  s.local_solver = c->local_solver;
+  s.local_direct_size = c->local_direct_size;
+  s.inner_tol_factor = c->inner_tol_factor;
+  s.stagnation_window = c->stagnation_window;
+  s.stagnation_drop = c->stagnation_drop;
+  T2S2_REQUIRE(s.residual_tol > 0 && s.rounding_tol > 0, kErrValue, "tolerances must be positive");
+  T2S2_REQUIRE(s.max_rank >= 1, kErrValue, "max_rank must be at least 1");
+  T2S2_REQUIRE(s.max_sweeps >= 1 && s.max_sweeps <= T2S2_MAX_SWEEPS, kErrValue,
+               "max_sweeps out of range");
+  return s;
+}
+
+void fill_report(const SolveReport& r, t2s2_solve_report* out) {
+  if (!out) return;
+  out->n_sweeps = (int)r.residuals.size();
+  for (int i = 0; i < out->n_sweeps; ++i) {
+    out->residuals[i] = r.residuals[i];
+    out->ranks[i] = r.ranks[i];
+    out->compression[i] = r.compression[i];
+  }
+  out->wall_time = r.wall_time;
+  out->converged = r.converged;
+  out->stagnated = r.stagnated;
+}
+
+}  // namespace
+
+extern "C" {
+
+int t2s2_context_create(int device, t2s2_context** out) {
+  if (!out) return T2S2_ERR_ARG;
+  auto ctx = std::make_unique<t2s2_context>();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) return T2S2_ERR_CUDA;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return T2S2_ERR_CUDA;
+  ctx->alloc.stream = ctx->stream;
+  // keep freed blocks in the pool between calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = ctx.release();
+  return T2S2_OK;
+}
+
+void t2s2_context_destroy(t2s2_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* t2s2_last_error(const t2s2_context* ctx) {
+  return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+int t2s2_synchronize(t2s2_context* ctx) {
+  return guarded(ctx, [&] { T2S2_CUDA(cudaStreamSynchronize(stream())); });
+}
+
+int t2s2_train_upload(t2s2_context* ctx, int d, const int* rows, const int* cols,
+                      const int* ranks, const double* host_cores, t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(out, kErrArg, "null output");
+    *out = wrap(make_train(d, rows, cols, ranks, host_cores, cudaMemcpyHostToDevice));
+  });
+}
+
+int t2s2_train_upload_device(t2s2_context* ctx, int d, const int* rows, const int* cols,
+                             const int* ranks, const double* device_cores, t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(out, kErrArg, "null output");
+    *out = wrap(make_train(d, rows, cols, ranks, device_cores, cudaMemcpyDeviceToDevice));
+  });
+}
+
+int t2s2_train_shape(const t2s2_train* h, int* d, int* rows, int* cols, int* ranks,
+                     size_t* n_entries) {
+  if (!h) return T2S2_ERR_ARG;
+  const Train& t = h->t;
+  if (d) *d = t.d();
+  size_t n = 0;
+  for (int l = 0; l < t.d(); ++l) {
+    if (rows) rows[l] = t.rows[l];
+    if (cols) cols[l] = t.is_op() ? t.cols[l] : 0;
+    n += t.cores[l].size();
+  }
+  if (ranks)
+    for (int l = 0; l <= t.d(); ++l) ranks[l] = t.rank(l);
+  if (n_entries) *n_entries = n;
+  return T2S2_OK;
+}
+
+int t2s2_train_download(t2s2_context* ctx, const t2s2_train* h, double* host_cores,
+                        size_t capacity) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(h && host_cores, kErrArg, "null argument");
+    size_t off = 0;
+    for (auto& c : h->t.cores) {
+      T2S2_REQUIRE(off + c.size() <= capacity, kErrCapacity, "download buffer too small");
+      T2S2_CUDA(cudaMemcpyAsync(host_cores + off, c.p, c.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, stream()));
+      off += c.size();
+    }
+    T2S2_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+void t2s2_train_free(t2s2_train* t) {
+  if (!t) return;
+  Bind b(t->ctx);
+  delete t;
+}
+
+int t2s2_round(t2s2_context* ctx, const t2s2_train* v, double tol, int max_rank,
+               t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(v && out, kErrArg, "null argument");
+    *out = wrap(tt_round(v->t, tol, max_rank));
+  });
+}
+
+int t2s2_norm(t2s2_context* ctx, const t2s2_train* v, double* out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(v && out, kErrArg, "null argument");
+    *out = tt_norm(v->t);
+  });
+}
+
+int t2s2_dot(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* b, double* out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(a && b && out, kErrArg, "null argument");
+    *out = tt_dot(a->t, b->t);
+  });
+}
+
+int t2s2_add(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* b, double sa, double sb,
+             t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(a && b && out, kErrArg, "null argument");
+    *out = wrap(tt_add(a->t, b->t, sa, sb));
+  });
+}
+
+int t2s2_scale(t2s2_context* ctx, const t2s2_train* a, double s, t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(a && out, kErrArg, "null argument");
+    *out = wrap(tt_scale(a->t, s));
+  });
+}
+
+int t2s2_apply(t2s2_context* ctx, const t2s2_train* op, const t2s2_train* v, t2s2_train** out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(op && v && out, kErrArg, "null argument");
+    *out = wrap(tt_apply(op->t, v->t));
+  });
+}
+
+int t2s2_full(t2s2_context* ctx, const t2s2_train* v, double* host_dense, size_t capacity) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(v && host_dense, kErrArg, "null argument");
+    tt_full(v->t, host_dense, capacity);
+  });
+}
+
+int t2s2_solve(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* rhs,
+               const t2s2_train* x0, const t2s2_solver_config* cfg, t2s2_train** x,
+               t2s2_solve_report* report) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(a && rhs && x0 && x, kErrArg, "null argument");
+    SolveReport rep;
+    Train sol = als_solve(a->t, rhs->t, x0->t, to_cfg(cfg), rep);
+    fill_report(rep, report);
+    *x = wrap(std::move(sol));
+  });
+}
+
+int t2s2_residual(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* x,
+                  const t2s2_train* rhs, double tol, double* out) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(a && x && rhs && out, kErrArg, "null argument");
+    *out = tt_residual(a->t, x->t, rhs->t, tol);
+  });
+}
+
+int t2s2_march(t2s2_context* ctx, const t2s2_train* left, const t2s2_train* right,
+               const t2s2_train* state0, int n_steps, const t2s2_train* const* bc,
+               const t2s2_train* const* src, int n_forcing, double step_tol,
+               const t2s2_solver_config* cfg, int store_stride, t2s2_train** states_out,
+               t2s2_step_report* reports, int* failed_step) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(left && right && state0, kErrArg, "null argument");
+    T2S2_REQUIRE(n_steps >= 1, kErrValue, "need at least one step");
+    T2S2_REQUIRE(n_forcing == 1 || n_forcing == n_steps, kErrArg,
+                 "n_forcing must be 1 or n_steps");
+    T2S2_REQUIRE(step_tol > 0, kErrValue, "step rounding tolerance must be positive");
+    const SolverConfig sc = to_cfg(cfg);
+    if (failed_step) *failed_step = 0;
+    Train state = state0->t.clone();
+    if (states_out)
+      for (int k = 0; k < n_steps; ++k) states_out[k] = nullptr;
+    for (int k = 1; k <= n_steps; ++k) {
+      const int f = n_forcing == 1 ? 0 : k - 1;
+      Train rhs = tt_apply(right->t, state);
+      if (bc && bc[f]) rhs = tt_add(rhs, bc[f]->t);
+      if (src && src[f]) rhs = tt_add(rhs, src[f]->t);
+      rhs = tt_round(rhs, 0.01 * step_tol, 0);
+      SolveReport rep;
+      Train nxt = als_solve(left->t, rhs, state, sc, rep);
+      double achieved = INFINITY;
+      for (double r : rep.residuals) achieved = r < achieved ? r : achieved;
+      if (!rep.converged && achieved > 50.0 * sc.residual_tol) {
+        if (failed_step) *failed_step = k;
+        char msg[160];
+        snprintf(msg, sizeof msg, "step %d: inner solver stagnated at residual %.3e", k,
+                 achieved);
+        throw Error(kErrStagnation, msg);
+      }
+      state = tt_round(nxt, step_tol, 0);
+      if (reports) {
+        reports[k - 1].step = k;
+        reports[k - 1].max_rank = state.max_rank();
+        reports[k - 1].compression = compression_ratio(state);
+        reports[k - 1].residual = rep.residuals.back();
+        reports[k - 1].sweeps = (int)rep.residuals.size();
+      }
+      if (states_out && store_stride > 0 && (k % store_stride == 0 || k == n_steps))
+        states_out[k - 1] = wrap(state.clone());
+    }
+  });
+}
+
+}  // extern "C"

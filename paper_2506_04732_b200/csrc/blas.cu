@@ -1,0 +1,393 @@
+// Dense fp64 kernels: tiled GEMM (FFMA), permutation, vector ops and
+// deterministic reductions.
+#include "blas.h"
+
+#include <cmath>
+
+namespace t2s2 {
+
+// ---------------------------------------------------------------------------
+// GEMM: 64x64 output tile per CTA, BK = 16, 256 threads, 4x4 per thread.
+// Operands are staged through shared memory with bounds checks so the same
+// kernel serves the many tiny contractions of the sweep as well as the
+// larger trailing updates.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
+                                                   double alpha, const double* __restrict__ A,
+                                                   int lda, long long sA,
+                                                   const double* __restrict__ B, int ldb,
+                                                   long long sB, double beta, double* C, int ldc,
+                                                   long long sC) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN + 1];
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int e = threadIdx.x + t * 256;  // 0..1023
+      // A tile: BM x BK
+      int ar = e / BK, ak = e % BK;
+      int gi = row0 + ar, gk = k0 + ak;
+      double va = 0.0;
+      if (gi < M && gk < K) va = ta ? A[(long long)gk * lda + gi] : A[(long long)gi * lda + gk];
+      As[ak][ar] = va;
+      // B tile: BK x BN
+      int bk = e / BN, bc = e % BN;
+      int gk2 = k0 + bk, gj = col0 + bc;
+      double vb = 0.0;
+      if (gk2 < K && gj < N) vb = tb ? B[(long long)gj * ldb + gk2] : B[(long long)gk2 * ldb + gj];
+      Bs[bk][bc] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gi = row0 + ty + 16 * i;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gj = col0 + tx + 16 * j;
+      if (gj >= N) continue;
+      double* c = C + (long long)gi * ldc + gj;
+      *c = beta == 0.0 ? alpha * acc[i][j] : alpha * acc[i][j] + beta * (*c);
+    }
+  }
+}
+
+struct PermArgs {
+  int nd;
+  int out_shape[8];
+  long long in_stride[8];  // stride in the input of output axis k
+};
+
+__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out,
+                               long long n, PermArgs a) {
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n;
+       o += (long long)gridDim.x * blockDim.x) {
+    long long rem = o, off = 0;
+    for (int k = a.nd - 1; k >= 0; --k) {
+      int i = (int)(rem % a.out_shape[k]);
+      rem /= a.out_shape[k];
+      off += i * a.in_stride[k];
+    }
+    out[o] = in[off];
+  }
+}
+
+__global__ void fill_kernel(double* x, double v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = v;
+}
+
+__global__ void scal_kernel(double* x, double s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] *= s;
+}
+
+__global__ void axpby_kernel(double a, const double* x, double b, double* y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + b * y[i];
+}
+
+__global__ void copy2d_kernel(double* dst, int ldd, const double* src, int lds, int rows,
+                              int cols) {
+  long long n = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r = (int)(e / cols), c = (int)(e % cols);
+    dst[(long long)r * ldd + c] = src[(long long)r * lds + c];
+  }
+}
+
+// Block-level sum of one double per thread (blockDim multiple of 32).
+__device__ double block_sum(double v) {
+  __shared__ double warp_part[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) warp_part[w] = v;
+  __syncthreads();
+  int nw = blockDim.x >> 5;
+  v = lane < nw ? warp_part[lane] : 0.0;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // valid in warp 0
+}
+
+__global__ void dot_partial_kernel(const double* x, const double* y, long long n, double* part) {
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_final_kernel(const double* part, int n, double* out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void transpose_kernel(const double* in, double* out, int rows, int cols) {
+  long long n = (long long)rows * cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r = (int)(e / cols), c = (int)(e % cols);
+    out[(long long)c * rows + r] = in[e];
+  }
+}
+
+int grid_for(long long n, int threads = 256, int cap = 1184) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+
+void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                  long long sA, const double* B, int ldb, long long sB, double beta, double* C,
+                  int ldc, long long sC, int batch) {
+  if (M <= 0 || N <= 0 || batch <= 0) return;
+  if (K <= 0) {
+    // C = beta * C
+    for (int b = 0; b < batch; ++b)
+      for (int i = 0; i < M; ++i) {
+        if (beta == 0.0)
+          dfill(C + b * sC + (long long)i * ldc, 0.0, N);
+        else
+          dscal(C + b * sC + (long long)i * ldc, beta, N);
+      }
+    return;
+  }
+  dim3 grid(ceil_div(N, BN), ceil_div(M, BM), batch);
+  gemm_kernel<<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C,
+                                          ldc, sC);
+  T2S2_CHECK_LAUNCH();
+}
+
+void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+          const double* B, int ldb, double beta, double* C, int ldc) {
+  gemm_batched(ta, tb, M, N, K, alpha, A, lda, 0, B, ldb, 0, beta, C, ldc, 0, 1);
+}
+
+DTensor permute(const DTensor& a, const std::vector<int>& perm) {
+  int nd = a.ndim();
+  T2S2_REQUIRE((int)perm.size() == nd && nd <= 8, kErrShape, "permute: bad axes");
+  bool ident = true;
+  for (int k = 0; k < nd; ++k) ident = ident && perm[k] == k;
+  std::vector<int> os(nd);
+  for (int k = 0; k < nd; ++k) os[k] = a.shape[perm[k]];
+  DTensor out(os);
+  if (ident) {
+    dcopy(out.p, a.p, a.size());
+    return out;
+  }
+  std::vector<long long> st(nd);
+  long long s = 1;
+  for (int k = nd - 1; k >= 0; --k) {
+    st[k] = s;
+    s *= a.shape[k];
+  }
+  PermArgs pa{};
+  pa.nd = nd;
+  for (int k = 0; k < nd; ++k) {
+    pa.out_shape[k] = os[k];
+    pa.in_stride[k] = st[perm[k]];
+  }
+  long long n = (long long)a.size();
+  permute_kernel<<<grid_for(n), 256, 0, stream()>>>(a.p, out.p, n, pa);
+  T2S2_CHECK_LAUNCH();
+  return out;
+}
+
+DTensor tensordot(const DTensor& a, const std::vector<int>& axa, const DTensor& b,
+                  const std::vector<int>& axb) {
+  T2S2_REQUIRE(axa.size() == axb.size(), kErrShape, "tensordot: axis count mismatch");
+  int na = a.ndim(), nb = b.ndim();
+  std::vector<int> fa, fb, norm_a, norm_b;
+  std::vector<bool> ca(na, false), cb(nb, false);
+  long long K = 1;
+  for (size_t i = 0; i < axa.size(); ++i) {
+    int ia = axa[i] < 0 ? axa[i] + na : axa[i];
+    int ib = axb[i] < 0 ? axb[i] + nb : axb[i];
+    T2S2_REQUIRE(a.shape[ia] == b.shape[ib], kErrShape, "tensordot: contracted size mismatch");
+    ca[ia] = true;
+    cb[ib] = true;
+    norm_a.push_back(ia);
+    norm_b.push_back(ib);
+    K *= a.shape[ia];
+  }
+  long long M = 1, N = 1;
+  std::vector<int> out_shape;
+  for (int k = 0; k < na; ++k)
+    if (!ca[k]) {
+      fa.push_back(k);
+      M *= a.shape[k];
+      out_shape.push_back(a.shape[k]);
+    }
+  for (int k = 0; k < nb; ++k)
+    if (!cb[k]) {
+      fb.push_back(k);
+      N *= b.shape[k];
+      out_shape.push_back(b.shape[k]);
+    }
+  // A as (free, contracted) or, if already laid out (contracted, free), transposed.
+  std::vector<int> pa_fc = fa, pa_cf = norm_a;
+  pa_fc.insert(pa_fc.end(), norm_a.begin(), norm_a.end());
+  pa_cf.insert(pa_cf.end(), fa.begin(), fa.end());
+  std::vector<int> pb_cf = norm_b, pb_fc = fb;
+  pb_cf.insert(pb_cf.end(), fb.begin(), fb.end());
+  pb_fc.insert(pb_fc.end(), norm_b.begin(), norm_b.end());
+  auto is_id = [](const std::vector<int>& p) {
+    for (size_t k = 0; k < p.size(); ++k)
+      if (p[k] != (int)k) return false;
+    return true;
+  };
+  DTensor ta_buf, tb_buf;
+  const double* Ap;
+  const double* Bp;
+  bool transA = false, transB = false;
+  if (is_id(pa_fc)) {
+    Ap = a.p;
+  } else if (is_id(pa_cf)) {
+    Ap = a.p;
+    transA = true;
+  } else {
+    ta_buf = permute(a, pa_fc);
+    Ap = ta_buf.p;
+  }
+  if (is_id(pb_cf)) {
+    Bp = b.p;
+  } else if (is_id(pb_fc)) {
+    Bp = b.p;
+    transB = true;
+  } else {
+    tb_buf = permute(b, pb_cf);
+    Bp = tb_buf.p;
+  }
+  if (out_shape.empty()) out_shape.push_back(1);
+  DTensor out(out_shape);
+  int lda = transA ? (int)M : (int)K;
+  int ldb = transB ? (int)K : (int)N;
+  gemm(transA, transB, (int)M, (int)N, (int)K, 1.0, Ap, lda, Bp, ldb, 0.0, out.p, (int)N);
+  return out;
+}
+
+void transpose(const double* in, double* out, int rows, int cols) {
+  long long n = (long long)rows * cols;
+  if (n <= 0) return;
+  transpose_kernel<<<grid_for(n), 256, 0, stream()>>>(in, out, rows, cols);
+  T2S2_CHECK_LAUNCH();
+}
+
+void dcopy(double* dst, const double* src, size_t n) {
+  if (n) T2S2_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+}
+
+void dfill(double* dst, double v, size_t n) {
+  if (!n) return;
+  fill_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(dst, v, (long long)n);
+  T2S2_CHECK_LAUNCH();
+}
+
+void dscal(double* x, double s, size_t n) {
+  if (!n) return;
+  scal_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(x, s, (long long)n);
+  T2S2_CHECK_LAUNCH();
+}
+
+void daxpby(double a, const double* x, double b, double* y, size_t n) {
+  if (!n) return;
+  axpby_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(a, x, b, y, (long long)n);
+  T2S2_CHECK_LAUNCH();
+}
+
+void daxpy(double a, const double* x, double* y, size_t n) { daxpby(a, x, 1.0, y, n); }
+
+void copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
+  long long n = (long long)rows * cols;
+  if (n <= 0) return;
+  copy2d_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols);
+  T2S2_CHECK_LAUNCH();
+}
+
+void ddot_dev(const double* x, const double* y, size_t n, double* out) {
+  int g = grid_for((long long)n, 256, 296);
+  double* part = allocator().alloc(g);
+  dot_partial_kernel<<<g, 256, 0, stream()>>>(x, y, (long long)n, part);
+  sum_final_kernel<<<1, 256, 0, stream()>>>(part, g, out);
+  T2S2_CHECK_LAUNCH();
+  allocator().release(part);
+}
+
+double scalar_to_host(const double* d) {
+  double h = 0.0;
+  T2S2_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+double ddot(const double* x, const double* y, size_t n) {
+  double* o = allocator().alloc(1);
+  ddot_dev(x, y, n, o);
+  double h = scalar_to_host(o);
+  allocator().release(o);
+  return h;
+}
+
+double dnrm2(const double* x, size_t n) { return std::sqrt(ddot(x, x, n)); }
+
+void to_host(double* h, const double* d, size_t n) {
+  if (n) T2S2_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void to_device(double* d, const double* h, size_t n) {
+  if (n) T2S2_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, stream()));
+}
+
+DTensor DTensor::clone() const {
+  DTensor o(shape);
+  dcopy(o.p, p, size());
+  return o;
+}
+
+Train Train::clone() const {
+  Train t;
+  t.rows = rows;
+  t.cols = cols;
+  for (auto& c : cores) t.cores.push_back(c.clone());
+  return t;
+}
+
+}  // namespace t2s2

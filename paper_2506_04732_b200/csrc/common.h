@@ -1,0 +1,133 @@
+// Shared infrastructure of the T^2S^2 B200 engine: error handling, the
+// device tensor type, and the per-context stream/allocator.
+//
+// Everything numeric is fp64 and device resident.  Shapes are host-known:
+// the engine reads back the few integers that decide bond ranks (SVD
+// truncation, enrichment) and keeps every core, interface and local system
+// in HBM (or L2) between kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace t2s2 {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+enum ErrCode {
+  kOk = 0,
+  kErrArg = 1,
+  kErrCuda = 2,
+  kErrShape = 3,
+  kErrValue = 4,
+  kErrStagnation = 5,
+  kErrCapacity = 6,
+};
+
+#define T2S2_CUDA(call)                                                       \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      throw ::t2s2::Error(::t2s2::kErrCuda,                                   \
+                          std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define T2S2_CHECK_LAUNCH() T2S2_CUDA(cudaGetLastError())
+
+#define T2S2_REQUIRE(cond, code, msg)                  \
+  do {                                                 \
+    if (!(cond)) throw ::t2s2::Error((code), (msg));   \
+  } while (0)
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Stream-ordered device allocation (cudaMallocAsync on the context stream).
+struct Allocator {
+  cudaStream_t stream = nullptr;
+  double* alloc(size_t n) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    T2S2_CUDA(cudaMallocAsync(&p, n * sizeof(double), stream));
+    return static_cast<double*>(p);
+  }
+  void release(double* p) {
+    if (p) cudaFreeAsync(p, stream);
+  }
+};
+
+Allocator& allocator();  // the current context's allocator
+cudaStream_t stream();   // the current context's stream
+
+// A dense row-major device array with a host-known shape.  Owns its
+// buffer (move-only).
+struct DTensor {
+  double* p = nullptr;
+  std::vector<int> shape;
+
+  DTensor() = default;
+  explicit DTensor(std::vector<int> s) : shape(std::move(s)) { p = allocator().alloc(size()); }
+  DTensor(const DTensor&) = delete;
+  DTensor& operator=(const DTensor&) = delete;
+  DTensor(DTensor&& o) noexcept : p(o.p), shape(std::move(o.shape)) { o.p = nullptr; }
+  DTensor& operator=(DTensor&& o) noexcept {
+    if (this != &o) {
+      allocator().release(p);
+      p = o.p;
+      shape = std::move(o.shape);
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  ~DTensor() { allocator().release(p); }
+
+  size_t size() const {
+    size_t n = 1;
+    for (int s : shape) n *= (size_t)s;
+    return n;
+  }
+  int ndim() const { return (int)shape.size(); }
+  int dim(int i) const { return shape[i < 0 ? shape.size() + i : i]; }
+  // reshape in place (same element count)
+  DTensor& view(std::vector<int> s) {
+    size_t n = 1;
+    for (int v : s) n *= (size_t)v;
+    T2S2_REQUIRE(n == size(), kErrShape, "view: element count mismatch");
+    shape = std::move(s);
+    return *this;
+  }
+  DTensor clone() const;
+};
+
+// A train: d cores.  Vector cores are (r0, n, r1); operator cores are
+// (r0, m, n, r1).  Rows/cols record the mode sizes.
+struct Train {
+  std::vector<DTensor> cores;
+  std::vector<int> rows, cols;  // cols empty for vectors
+  bool is_op() const { return !cols.empty(); }
+  int d() const { return (int)cores.size(); }
+  int rank(int l) const {  // bond l in 0..d
+    if (l == 0) return 1;
+    return cores[l - 1].dim(-1);
+  }
+  std::vector<int> ranks() const {
+    std::vector<int> r(d() + 1);
+    for (int l = 0; l <= d(); ++l) r[l] = rank(l);
+    return r;
+  }
+  int max_rank() const {
+    int m = 1;
+    for (int l = 0; l <= d(); ++l) m = rank(l) > m ? rank(l) : m;
+    return m;
+  }
+  Train clone() const;
+};
+
+}  // namespace t2s2

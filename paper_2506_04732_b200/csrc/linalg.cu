@@ -1,0 +1,286 @@
+// Householder QR and one-sided Jacobi SVD for the small, tall matrices of
+// TT orthogonalisation and rounding (core unfoldings of size r*n x r).
+//
+// One CTA per factorisation: columns live contiguously (column-major
+// scratch, L1/L2 resident), one warp owns one column at a time, so a
+// Householder step needs two CTA barriers and a Jacobi round one.
+#include <cfloat>
+#include <cmath>
+
+#include "blas.h"
+#include "linalg.h"
+
+namespace t2s2 {
+namespace {
+
+constexpr int kQrThreads = 512;
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// A row-major (m x n) -> Q row-major (m x k), R row-major (k x n).
+// W: column-major m x n scratch, Qc: column-major m x k scratch, tau: k.
+__global__ void __launch_bounds__(kQrThreads)
+    qr_kernel(int m, int n, const double* __restrict__ A, double* W, double* Qc, double* tau,
+              double* Q, double* R) {
+  const int k = m < n ? m : n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  __shared__ double sh_tau, sh_scal, sh_beta;
+  for (long long e = tid; e < (long long)m * n; e += blockDim.x) {
+    int i = (int)(e / n), j = (int)(e % n);
+    W[(long long)j * m + i] = A[e];
+  }
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    double* v = W + (long long)j * m;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) s = fma(v[i], v[i], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        double alpha = v[j];
+        if (s == 0.0) {
+          sh_tau = 0.0;
+          sh_scal = 1.0;
+          sh_beta = alpha;
+        } else {
+          double nrm = sqrt(alpha * alpha + s);
+          double beta = alpha >= 0.0 ? -nrm : nrm;
+          sh_tau = (beta - alpha) / beta;
+          sh_scal = 1.0 / (alpha - beta);
+          sh_beta = beta;
+        }
+        tau[j] = sh_tau;
+      }
+    }
+    __syncthreads();
+    const double t = sh_tau, sc = sh_scal;
+    if (t != 0.0) {
+      for (int c = j + 1 + warp; c < n; c += nwarps) {
+        double* col = W + (long long)c * m;
+        double w = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) w = fma(v[i] * sc, col[i], w);
+        w = warp_sum(w) + col[j];
+        double tw = t * w;
+        if (lane == 0) col[j] -= tw;
+        for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i] * sc, col[i]);
+      }
+    }
+    __syncthreads();
+    if (t != 0.0) {
+      for (int i = j + 1 + tid; i < m; i += blockDim.x) v[i] *= sc;
+      if (tid == 0) v[j] = sh_beta;
+    }
+    __syncthreads();
+  }
+  // R
+  for (long long e = tid; e < (long long)k * n; e += blockDim.x) {
+    int r = (int)(e / n), c = (int)(e % n);
+    R[e] = c >= r ? W[(long long)c * m + r] : 0.0;
+  }
+  // Q = H_0 ... H_{k-1} [I_k; 0], accumulated backwards.
+  for (long long e = tid; e < (long long)m * k; e += blockDim.x) {
+    int c = (int)(e / m), i = (int)(e % m);
+    Qc[e] = i == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = k - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    const double* v = W + (long long)j * m;  // v_j = 1 implicit, v_i (i>j) stored
+    for (int c = j + warp; c < k; c += nwarps) {
+      double* col = Qc + (long long)c * m;
+      double w = 0.0;
+      for (int i = j + 1 + lane; i < m; i += 32) w = fma(v[i], col[i], w);
+      w = warp_sum(w) + col[j];
+      double tw = t * w;
+      if (lane == 0) col[j] -= tw;
+      for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i], col[i]);
+    }
+    __syncthreads();
+  }
+  for (long long e = tid; e < (long long)m * k; e += blockDim.x) {
+    int i = (int)(e / k), c = (int)(e % k);
+    Q[e] = Qc[(long long)c * m + i];
+  }
+}
+
+// One-sided (Hestenes) Jacobi on the columns of G (column-major p x q,
+// p >= q).  Circle-method ordering: each round rotates q/2 disjoint column
+// pairs, one warp per pair.  Outputs U (row-major p x q), s (q), Vt
+// (row-major q x q), singular values sorted descending.
+__global__ void __launch_bounds__(kQrThreads)
+    jacobi_kernel(int p, int q, double* G, double* V, int* perm, double* U, double* s,
+                  double* Vt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int sh_rot;
+  for (long long e = tid; e < (long long)q * q; e += blockDim.x) {
+    int c = (int)(e / q), i = (int)(e % q);
+    V[e] = i == c ? 1.0 : 0.0;
+  }
+  const double tol = DBL_EPSILON * sqrt((double)p);
+  const int qe = q + (q & 1);
+  __syncthreads();
+  for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+    if (tid == 0) sh_rot = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < qe - 1; ++rnd) {
+      for (int pi = warp; pi < qe / 2; pi += nwarps) {
+        int a, b;
+        if (pi == 0) {
+          a = qe - 1;
+          b = rnd;
+        } else {
+          a = (rnd + pi) % (qe - 1);
+          b = (rnd - pi + qe - 1) % (qe - 1);
+        }
+        if (a >= q || b >= q) continue;
+        if (a > b) {
+          int t = a;
+          a = b;
+          b = t;
+        }
+        double* ga = G + (long long)a * p;
+        double* gb = G + (long long)b * p;
+        double al = 0.0, be = 0.0, ga_b = 0.0;
+        for (int i = lane; i < p; i += 32) {
+          double x = ga[i], y = gb[i];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga_b = fma(x, y, ga_b);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga_b = warp_sum(ga_b);
+        if (ga_b == 0.0 || al == 0.0 || be == 0.0) continue;
+        if (fabs(ga_b) <= tol * sqrt(al) * sqrt(be)) continue;
+        double zeta = (be - al) / (2.0 * ga_b);
+        double t;
+        if (fabs(zeta) > 1e150)
+          t = 0.5 / zeta;
+        else
+          t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int i = lane; i < p; i += 32) {
+          double x = ga[i], y = gb[i];
+          ga[i] = c * x - sn * y;
+          gb[i] = sn * x + c * y;
+        }
+        double* va = V + (long long)a * q;
+        double* vb = V + (long long)b * q;
+        for (int i = lane; i < q; i += 32) {
+          double x = va[i], y = vb[i];
+          va[i] = c * x - sn * y;
+          vb[i] = sn * x + c * y;
+        }
+        if (lane == 0) sh_rot = 1;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!sh_rot) break;
+    __syncthreads();
+  }
+  // column norms -> s (unsorted, staged in s), then a stable descending order
+  for (int c = warp; c < q; c += nwarps) {
+    const double* g = G + (long long)c * p;
+    double acc = 0.0;
+    for (int i = lane; i < p; i += 32) acc = fma(g[i], g[i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) s[c] = sqrt(acc);
+  }
+  __syncthreads();
+  for (int c = tid; c < q; c += blockDim.x) {
+    double sc = s[c];
+    int rank = 0;
+    for (int o = 0; o < q; ++o) {
+      double so = s[o];
+      rank += (so > sc) || (so == sc && o < c);
+    }
+    perm[rank] = c;
+  }
+  __syncthreads();
+  double* sv = V + (long long)q * q;  // q extra doubles of scratch after V
+  for (int j = tid; j < q; j += blockDim.x) sv[j] = s[perm[j]];
+  __syncthreads();
+  for (int j = tid; j < q; j += blockDim.x) s[j] = sv[j];
+  __syncthreads();
+  for (long long e = tid; e < (long long)p * q; e += blockDim.x) {
+    int i = (int)(e / q), j = (int)(e % q);
+    double sj = s[j];
+    U[e] = sj > 0.0 ? G[(long long)perm[j] * p + i] / sj : 0.0;
+  }
+  for (long long e = tid; e < (long long)q * q; e += blockDim.x) {
+    int j = (int)(e / q), i = (int)(e % q);
+    Vt[e] = V[(long long)perm[j] * q + i];
+  }
+}
+
+}  // namespace
+
+void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
+  T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_thin: empty matrix");
+  const int k = m < n ? m : n;
+  Q = DTensor({m, k});
+  R = DTensor({k, n});
+  double* W = allocator().alloc((size_t)m * n);
+  double* Qc = allocator().alloc((size_t)m * k);
+  double* tau = allocator().alloc(k);
+  qr_kernel<<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+  T2S2_CHECK_LAUNCH();
+  allocator().release(W);
+  allocator().release(Qc);
+  allocator().release(tau);
+}
+
+namespace {
+
+// Jacobi SVD of a column-major p x q (p >= q) matrix held in G (clobbered).
+void jacobi_svd(int p, int q, double* G, DTensor& U, DTensor& s, DTensor& Vt) {
+  U = DTensor({p, q});
+  s = DTensor({q});
+  Vt = DTensor({q, q});
+  double* V = allocator().alloc((size_t)q * q + q);
+  int* perm = reinterpret_cast<int*>(allocator().alloc(q));
+  jacobi_kernel<<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+  T2S2_CHECK_LAUNCH();
+  allocator().release(V);
+  allocator().release(reinterpret_cast<double*>(perm));
+}
+
+// Tall case (m >= n): A = Q R, R = Ur S Vt, U = Q Ur.
+void svd_tall(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt) {
+  DTensor Q, R;
+  qr_thin(m, n, A, Q, R);  // Q m x n, R n x n
+  double* G = allocator().alloc((size_t)n * n);
+  transpose(R.p, G, n, n);  // column-major copy of R
+  DTensor Ur;
+  jacobi_svd(n, n, G, Ur, s, Vt);
+  allocator().release(G);
+  U = DTensor({m, n});
+  gemm(false, false, m, n, n, 1.0, Q.p, n, Ur.p, n, 0.0, U.p, n);
+}
+
+}  // namespace
+
+void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt) {
+  T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
+  if (m >= n) {
+    svd_tall(m, n, A, U, s, Vt);
+    return;
+  }
+  // A^T (n x m, tall) = U' S V'^T  =>  A = V' S U'^T
+  double* At = allocator().alloc((size_t)m * n);
+  transpose(A, At, m, n);
+  DTensor U2, Vt2;
+  svd_tall(n, m, At, U2, s, Vt2);  // U2 n x m, Vt2 m x m
+  allocator().release(At);
+  U = DTensor({m, m});
+  transpose(Vt2.p, U.p, m, m);
+  Vt = DTensor({m, n});
+  transpose(U2.p, Vt.p, n, m);
+}
+
+}  // namespace t2s2

@@ -1,0 +1,25 @@
+// Small dense factorisations for TT orthogonalisation, rounding and the
+// local solves: Householder QR, one-sided Jacobi SVD, LU with partial
+// pivoting.
+#pragma once
+
+#include "common.h"
+
+namespace t2s2 {
+
+// Thin QR of a row-major m x n matrix: Q (m x k, orthonormal columns) and
+// R (k x n, upper trapezoidal), k = min(m, n).  Householder reflectors in
+// the LAPACK dgeqrf/dorgqr convention.
+void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R);
+
+// Thin SVD A = U diag(s) Vt of a row-major m x n matrix, k = min(m, n),
+// singular values descending.  Tall case: QR, then one-sided Jacobi on R.
+void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt);
+
+// In-place LU with partial pivoting of a column-major N x N matrix (ld=N);
+// ipiv 0-based row swaps; *info_dev = 0 or 1 + first zero pivot column.
+void lu_factor(int N, double* A, int* ipiv, int* info_dev);
+// Solve with the factors for one right-hand side (in place).
+void lu_solve(int N, const double* LU, const int* ipiv, double* b);
+
+}  // namespace t2s2

@@ -1,0 +1,159 @@
+"""Parity of the CUDA path (through the C ABI) with the reference's outputs
+(tests/golden) and the CPU oracle.  Protocol: see tests/helpers.py."""
+
+import numpy as np
+import pytest
+
+from golden_io import get_train
+from helpers import numerical_ranks, rel_diff, value_tol
+from oracle import tt_ops as ot
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_2506_04732_b200 as pkg
+    from paper_2506_04732_b200 import _native, march, solver, tt
+
+    _native.context()  # fail loudly if the engine cannot start
+    return pkg, tt, solver, march
+
+
+def V(tt, cores):
+    return tt.TTVector(cores)
+
+
+def O(tt, cores):
+    return tt.TTOperator(cores)
+
+
+def test_round_matches_reference(golden, pk):
+    _, tt, _, _ = pk
+    z = golden("round.npz")
+    for i in range(int(z["count"])):
+        v, want = get_train(z, f"in{i}"), get_train(z, f"out{i}")
+        tol, cap = float(z[f"tol{i}"]), int(z[f"cap{i}"]) or None
+        got = tt.tt_round(V(tt, v), tol, max_rank=cap).cores
+        assert ot.ranks_of(got) == ot.ranks_of(want), (i, ot.ranks_of(got), ot.ranks_of(want))
+        assert rel_diff(got, want) <= 1e-12, i
+        nrm = tt.tt_norm(V(tt, v))
+        assert abs(nrm - float(z[f"norm{i}"])) <= 1e-13 * float(z[f"norm{i}"])
+
+
+def test_exact_arithmetic_matches_oracle(pk):
+    _, tt, _, _ = pk
+    rng = np.random.default_rng(5)
+    for modes, ra, rb in [((5, 6, 4), 3, 2), ((4, 4, 4, 4), 2, 5), ((7,), 1, 1), ((3, 9), 4, 4)]:
+        d = len(modes)
+        rka = [1] + [ra] * (d - 1) + [1]
+        rkb = [1] + [rb] * (d - 1) + [1]
+        a = [rng.standard_normal((rka[l], modes[l], rka[l + 1])) for l in range(d)]
+        b = [rng.standard_normal((rkb[l], modes[l], rkb[l + 1])) for l in range(d)]
+        op = [rng.standard_normal((2 if l else 1, modes[l], modes[l], 2 if l < d - 1 else 1))
+              for l in range(d)]
+        assert abs(tt.tt_dot(V(tt, a), V(tt, b)) - ot.tt_dot(a, b)) <= 1e-12 * (
+            ot.tt_norm(a) * ot.tt_norm(b))
+        s = tt.tt_add(V(tt, a), V(tt, b)).cores
+        assert ot.ranks_of(s) == ot.ranks_of(ot.tt_add(a, b))
+        np.testing.assert_allclose(tt.tt_full(V(tt, s)), ot.tt_full(a) + ot.tt_full(b),
+                                   rtol=1e-12, atol=1e-12 * np.abs(ot.tt_full(a)).max())
+        ap = tt.tt_apply(O(tt, op), V(tt, a)).cores
+        np.testing.assert_allclose(ot.tt_full(ap), ot.tt_full(ot.tt_apply(op, a)), rtol=1e-11,
+                                   atol=1e-11 * np.abs(ot.tt_full(ap)).max())
+        np.testing.assert_allclose(tt.tt_op_full(O(tt, op)), ot.tt_op_full(op), rtol=1e-12,
+                                   atol=1e-12)
+
+
+def _cfg(solver, z, tag):
+    kw = {k[len(tag) + 5:]: z[k].item() for k in z if k.startswith(f"{tag}_cfg_")}
+    return solver.SolverConfig(**kw)
+
+
+@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7"])
+def test_solve_small_matches_reference(golden, pk, tag):
+    _, tt, solver, _ = pk
+    z = golden("solve_small.npz")
+    a, b = O(tt, get_train(z, f"{tag}_a")), V(tt, get_train(z, f"{tag}_b"))
+    cfg = _cfg(solver, z, tag)
+    x, rep = solver.solve(a, b, cfg=cfg)
+    want = get_train(z, f"{tag}_x")
+    ref_res = np.array(z[f"{tag}_res"])
+    conv = bool(z[f"{tag}_conv"])
+    assert rep.converged == conv
+    assert rep.stagnated == bool(z[f"{tag}_stag"])
+    assert max(rep.rank_history) <= cfg.max_rank
+    if conv:
+        assert numerical_ranks(x.cores) == numerical_ranks(want)
+        assert rel_diff(x.cores, want) <= value_tol(rep.residual_history[-1], ref_res[-1])
+    else:
+        assert abs(rep.residual_history[-1] - ref_res[-1]) <= 5e-2 * ref_res[-1]
+
+
+def test_config0_matches_reference(golden, pk):
+    _, tt, solver, _ = pk
+    z = golden("config0.npz")
+    cfg = solver.SolverConfig(residual_tol=1e-10, rounding_tol=1e-12)
+    x, rep = solver.solve(O(tt, get_train(z, "a")), V(tt, get_train(z, "b")),
+                          x0=V(tt, get_train(z, "x0")), cfg=cfg)
+    want = get_train(z, "x")
+    assert rep.converged
+    assert numerical_ranks(x.cores) == numerical_ranks(want)
+    assert rel_diff(x.cores, want) <= value_tol(rep.residual_history[-1], z["res"][-1])
+
+
+@pytest.mark.parametrize("fname,steps", [("config2_small.npz", 5), ("config3_small.npz", 3),
+                                         ("config2_steps.npz", 3)])
+def test_march_matches_reference(golden, pk, fname, steps):
+    _, tt, solver, march = pk
+    z = golden(fname)
+    left, right = tt.to_device(O(tt, get_train(z, "left"))), tt.to_device(O(tt, get_train(z, "right")))
+    state = tt.to_device(V(tt, get_train(z, "state0")))
+    bcs = [tt.to_device(V(tt, get_train(z, f"bc{k}"))) for k in range(1, steps + 1)]
+    srcs = [tt.to_device(V(tt, get_train(z, f"src{k}"))) for k in range(1, steps + 1)]
+    cfg = solver.SolverConfig(residual_tol=1e-10, rounding_tol=1e-12, max_rank=64)
+    stored, rows = march.march_device(left, right, state, steps, bcs, srcs, 1e-12, cfg,
+                                      store_stride=1)
+    for k in range(1, steps + 1):
+        got = tt.from_device(stored[k]).cores
+        want = get_train(z, f"state{k}")
+        assert numerical_ranks(got) == numerical_ranks(want), k
+        assert rel_diff(got, want) <= k * value_tol(rows[k - 1][3], z[f"res{k}"][-1]), k
+    for h in [left, right, state] + bcs + srcs + list(stored.values()):
+        h.free()
+
+
+def test_errors_follow_reference(pk):
+    pkg, tt, solver, march = pk
+    rng = np.random.default_rng(1)
+    eye = tt.tt_identity_operator((3, 3))
+    zero = tt.tt_from_separable([(0.0, [np.ones(3), np.ones(3)])])
+    with pytest.raises(ValueError):
+        solver.solve(eye, zero)
+    v = tt.tt_random((3, 4), 2, rng)
+    with pytest.raises(pkg.ShapeError):
+        solver.solve(tt.tt_identity_operator((3, 5)), v)
+    with pytest.raises(ValueError):
+        tt.tt_round(v, -1.0)
+
+
+def test_identity_system_one_sweep(pk):
+    _, tt, solver, _ = pk
+    rng = np.random.default_rng(0)
+    v = tt.tt_random((5, 6, 4), 3, rng, norm=2.0)
+    x, rep = solver.solve(tt.tt_identity_operator((5, 6, 4)), v,
+                          cfg=solver.SolverConfig(residual_tol=1e-12))
+    assert rep.converged and rep.residual_history[-1] <= 1e-12
+    assert rel_diff(x.cores, v.cores) <= 1e-12
+
+
+def test_march_stagnation_raises_with_step(golden, pk):
+    pkg, tt, solver, march = pk
+    z = golden("config2_small.npz")
+    left, right = tt.to_device(O(tt, get_train(z, "left"))), tt.to_device(O(tt, get_train(z, "right")))
+    state = tt.to_device(V(tt, get_train(z, "state0")))
+    bc, src = tt.to_device(V(tt, get_train(z, "bc1"))), tt.to_device(V(tt, get_train(z, "src1")))
+    cfg = solver.SolverConfig(residual_tol=1e-30, max_rank=1, enrichment_rank=0, max_sweeps=8)
+    with pytest.raises(pkg.MarchStepError) as err:
+        march.march_device(left, right, state, 2, [bc], [src], 1e-12, cfg)
+    assert err.value.step == 1

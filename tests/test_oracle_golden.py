@@ -1,0 +1,85 @@
+"""Pin the CPU oracle against outputs of the reference itself
+(tests/golden/*.npz, produced by tools/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+from golden_io import get_train
+from helpers import numerical_ranks, rel_diff, same_ranks, value_tol
+from oracle import als_solver as als
+from oracle import march as om
+from oracle import tt_ops as ot
+
+
+def test_round_matches_reference(golden):
+    z = golden("round.npz")
+    for i in range(int(z["count"])):
+        v, want = get_train(z, f"in{i}"), get_train(z, f"out{i}")
+        tol, cap = float(z[f"tol{i}"]), int(z[f"cap{i}"]) or None
+        got = ot.tt_round(v, tol, max_rank=cap)
+        assert ot.ranks_of(got) == ot.ranks_of(want), i
+        assert rel_diff(got, want) <= 1e-12, i
+        assert abs(ot.tt_norm(v) - float(z[f"norm{i}"])) <= 1e-13 * float(z[f"norm{i}"])
+
+
+def _cfg(z, tag):
+    kw = {k[len(tag) + 5:]: z[k].item() for k in z if k.startswith(f"{tag}_cfg_")}
+    return als.Config(**kw)
+
+
+@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7"])
+def test_solve_small_matches_reference(golden, tag):
+    z = golden("solve_small.npz")
+    a, b, x0 = get_train(z, f"{tag}_a"), get_train(z, f"{tag}_b"), get_train(z, f"{tag}_x0")
+    cfg = _cfg(z, tag)
+    x, rep = als.solve(a, b, x0=x0, cfg=cfg)
+    want = get_train(z, f"{tag}_x")
+    conv = bool(z[f"{tag}_conv"])
+    assert rep.converged == conv
+    assert rep.stagnated == bool(z[f"{tag}_stag"])
+    ref_res = np.array(z[f"{tag}_res"])
+    if conv:
+        assert numerical_ranks(x) == numerical_ranks(want)
+        assert rel_diff(x, want) <= value_tol(rep.residual_history[-1], ref_res[-1])
+    else:
+        # Rank-capped, non-converging sweeps hinge on near-ties between the
+        # Galerkin and least-squares candidates; the reference itself varies
+        # run to run here.  Compare the plateau and the rank cap only.
+        assert max(rep.rank_history) <= cfg.max_rank
+        assert abs(rep.residual_history[-1] - ref_res[-1]) <= 5e-2 * ref_res[-1]
+
+
+def test_initial_guess_matches_reference(golden):
+    z = golden("solve_small.npz")
+    for tag in ["s1", "s2", "s3"]:
+        b = get_train(z, f"{tag}_b")
+        x0 = als.initial_guess(b, als.Config(), np.random.default_rng(0))
+        assert rel_diff(x0, get_train(z, f"{tag}_x0")) <= 1e-12
+
+
+def test_config0_matches_reference(golden):
+    z = golden("config0.npz")
+    cfg = als.Config(residual_tol=1e-10, rounding_tol=1e-12)
+    x, rep = als.solve(get_train(z, "a"), get_train(z, "b"), x0=get_train(z, "x0"), cfg=cfg)
+    want = get_train(z, "x")
+    assert rep.converged
+    assert numerical_ranks(x) == numerical_ranks(want)
+    assert rel_diff(x, want) <= value_tol(rep.residual_history[-1], z["res"][-1])
+
+
+@pytest.mark.parametrize("fname,steps", [("config2_small.npz", 5), ("config3_small.npz", 3),
+                                         ("config2_steps.npz", 2)])
+def test_march_matches_reference(golden, fname, steps):
+    z = golden(fname)
+    left, right = get_train(z, "left"), get_train(z, "right")
+    state = get_train(z, "state0")
+    cfg = als.Config(residual_tol=1e-10, rounding_tol=1e-12,
+                     max_rank=64)
+    for k in range(1, steps + 1):
+        state, rep, _ = om.step(left, right, state, get_train(z, f"bc{k}"),
+                                get_train(z, f"src{k}"), 1e-12, cfg, index=k)
+        want = get_train(z, f"state{k}")
+        assert numerical_ranks(state) == numerical_ranks(want), k
+        tol = value_tol(rep.residual_history[-1], z[f"res{k}"][-1])
+        # states carry the previous steps' differences too
+        assert rel_diff(state, want) <= k * tol, k
