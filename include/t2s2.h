@@ -85,11 +85,29 @@ typedef struct {
   int sweeps;
 } t2s2_step_report;
 
+/* Per-family launch accounting: launches, algorithmic flops/bytes, and
+ * (while profile_events is on) summed CUDA-event device time. */
+typedef struct {
+  char family[32];
+  long long launches;
+  double device_ms;
+  double flops;
+  double bytes;
+} t2s2_kernel_stat;
+
 int t2s2_context_create(int device, t2s2_context** out);
 void t2s2_context_destroy(t2s2_context* ctx);
 const char* t2s2_last_error(const t2s2_context* ctx);
+/* The cudaStream_t every kernel of the context is launched on (for
+ * callers that time or order work around the engine). */
+void* t2s2_stream(t2s2_context* ctx);
 /* Wait for all device work of the context. */
 int t2s2_synchronize(t2s2_context* ctx);
+
+/* Reset the counters; profile_events != 0 also records a CUDA event pair
+ * around every launch (adds ~2 us per launch). */
+int t2s2_stats_reset(t2s2_context* ctx, int profile_events);
+int t2s2_stats_read(t2s2_context* ctx, t2s2_kernel_stat* out, int capacity, int* count);
 
 /* cols == NULL uploads a vector train (cores r0 x rows x r1), otherwise an
  * operator train (cores r0 x rows x cols x r1).  host_cores holds the

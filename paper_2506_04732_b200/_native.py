@@ -80,6 +80,16 @@ class StepReportC(ctypes.Structure):
     ]
 
 
+class KernelStatC(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_char * 32),
+        ("launches", ctypes.c_longlong),
+        ("device_ms", ctypes.c_double),
+        ("flops", ctypes.c_double),
+        ("bytes", ctypes.c_double),
+    ]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
@@ -91,6 +101,9 @@ _SIGNATURES = {
     "t2s2_context_destroy": (None, [_P]),
     "t2s2_last_error": (ctypes.c_char_p, [_P]),
     "t2s2_synchronize": (_I, [_P]),
+    "t2s2_stream": (_P, [_P]),
+    "t2s2_stats_reset": (_I, [_P, _I]),
+    "t2s2_stats_read": (_I, [_P, ctypes.POINTER(KernelStatC), _I, _IP]),
     "t2s2_train_upload": (_I, [_P, _I, _IP, _IP, _IP, _DP, ctypes.POINTER(_P)]),
     "t2s2_train_upload_device": (_I, [_P, _I, _IP, _IP, _IP, _P, ctypes.POINTER(_P)]),
     "t2s2_train_shape": (_I, [_P, _IP, _IP, _IP, _IP, ctypes.POINTER(ctypes.c_size_t)]),
@@ -175,6 +188,26 @@ def check(rc, step=None):
     raise RuntimeError(f"t2s2 error {rc}: {msg}")
 
 
+def stats_reset(profile_events=False):
+    check(lib().t2s2_stats_reset(context(), 1 if profile_events else 0))
+
+
+def stats_read():
+    """{family: dict(launches, device_ms, flops, bytes)} since the last reset."""
+    n = ctypes.c_int()
+    check(lib().t2s2_stats_read(context(), None, 0, ctypes.byref(n)))
+    buf = (KernelStatC * max(n.value, 1))()
+    check(lib().t2s2_stats_read(context(), buf, n.value, ctypes.byref(n)))
+    return {buf[i].family.decode(): dict(launches=int(buf[i].launches),
+                                         device_ms=float(buf[i].device_ms),
+                                         flops=float(buf[i].flops), bytes=float(buf[i].bytes))
+            for i in range(n.value)}
+
+
+def synchronize():
+    check(lib().t2s2_synchronize(context()))
+
+
 def _iarr(vals):
     a = (ctypes.c_int * len(vals))(*[int(v) for v in vals])
     return a
@@ -201,6 +234,19 @@ class DeviceTrain:
         check(lib().t2s2_train_upload(context(), d, rows, cols, ranks,
                                       flat.ctypes.data_as(_DP), ctypes.byref(h)))
         return cls(h)
+
+    @classmethod
+    def upload_flat(cls, host_ptr, rows, cols, ranks):
+        """Upload from a caller-owned flat float64 buffer (e.g. pinned memory)."""
+        h = _P()
+        check(lib().t2s2_train_upload(context(), len(rows), _iarr(rows),
+                                      _iarr(cols) if cols is not None else None,
+                                      _iarr(ranks), ctypes.cast(host_ptr, _DP), ctypes.byref(h)))
+        return cls(h)
+
+    def download_into(self, host_ptr, capacity):
+        check(lib().t2s2_train_download(context(), self.handle, ctypes.cast(host_ptr, _DP),
+                                        int(capacity)))
 
     @classmethod
     def upload_device(cls, ptr, d, rows, cols, ranks):

@@ -10,6 +10,7 @@
 
 #include "als.h"
 #include "blas.h"
+#include "iterative.h"
 #include "linalg.h"
 #include "tt.h"
 
@@ -50,6 +51,50 @@ __global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
   }
 }
 
+// G[a,b,m,P,Q] = sum_k ac[a,k,m,P] ac[b,k,m,Q] (diagonal of A^T A per core).
+__global__ void gram_diag_kernel(int ra, int n, int rb, const double* __restrict__ ac,
+                                 double* __restrict__ G) {
+  const long long total = (long long)ra * ra * n * rb * rb;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int Q = (int)(e % rb);
+    long long t = e / rb;
+    const int P = (int)(t % rb);
+    t /= rb;
+    const int m = (int)(t % n);
+    t /= n;
+    const int b = (int)(t % ra), a = (int)(t / ra);
+    double s = 0.0;
+    for (int k = 0; k < n; ++k)
+      s = fma(ac[(((long long)a * n + k) * n + m) * rb + P], ac[(((long long)b * n + k) * n + m) * rb + Q], s);
+    G[e] = s;
+  }
+}
+
+// Jacobi diagonal of the normal block (tt_solver.py:234-236), zeros -> 1.
+__global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
+                                   const double* __restrict__ pnl, const double* __restrict__ G,
+                                   const double* __restrict__ pnr, double* __restrict__ out) {
+  const long long total = (long long)rx * n * ry;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int y = (int)(e % ry), m = (int)((e / ry) % n), x = (int)(e / ((long long)ry * n));
+    double s = 0.0;
+    for (int a = 0; a < ra; ++a)
+      for (int b = 0; b < ra; ++b) {
+        const double l = pnl[(((long long)x * ra + a) * ra + b) * rx + x];
+        if (l == 0.0) continue;
+        const double* g = G + ((((long long)a * ra + b) * n + m) * rb) * rb;
+        double t = 0.0;
+        for (int P = 0; P < rb; ++P)
+          for (int Q = 0; Q < rb; ++Q)
+            t = fma(g[P * rb + Q], pnr[(((long long)y * rb + P) * rb + Q) * ry + y], t);
+        s = fma(l, t, s);
+      }
+    out[e] = fabs(s) > 1e-300 ? s : 1.0;
+  }
+}
+
 __global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -59,8 +104,11 @@ __global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
 bool all_finite(const DTensor& t) {
   int* flag = reinterpret_cast<int*>(allocator().alloc(1));
   T2S2_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream()));
-  nonfinite_kernel<<<grid_of((long long)t.size()), 256, 0, stream()>>>(t.p, (long long)t.size(),
-                                                                         flag);
+  {
+    LaunchScope ls("check", 0, (double)t.size()*8);
+    nonfinite_kernel<<<grid_of((long long)t.size()), 256, 0, stream()>>>(t.p, (long long)t.size(),
+                                                                           flag);
+  }
   T2S2_CHECK_LAUNCH();
   int h = 0;
   T2S2_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
@@ -156,12 +204,48 @@ DTensor normal_matrix(const DTensor& pnl, const DTensor& ac, const DTensor& pnr)
   return permute(t, {1, 3, 5, 0, 2, 4});       // (z, n, w | x, m, y): column-major
 }
 
+DTensor galerkin_apply(const DTensor& pal, const DTensor& ac, const DTensor& par, const DTensor& u) {
+  DTensor t = tensordot(pal, {2}, u, {0});     // (x, a, n, w)
+  t = tensordot(t, {1, 2}, ac, {0, 2});        // (x, w, m, b)
+  return tensordot(t, {1, 3}, par, {2, 1});    // (x, m, y)
+}
+
+DTensor normal_diagonal(const DTensor& pnl, const DTensor& ac, const DTensor& pnr) {
+  const int rx = pnl.dim(0), ra = ac.dim(0), n = ac.dim(1), rb = ac.dim(3), ry = pnr.dim(0);
+  DTensor G({ra, ra, n, rb, rb});
+  {
+    LaunchScope ls("normal_diag", 2.0*G.size()*n, 0);
+    gram_diag_kernel<<<grid_of((long long)G.size()), 256, 0, stream()>>>(ra, n, rb, ac.p, G.p);
+  }
+  DTensor out({rx, n, ry});
+  {
+    LaunchScope ls("normal_diag", 2.0*out.size()*ra*ra*rb*rb, 0);
+    normal_diag_kernel<<<grid_of((long long)out.size()), 256, 0, stream()>>>(rx, ra, n, ry, rb, pnl.p,
+                                                                            G.p, pnr.p, out.p);
+  }
+  T2S2_CHECK_LAUNCH();
+  return out;
+}
+
+// Wrap a tensor-valued local operator as a flat device matvec.
+MatVec as_matvec(std::vector<int> shape, std::function<DTensor(const DTensor&)> f) {
+  return [shape, f](const double* in, double* out) {
+    DTensor u(shape);
+    dcopy(u.p, in, u.size());
+    DTensor r = f(u);
+    dcopy(out, r.p, r.size());
+  };
+}
+
 DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& par) {
   const int rx = pal.dim(0), ra = pal.dim(1), n = ac.dim(1), rb = ac.dim(3), ry = par.dim(0);
   const long long N = (long long)rx * n * ry;
   DTensor B({(int)N, (int)N});
-  galerkin_matrix_kernel<<<grid_of(N * N), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
-                                                                par.p, B.p);
+  {
+    LaunchScope ls("galerkin_build", 2.0*(double)N*N*ra*(rb+1), 8.0*(double)N*N);
+    galerkin_matrix_kernel<<<grid_of(N * N), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
+                                                                  par.p, B.p);
+  }
   T2S2_CHECK_LAUNCH();
   return B;
 }
@@ -337,15 +421,22 @@ struct Sweep {
     DTensor nu_old = normal_apply(ln[l], ac, rn[l + 1], u_old);
     const double q_old = score(u_old, nu_old, c_ls);
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
-    T2S2_REQUIRE(direct, kErrCapacity,
-                 "local system of size " + std::to_string(size) +
-                     " exceeds local_direct_size; iterative local solver not available");
+    const double inner_rtol = std::fmax(cfg.inner_tol_factor * current_res, 1e-12);
     const bool try_gal = gal_rejects < gal_cap;
     bool have_gal = false;
     DTensor u_gal;
     if (try_gal) {
-      DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
-      have_gal = dense_solve(B, c_gal, u_gal);
+      if (direct) {
+        DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+        have_gal = dense_solve(B, c_gal, u_gal);
+      } else {
+        // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
+        u_gal = u_old.clone();
+        const DTensor &pal = la[l], &par = ra[l + 1];
+        gmres(as_matvec(u_old.shape, [&](const DTensor& u) { return galerkin_apply(pal, ac, par, u); }),
+              (int)size, c_gal.p, u_gal.p, inner_rtol, 40, 10);
+        have_gal = true;
+      }
       if (have_gal) have_gal = all_finite(u_gal);
     }
     double best_q = q_old;
@@ -366,10 +457,20 @@ struct Sweep {
       }
     }
     if (choice == 0) {
-      DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
-      Nm.view({(int)size, (int)size});
       DTensor u_ls;
-      bool ok = dense_solve(Nm, c_ls, u_ls);
+      bool ok = true;
+      if (direct) {
+        DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
+        Nm.view({(int)size, (int)size});
+        ok = dense_solve(Nm, c_ls, u_ls);
+      } else {
+        // scipy cg(x0=u_old, rtol, atol=0, maxiter=250, M=diag^{-1})
+        u_ls = u_old.clone();
+        const DTensor &pnl = ln[l], &pnr = rn[l + 1];
+        DTensor dg = normal_diagonal(pnl, ac, pnr);
+        pcg(as_matvec(u_old.shape, [&](const DTensor& u) { return normal_apply(pnl, ac, pnr, u); }),
+            (int)size, c_ls.p, u_ls.p, dg.p, inner_rtol, 250);
+      }
       if (ok && all_finite(u_ls)) {
         u_ls.view(u_old.shape);
         DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);

@@ -3,17 +3,38 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <string>
+#include <unordered_map>
 
 #include "../../include/t2s2.h"
 #include "als.h"
 #include "blas.h"
 #include "tt.h"
 
+namespace t2s2 {
+struct FamilyStat {
+  std::string name;
+  long long launches = 0;
+  double flops = 0.0, bytes = 0.0, ms = 0.0;
+};
+struct Pending {
+  int fam;
+  cudaEvent_t a, b;
+};
+}  // namespace t2s2
+
 struct t2s2_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   t2s2::Allocator alloc;
   std::string last_error;
+  // launch accounting
+  std::vector<t2s2::FamilyStat> fams;
+  std::unordered_map<std::string, int> fam_index;
+  bool profiling = false;
+  std::vector<cudaEvent_t> event_pool;
+  size_t pool_used = 0;
+  std::vector<t2s2::Pending> pending;
 };
 
 struct t2s2_train {
@@ -36,6 +57,51 @@ struct Bind {  // makes ctx current for the duration of an API call
 }  // namespace
 
 Allocator& allocator() { return g_ctx->alloc; }
+
+LaunchScope::LaunchScope(const char* family, double flops, double bytes) {
+  t2s2_context* c = g_ctx;
+  auto it = c->fam_index.find(family);
+  int f;
+  if (it == c->fam_index.end()) {
+    f = (int)c->fams.size();
+    c->fam_index.emplace(family, f);
+    c->fams.push_back(FamilyStat{family});
+  } else {
+    f = it->second;
+  }
+  FamilyStat& st = c->fams[f];
+  st.launches += 1;
+  st.flops += flops;
+  st.bytes += bytes;
+  if (!c->profiling) return;
+  while (c->event_pool.size() < c->pool_used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    c->event_pool.push_back(e);
+  }
+  Pending p{f, c->event_pool[c->pool_used], c->event_pool[c->pool_used + 1]};
+  c->pool_used += 2;
+  cudaEventRecord(p.a, c->stream);
+  slot = (int)c->pending.size();
+  c->pending.push_back(p);
+}
+
+LaunchScope::~LaunchScope() {
+  if (slot >= 0) cudaEventRecord(g_ctx->pending[slot].b, g_ctx->stream);
+}
+
+namespace {
+void resolve_pending(t2s2_context* c) {
+  if (c->pending.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) c->fams[p.fam].ms += ms;
+  }
+  c->pending.clear();
+  c->pool_used = 0;
+}
+}  // namespace
 cudaStream_t stream() { return g_ctx->stream; }
 
 }  // namespace t2s2
@@ -147,6 +213,7 @@ void t2s2_context_destroy(t2s2_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -155,8 +222,35 @@ const char* t2s2_last_error(const t2s2_context* ctx) {
   return ctx ? ctx->last_error.c_str() : "null context";
 }
 
+void* t2s2_stream(t2s2_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
 int t2s2_synchronize(t2s2_context* ctx) {
   return guarded(ctx, [&] { T2S2_CUDA(cudaStreamSynchronize(stream())); });
+}
+
+int t2s2_stats_reset(t2s2_context* ctx, int profile_events) {
+  return guarded(ctx, [&] {
+    resolve_pending(ctx);
+    for (auto& f : ctx->fams) f = FamilyStat{f.name};
+    ctx->profiling = profile_events != 0;
+  });
+}
+
+int t2s2_stats_read(t2s2_context* ctx, t2s2_kernel_stat* out, int capacity, int* count) {
+  return guarded(ctx, [&] {
+    resolve_pending(ctx);
+    const int n = (int)ctx->fams.size();
+    if (count) *count = n;
+    for (int i = 0; i < n && i < capacity && out; ++i) {
+      const FamilyStat& f = ctx->fams[i];
+      std::memset(out[i].family, 0, sizeof out[i].family);
+      std::strncpy(out[i].family, f.name.c_str(), sizeof out[i].family - 1);
+      out[i].launches = f.launches;
+      out[i].device_ms = f.ms;
+      out[i].flops = f.flops;
+      out[i].bytes = f.bytes;
+    }
+  });
 }
 
 int t2s2_train_upload(t2s2_context* ctx, int d, const int* rows, const int* cols,

@@ -190,8 +190,11 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
     return;
   }
   dim3 grid(ceil_div(N, BN), ceil_div(M, BM), batch);
-  gemm_kernel<<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C,
-                                          ldc, sC);
+  {
+    LaunchScope ls("gemm", 2.0*M*N*(double)K*batch, 8.0*batch*((double)M*K+(double)K*N+2.0*M*N));
+    gemm_kernel<<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C,
+                                            ldc, sC);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
@@ -225,7 +228,10 @@ DTensor permute(const DTensor& a, const std::vector<int>& perm) {
     pa.in_stride[k] = st[perm[k]];
   }
   long long n = (long long)a.size();
-  permute_kernel<<<grid_for(n), 256, 0, stream()>>>(a.p, out.p, n, pa);
+  {
+    LaunchScope ls("permute", 0, 16.0*n);
+    permute_kernel<<<grid_for(n), 256, 0, stream()>>>(a.p, out.p, n, pa);
+  }
   T2S2_CHECK_LAUNCH();
   return out;
 }
@@ -306,7 +312,10 @@ DTensor tensordot(const DTensor& a, const std::vector<int>& axa, const DTensor& 
 void transpose(const double* in, double* out, int rows, int cols) {
   long long n = (long long)rows * cols;
   if (n <= 0) return;
-  transpose_kernel<<<grid_for(n), 256, 0, stream()>>>(in, out, rows, cols);
+  {
+    LaunchScope ls("permute", 0, 16.0*n);
+    transpose_kernel<<<grid_for(n), 256, 0, stream()>>>(in, out, rows, cols);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
@@ -316,19 +325,28 @@ void dcopy(double* dst, const double* src, size_t n) {
 
 void dfill(double* dst, double v, size_t n) {
   if (!n) return;
-  fill_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(dst, v, (long long)n);
+  {
+    LaunchScope ls("vector", 0, 8.0*n);
+    fill_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(dst, v, (long long)n);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
 void dscal(double* x, double s, size_t n) {
   if (!n) return;
-  scal_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(x, s, (long long)n);
+  {
+    LaunchScope ls("vector", n, 16.0*n);
+    scal_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(x, s, (long long)n);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
 void daxpby(double a, const double* x, double b, double* y, size_t n) {
   if (!n) return;
-  axpby_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(a, x, b, y, (long long)n);
+  {
+    LaunchScope ls("vector", 3.0*n, 24.0*n);
+    axpby_kernel<<<grid_for((long long)n), 256, 0, stream()>>>(a, x, b, y, (long long)n);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
@@ -337,15 +355,24 @@ void daxpy(double a, const double* x, double* y, size_t n) { daxpby(a, x, 1.0, y
 void copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
   long long n = (long long)rows * cols;
   if (n <= 0) return;
-  copy2d_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols);
+  {
+    LaunchScope ls("vector", 0, 16.0*n);
+    copy2d_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
 void ddot_dev(const double* x, const double* y, size_t n, double* out) {
   int g = grid_for((long long)n, 256, 296);
   double* part = allocator().alloc(g);
-  dot_partial_kernel<<<g, 256, 0, stream()>>>(x, y, (long long)n, part);
-  sum_final_kernel<<<1, 256, 0, stream()>>>(part, g, out);
+  {
+    LaunchScope ls("reduce", 2.0*n, 16.0*n);
+    dot_partial_kernel<<<g, 256, 0, stream()>>>(x, y, (long long)n, part);
+  }
+  {
+    LaunchScope ls("reduce", 0, 0);
+    sum_final_kernel<<<1, 256, 0, stream()>>>(part, g, out);
+  }
   T2S2_CHECK_LAUNCH();
   allocator().release(part);
 }

@@ -63,6 +63,16 @@ struct Allocator {
   }
 };
 
+// Launch accounting (per context).  Every kernel launch sits inside a
+// LaunchScope naming its family and the algorithmic flops/bytes of that
+// launch; counts are always kept, CUDA-event timings only while profiling
+// is switched on (t2s2_stats_reset(ctx, 1)).
+struct LaunchScope {
+  int slot = -1;
+  LaunchScope(const char* family, double flops = 0.0, double bytes = 0.0);
+  ~LaunchScope();
+};
+
 Allocator& allocator();  // the current context's allocator
 cudaStream_t stream();   // the current context's stream
 

@@ -1,0 +1,311 @@
+// Device GMRES(restart) and Jacobi-PCG (see iterative.h).
+#include <cfloat>
+#include <cmath>
+
+#include "blas.h"
+#include "iterative.h"
+
+namespace t2s2 {
+namespace {
+
+constexpr int kMaxRestart = 64;
+constexpr int kThreads = 1024;
+
+struct GmState {
+  double h[kMaxRestart][kMaxRestart + 1];  // h[col][row] as in scipy
+  double gc[kMaxRestart], gs[kMaxRestart];
+  double S[kMaxRestart + 1];
+  double presid, ptol;
+  int col_final;
+  int active;
+  int breakdown;
+};
+
+struct CgState {
+  double rho_prev, rho_cur;
+  int active;
+};
+
+__device__ double cta_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__device__ double cta_dot(const double* a, const double* b, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+  return cta_sum(s, red);
+}
+
+// LAPACK 3.10+ dlartg: c >= 0, r carries the sign of f, s = g / r.
+__device__ void lartg(double f, double g, double& c, double& s, double& r) {
+  if (g == 0.0) {
+    c = 1.0;
+    s = 0.0;
+    r = f;
+  } else if (f == 0.0) {
+    c = 0.0;
+    s = g > 0 ? 1.0 : -1.0;
+    r = fabs(g);
+  } else {
+    double d = sqrt(f * f + g * g);
+    c = fabs(f) / d;
+    r = f > 0 ? d : -d;
+    s = g / r;
+  }
+}
+
+// New cycle: V[0] = r / ||r||, S = (||r||, 0, ...).
+__global__ void __launch_bounds__(kThreads)
+    gm_cycle_kernel(GmState* st, const double* r, double* V, int n, double ptol) {
+  __shared__ double red[33];
+  const double nr = sqrt(cta_dot(r, r, n, red));
+  const double inv = 1.0 / nr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) V[i] = r[i] * inv;
+  for (int e = threadIdx.x; e < kMaxRestart * (kMaxRestart + 1); e += blockDim.x)
+    (&st->h[0][0])[e] = 0.0;
+  for (int e = threadIdx.x; e <= kMaxRestart; e += blockDim.x) st->S[e] = 0.0;
+  if (threadIdx.x == 0) {
+    st->S[0] = nr;
+    st->ptol = ptol;
+    st->active = 1;
+    st->breakdown = 0;
+    st->col_final = -1;
+    st->presid = 0.0;
+  }
+}
+
+// Arnoldi step for column col (w = A v_col already in V[col+1]).
+__global__ void __launch_bounds__(kThreads)
+    gm_arnoldi_kernel(GmState* st, double* V, int n, int col, int restart) {
+  __shared__ double red[33];
+  if (!st->active) return;
+  double* w = V + (size_t)(col + 1) * n;
+  const double h0 = sqrt(cta_dot(w, w, n, red));
+  for (int k = 0; k <= col; ++k) {
+    const double* vk = V + (size_t)k * n;
+    const double t = cta_dot(vk, w, n, red);
+    if (threadIdx.x == 0) st->h[col][k] = t;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = fma(-t, vk[i], w[i]);
+    __syncthreads();
+  }
+  const double h1 = sqrt(cta_dot(w, w, n, red));
+  const bool brk = h1 <= DBL_EPSILON * h0;
+  if (!brk) {
+    const double inv = 1.0 / h1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] *= inv;
+  }
+  if (threadIdx.x == 0) {
+    double* hc = st->h[col];
+    hc[col + 1] = brk ? 0.0 : h1;
+    if (brk) st->breakdown = 1;
+    for (int k = 0; k < col; ++k) {
+      const double c = st->gc[k], s = st->gs[k];
+      const double n0 = hc[k], n1 = hc[k + 1];
+      hc[k] = c * n0 + s * n1;
+      hc[k + 1] = -s * n0 + c * n1;
+    }
+    double c, s, mag;
+    lartg(hc[col], hc[col + 1], c, s, mag);
+    st->gc[col] = c;
+    st->gs[col] = s;
+    hc[col] = mag;
+    hc[col + 1] = 0.0;
+    const double t = -s * st->S[col];
+    st->S[col] = c * st->S[col];
+    st->S[col + 1] = t;
+    st->presid = fabs(t);
+    if (st->presid <= st->ptol || brk || col == restart - 1) {
+      st->active = 0;
+      st->col_final = col;
+    }
+  }
+}
+
+// y = H^{-1} S (upper triangular, scipy's pseudo-solve), x += y V.
+__global__ void __launch_bounds__(kThreads)
+    gm_update_kernel(GmState* st, const double* V, double* x, int n) {
+  __shared__ double y[kMaxRestart];
+  const int c = st->col_final;
+  if (threadIdx.x == 0) {
+    if (st->h[c][c] == 0.0) st->S[c] = 0.0;
+    for (int k = 0; k <= c; ++k) y[k] = st->S[k];
+    for (int k = c; k > 0; --k) {
+      if (y[k] != 0.0) {
+        y[k] /= st->h[k][k];
+        const double t = y[k];
+        for (int j = 0; j < k; ++j) y[j] -= t * st->h[k][j];
+      }
+    }
+    if (y[0] != 0.0) y[0] /= st->h[0][0];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double acc = x[i];
+    for (int k = 0; k <= c; ++k) acc = fma(y[k], V[(size_t)k * n + i], acc);
+    x[i] = acc;
+  }
+}
+
+// scipy cg, top of iteration: convergence check, z = M r, rho, p update.
+__global__ void __launch_bounds__(kThreads)
+    cg_pre_kernel(CgState* st, const double* r, const double* diag, double* z, double* p, int n,
+                  double atol, int iteration) {
+  __shared__ double red[33];
+  if (!st->active) return;
+  const double rn = sqrt(cta_dot(r, r, n, red));
+  if (rn < atol) {
+    if (threadIdx.x == 0) st->active = 0;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) z[i] = r[i] / diag[i];
+  __syncthreads();
+  const double rho = cta_dot(r, z, n, red);
+  const double beta = iteration > 0 ? rho / st->rho_prev : 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    p[i] = iteration > 0 ? fma(p[i], beta, z[i]) : z[i];
+  if (threadIdx.x == 0) st->rho_cur = rho;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_post_kernel(CgState* st, const double* p, const double* q, double* x, double* r, int n) {
+  __shared__ double red[33];
+  if (!st->active) return;
+  const double pq = cta_dot(p, q, n, red);
+  const double alpha = st->rho_cur / pq;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    r[i] = fma(-alpha, q[i], r[i]);
+  }
+  if (threadIdx.x == 0) st->rho_prev = st->rho_cur;
+}
+
+template <class T>
+T read_state(const T* d) {
+  T h;
+  T2S2_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+int read_flag(const int* d) { return read_state<int>(d); }
+
+}  // namespace
+
+int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int restart,
+          int maxiter) {
+  const double bnrm2 = dnrm2(b, n);
+  const double atol = rtol * bnrm2;  // scipy: max(atol=0, rtol*||b||)
+  if (bnrm2 == 0.0) {
+    dcopy(x, b, n);
+    return 0;
+  }
+  if (restart > n) restart = n;
+  if (restart > kMaxRestart) restart = kMaxRestart;
+  double* V = allocator().alloc((size_t)(restart + 1) * n);
+  double* r = allocator().alloc(n);
+  GmState* st = reinterpret_cast<GmState*>(allocator().alloc(sizeof(GmState) / sizeof(double) + 1));
+  auto residual = [&]() {  // r = b - A x, returns ||r||
+    A(x, r);
+    daxpby(1.0, b, -1.0, r, n);
+    return dnrm2(r, n);
+  };
+  double rnorm = residual();
+  int inner = 0;
+  if (rnorm < atol) {
+    allocator().release(V);
+    allocator().release(r);
+    allocator().release(reinterpret_cast<double*>(st));
+    return 0;
+  }
+  double ptol_max_factor = 1.0;
+  double ptol = bnrm2 * std::fmin(ptol_max_factor, atol / bnrm2);
+  for (int it = 0; it < maxiter; ++it) {
+    {
+      LaunchScope ls("gmres", 3.0*n, 24.0*n);
+      gm_cycle_kernel<<<1, kThreads, 0, stream()>>>(st, r, V, n, ptol);
+    }
+    T2S2_CHECK_LAUNCH();
+    for (int col = 0; col < restart; ++col) {
+      if (col > 0 && col % 8 == 0 && !read_flag(&st->active)) break;
+      A(V + (size_t)col * n, V + (size_t)(col + 1) * n);
+      {
+        LaunchScope ls("gmres", 4.0*n*(col+2), 16.0*n*(col+2));
+        gm_arnoldi_kernel<<<1, kThreads, 0, stream()>>>(st, V, n, col, restart);
+      }
+      T2S2_CHECK_LAUNCH();
+    }
+    {
+      LaunchScope ls("gmres", 2.0*n*restart, 8.0*n*restart);
+      gm_update_kernel<<<1, kThreads, 0, stream()>>>(st, V, x, n);
+    }
+    T2S2_CHECK_LAUNCH();
+    GmState h = read_state<GmState>(st);
+    inner += h.col_final + 1;
+    const double presid = h.presid;
+    rnorm = residual();
+    if (rnorm <= atol) break;
+    if (h.breakdown) break;
+    if (presid <= ptol)
+      ptol_max_factor = std::fmax(DBL_EPSILON, 0.25 * ptol_max_factor);
+    else
+      ptol_max_factor = std::fmin(1.0, 1.5 * ptol_max_factor);
+    ptol = presid * std::fmin(ptol_max_factor, atol / rnorm);
+  }
+  allocator().release(V);
+  allocator().release(r);
+  allocator().release(reinterpret_cast<double*>(st));
+  return inner;
+}
+
+int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, double rtol,
+        int maxiter) {
+  const double bnrm2 = dnrm2(b, n);
+  const double atol = rtol * bnrm2;
+  if (bnrm2 == 0.0) {
+    dcopy(x, b, n);
+    return 0;
+  }
+  double* r = allocator().alloc(n);
+  double* z = allocator().alloc(n);
+  double* p = allocator().alloc(n);
+  double* q = allocator().alloc(n);
+  CgState* st = reinterpret_cast<CgState*>(allocator().alloc(sizeof(CgState) / sizeof(double) + 1));
+  A(x, r);
+  daxpby(1.0, b, -1.0, r, n);
+  CgState init{0.0, 0.0, 1};
+  T2S2_CUDA(cudaMemcpyAsync(st, &init, sizeof(CgState), cudaMemcpyHostToDevice, stream()));
+  int it = 0;
+  for (; it < maxiter; ++it) {
+    if (it > 0 && it % 10 == 0 && !read_flag(&st->active)) break;
+    {
+      LaunchScope ls("cg", 6.0*n, 40.0*n);
+      cg_pre_kernel<<<1, kThreads, 0, stream()>>>(st, r, diag, z, p, n, atol, it);
+    }
+    A(p, q);
+    {
+      LaunchScope ls("cg", 6.0*n, 48.0*n);
+      cg_post_kernel<<<1, kThreads, 0, stream()>>>(st, p, q, x, r, n);
+    }
+    T2S2_CHECK_LAUNCH();
+  }
+  T2S2_CUDA(cudaStreamSynchronize(stream()));  // init lives on the host stack
+  allocator().release(r);
+  allocator().release(z);
+  allocator().release(p);
+  allocator().release(q);
+  allocator().release(reinterpret_cast<double*>(st));
+  return it;
+}
+
+}  // namespace t2s2

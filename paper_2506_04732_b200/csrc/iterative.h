@@ -1,0 +1,30 @@
+// Restarted GMRES and Jacobi-preconditioned CG for the local systems that
+// exceed the direct-solve size (reference: tt_solver.py:375-414, which calls
+// scipy.sparse.linalg.gmres(restart=40, maxiter=10) and cg(maxiter=250)).
+//
+// The Krylov recurrences follow scipy 1.18's pure-Python implementations
+// (modified Gram-Schmidt Arnoldi with LAPACK-style Givens rotations and the
+// gh-8400 inner-tolerance control; textbook PCG), with every vector and
+// scalar resident on the device.  The host only polls a convergence flag
+// every few iterations.
+#pragma once
+
+#include <functional>
+
+#include "common.h"
+
+namespace t2s2 {
+
+using MatVec = std::function<void(const double* in, double* out)>;
+
+// x (device, length n) is the initial guess and receives the result.
+// rtol relative to ||b|| (scipy's atol = rtol * ||b||).  Returns inner
+// iterations performed.
+int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int restart,
+          int maxiter);
+
+// Preconditioner M = diag^{-1}.
+int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, double rtol,
+        int maxiter);
+
+}  // namespace t2s2

@@ -228,7 +228,10 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
   double* W = allocator().alloc((size_t)m * n);
   double* Qc = allocator().alloc((size_t)m * k);
   double* tau = allocator().alloc(k);
-  qr_kernel<<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+  {
+    LaunchScope ls("qr", 4.0*m*(double)n*(m<n?m:n), 16.0*m*(double)n);
+    qr_kernel<<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+  }
   T2S2_CHECK_LAUNCH();
   allocator().release(W);
   allocator().release(Qc);
@@ -244,7 +247,10 @@ void jacobi_svd(int p, int q, double* G, DTensor& U, DTensor& s, DTensor& Vt) {
   Vt = DTensor({q, q});
   double* V = allocator().alloc((size_t)q * q + q);
   int* perm = reinterpret_cast<int*>(allocator().alloc(q));
-  jacobi_kernel<<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+  {
+    LaunchScope ls("svd_jacobi", 0, 0);
+    jacobi_kernel<<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+  }
   T2S2_CHECK_LAUNCH();
   allocator().release(V);
   allocator().release(reinterpret_cast<double*>(perm));

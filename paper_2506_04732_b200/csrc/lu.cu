@@ -197,9 +197,15 @@ void lu_factor(int N, double* A, int* ipiv, int* info_dev) {
   T2S2_CUDA(cudaMemsetAsync(info_dev, 0, sizeof(int), stream()));
   for (int k0 = 0; k0 < N; k0 += NB) {
     const int nb = N - k0 < NB ? N - k0 : NB;
-    panel_kernel<<<1, kPanelThreads, 0, stream()>>>(N, A, k0, nb, ipiv, info_dev);
+    {
+      LaunchScope ls("lu_panel", (double)(N-k0)*nb*nb, 16.0*(double)(N-k0)*nb);
+      panel_kernel<<<1, kPanelThreads, 0, stream()>>>(N, A, k0, nb, ipiv, info_dev);
+    }
     T2S2_CHECK_LAUNCH();
-    swap_trsm_kernel<<<ceil_div(N, 128), 128, 0, stream()>>>(N, A, k0, nb, ipiv);
+    {
+      LaunchScope ls("lu_trsm", (double)(N-k0-nb)*nb*nb, 16.0*(double)N*nb);
+      swap_trsm_kernel<<<ceil_div(N, 128), 128, 0, stream()>>>(N, A, k0, nb, ipiv);
+    }
     T2S2_CHECK_LAUNCH();
     const int rest = N - k0 - nb;
     if (rest > 0) {
@@ -217,7 +223,10 @@ void lu_solve(int N, const double* LU, const int* ipiv, double* b) {
   if (smem > 48 * 1024)
     T2S2_CUDA(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-  lu_solve_kernel<<<1, kSolveThreads, smem, stream()>>>(N, LU, ipiv, b);
+  {
+    LaunchScope ls("lu_solve", 2.0*(double)N*N, 8.0*(double)N*N);
+    lu_solve_kernel<<<1, kSolveThreads, smem, stream()>>>(N, LU, ipiv, b);
+  }
   T2S2_CHECK_LAUNCH();
 }
 

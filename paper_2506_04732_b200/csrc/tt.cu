@@ -61,13 +61,19 @@ long long mid_size(const DTensor& c) { return (long long)c.size() / ((long long)
 
 void scale_rows(double* X, int rows, int cols, int ld, const double* s) {
   if ((long long)rows * cols <= 0) return;
-  scale_rows_kernel<<<grid_of((long long)rows * cols), 256, 0, stream()>>>(X, rows, cols, ld, s);
+  {
+    LaunchScope ls("vector", (double)rows*cols, 16.0*rows*cols);
+    scale_rows_kernel<<<grid_of((long long)rows * cols), 256, 0, stream()>>>(X, rows, cols, ld, s);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
 void scale_cols(double* X, int rows, int cols, int ld, const double* s) {
   if ((long long)rows * cols <= 0) return;
-  scale_cols_kernel<<<grid_of((long long)rows * cols), 256, 0, stream()>>>(X, rows, cols, ld, s);
+  {
+    LaunchScope ls("vector", (double)rows*cols, 16.0*rows*cols);
+    scale_cols_kernel<<<grid_of((long long)rows * cols), 256, 0, stream()>>>(X, rows, cols, ld, s);
+  }
   T2S2_CHECK_LAUNCH();
 }
 
@@ -196,10 +202,16 @@ Train tt_add(const Train& a, const Train& b, double sa, double sb) {
     dfill(o.p, 0.0, o.size());
     const int ob0 = l == 0 ? 0 : ca.dim(0), ob1 = l == d - 1 ? 0 : ca.dim(-1);
     long long na = (long long)ca.size(), nb = (long long)cb.size();
-    place_block_kernel<<<grid_of(na), 256, 0, stream()>>>(o.p, r0, mid, r1, ca.p, ca.dim(0),
-                                                          ca.dim(-1), 0, 0, fa);
-    place_block_kernel<<<grid_of(nb), 256, 0, stream()>>>(o.p, r0, mid, r1, cb.p, cb.dim(0),
-                                                          cb.dim(-1), ob0, ob1, fb);
+    {
+      LaunchScope ls("vector", 0, 16.0*na);
+      place_block_kernel<<<grid_of(na), 256, 0, stream()>>>(o.p, r0, mid, r1, ca.p, ca.dim(0),
+                                                            ca.dim(-1), 0, 0, fa);
+    }
+    {
+      LaunchScope ls("vector", 0, 16.0*nb);
+      place_block_kernel<<<grid_of(nb), 256, 0, stream()>>>(o.p, r0, mid, r1, cb.p, cb.dim(0),
+                                                            cb.dim(-1), ob0, ob1, fb);
+    }
     T2S2_CHECK_LAUNCH();
     out.cores.push_back(std::move(o));
   }

