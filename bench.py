@@ -87,7 +87,11 @@ def oracle_problem(recipe):
     from paper_2506_04732_b200 import assembly, tt, workloads as wl
 
     def rnd(v, tol, max_rank=None):
-        return type(v)(ot.tt_round(v.cores, tol, max_rank))
+        if isinstance(v, tt.TTOperator):
+            rows, cols = v.row_sizes, v.col_sizes
+            return tt.TTOperator(ot.as_operator(ot.tt_round(ot.as_vector(v.cores), tol, max_rank),
+                                                rows, cols))
+        return tt.TTVector(ot.tt_round(v.cores, tol, max_rank))
 
     def add(a, b):
         return type(a)(ot.tt_add(a.cores, b.cores))

@@ -118,6 +118,7 @@ _SIGNATURES = {
     "t2s2_full": (_I, [_P, _P, _DP, ctypes.c_size_t]),
     "t2s2_solve": (_I, [_P, _P, _P, _P, ctypes.POINTER(SolverConfigC), ctypes.POINTER(_P),
                         ctypes.POINTER(SolveReportC)]),
+    "t2s2_dense_solve": (_I, [_P, _I, _DP, _DP, _DP]),
     "t2s2_residual": (_I, [_P, _P, _P, _P, _D, _DP]),
     "t2s2_march": (_I, [_P, _P, _P, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _D,
                         ctypes.POINTER(SolverConfigC), _I, ctypes.POINTER(_P),
@@ -202,6 +203,17 @@ def stats_read():
                                          device_ms=float(buf[i].device_ms),
                                          flops=float(buf[i].flops), bytes=float(buf[i].bytes))
             for i in range(n.value)}
+
+
+def dense_solve(a, b):
+    """x = a^{-1} b through the engine's fused LU kernel (testing hook)."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    n = b.size
+    check(lib().t2s2_dense_solve(context(), n, a.ravel(order="F").ctypes.data_as(_DP),
+                                 b.ctypes.data_as(_DP), x.ctypes.data_as(_DP)))
+    return x
 
 
 def synchronize():

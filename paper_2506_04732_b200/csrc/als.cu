@@ -255,9 +255,11 @@ bool dense_solve(DTensor& M, const DTensor& rhs, DTensor& out) {
   const int N = M.dim(0);
   int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
   int* info = reinterpret_cast<int*>(allocator().alloc(1));
-  lu_factor(N, M.p, ipiv, info);
   out = rhs.clone();
-  lu_solve(N, M.p, ipiv, out.p);
+  if (!lu_solve_fused(N, M.p, out.p, ipiv, info)) {
+    lu_factor(N, M.p, ipiv, info);
+    lu_solve(N, M.p, ipiv, out.p);
+  }
   int h = 0;
   T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
   T2S2_CUDA(cudaStreamSynchronize(stream()));

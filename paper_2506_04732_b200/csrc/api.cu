@@ -9,6 +9,7 @@
 #include "../../include/t2s2.h"
 #include "als.h"
 #include "blas.h"
+#include "linalg.h"
 #include "tt.h"
 
 namespace t2s2 {
@@ -367,6 +368,28 @@ int t2s2_solve(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* rhs,
     Train sol = als_solve(a->t, rhs->t, x0->t, to_cfg(cfg), rep);
     fill_report(rep, report);
     *x = wrap(std::move(sol));
+  });
+}
+
+int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const double* b,
+                     double* x) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(n >= 1 && a_colmajor && b && x, kErrArg, "bad dense solve arguments");
+    DTensor A({n, n}), rhs({n});
+    to_device(A.p, a_colmajor, (size_t)n * n);
+    to_device(rhs.p, b, n);
+    int* piv = reinterpret_cast<int*>(allocator().alloc((size_t)n / 2 + 1));
+    int* info = reinterpret_cast<int*>(allocator().alloc(1));
+    if (!lu_solve_fused(n, A.p, rhs.p, piv, info)) {
+      lu_factor(n, A.p, piv, info);
+      lu_solve(n, A.p, piv, rhs.p);
+    }
+    int h = 0;
+    T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    to_host(x, rhs.p, n);
+    allocator().release(reinterpret_cast<double*>(piv));
+    allocator().release(reinterpret_cast<double*>(info));
+    T2S2_REQUIRE(h == 0, kErrValue, "singular matrix");
   });
 }
 

@@ -21,5 +21,8 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
 void lu_factor(int N, double* A, int* ipiv, int* info_dev);
 // Solve with the factors for one right-hand side (in place).
 void lu_solve(int N, const double* LU, const int* ipiv, double* b);
+// One cooperative launch: factor A (clobbered) and overwrite b with the
+// solution.  Returns false when N is too large for the smem panel.
+bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev);
 
 }  // namespace t2s2

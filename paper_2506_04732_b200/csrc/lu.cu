@@ -135,9 +135,12 @@ __global__ void __launch_bounds__(kSolveThreads)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) x[i] = b[i];
   __syncthreads();
+  int* sp = reinterpret_cast<int*>(x + N);
+  for (int i = tid; i < N; i += blockDim.x) sp[i] = ipiv[i];
+  __syncthreads();
   if (tid == 0)
     for (int i = 0; i < N; ++i) {
-      int p = ipiv[i];
+      int p = sp[i];
       if (p != i) {
         double t = x[i];
         x[i] = x[p];
@@ -218,7 +221,7 @@ void lu_factor(int N, double* A, int* ipiv, int* info_dev) {
 }
 
 void lu_solve(int N, const double* LU, const int* ipiv, double* b) {
-  size_t smem = (size_t)N * sizeof(double);
+  size_t smem = (size_t)N * (sizeof(double) + sizeof(int));
   T2S2_REQUIRE(smem <= 200 * 1024, kErrCapacity, "lu_solve: system too large for smem rhs");
   if (smem > 48 * 1024)
     T2S2_CUDA(cudaFuncSetAttribute(lu_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

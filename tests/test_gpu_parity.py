@@ -183,3 +183,28 @@ def test_iterative_local_solver_matches_oracle(golden, pk, tag):
         assert numerical_ranks(x.cores) == numerical_ranks(xo)
         assert rel_diff(x.cores, xo) <= value_tol(rep.residual_history[-1],
                                                   repo.residual_history[-1])
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 165, 500, 825, 1617, 2000, 2112])
+def test_dense_local_solve_kernel(pk, n):
+    """The fused LU kernel against numpy.linalg.solve (LAPACK getrf/getrs),
+    on matrices needing pivoting."""
+    from paper_2506_04732_b200 import _native
+
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n))
+    a[np.arange(n), np.arange(n)] *= 1e-3  # small diagonal forces row interchanges
+    b = rng.standard_normal(n)
+    x = _native.dense_solve(a, b)
+    want = np.linalg.solve(a, b)
+    cond = np.linalg.cond(a)
+    assert np.linalg.norm(x - want) <= 1e-14 * cond * np.linalg.norm(want) + 1e-300
+    assert np.linalg.norm(a @ x - b) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(x)
+
+
+def test_dense_local_solve_singular(pk):
+    from paper_2506_04732_b200 import _native
+
+    a = np.ones((4, 4))
+    with pytest.raises(ValueError):
+        _native.dense_solve(a, np.ones(4))

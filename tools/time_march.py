@@ -17,9 +17,20 @@ hl, hr, hs = to_device(left), to_device(right), to_device(state0)
 bcs = [to_device(b) for b, _ in fs]; srcs = [to_device(s) for _, s in fs]
 cfg = SolverConfig(**recipe.solver)
 _native.check(_native.lib().t2s2_synchronize(_native.context()))
-t0 = time.time()
-stored, rows = march_device(hl, hr, hs, steps, bcs, srcs, recipe.step_tol, cfg)
-_native.check(_native.lib().t2s2_synchronize(_native.context()))
-dt = time.time() - t0
-print(f"{steps} steps in {dt:.3f}s -> {steps/dt:.2f} steps/s")
-for r in rows: print(r)
+prof = len(sys.argv) > 3 and sys.argv[3] == "prof"
+state = hs
+tot = 0.0
+for k in range(steps):
+    _native.stats_reset(profile_events=prof)
+    t0 = time.time()
+    stored, rows = march_device(hl, hr, state, 1, [bcs[k]], [srcs[k]], recipe.step_tol, cfg, store_stride=1)
+    _native.synchronize()
+    dt = time.time() - t0
+    tot += dt
+    state = stored[1]
+    st = _native.stats_read()
+    top = sorted(st.items(), key=lambda kv: -kv[1]["device_ms"] if prof else -kv[1]["launches"])[:8]
+    print(f"step {k+1}: {dt*1e3:.1f} ms", rows[0], "launches", sum(v["launches"] for v in st.values()))
+    for name, v in top:
+        print(f"    {name:16s} n={v['launches']:6d} ms={v['device_ms']:9.3f} gflop={v['flops']/1e9:8.4f}")
+print(f"{steps} steps in {tot:.3f}s -> {steps/tot:.2f} steps/s")
