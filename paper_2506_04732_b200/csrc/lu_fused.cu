@@ -51,74 +51,84 @@ struct LuArgs {
   int w;         // panel width
 };
 
+// Factor the panel A[k0:N, k0:k0+w] with partial pivoting inside one CTA,
+// one barrier per column: rows never move while factoring (a chosen pivot
+// row is flagged done and read in place), so each thread only touches its
+// own rows; the LAPACK-order interchanges are replayed on an index map and
+// applied when the panel is written back.
 __device__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv) {
   const int N = a.N, rows = N - k0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ double rv[32];
-  __shared__ int ri[32];
-  __shared__ double s_pval;
-  __shared__ int s_p;
+  __shared__ double rv[2][32];
+  __shared__ int ri[2][32];
+  int* cur = reinterpret_cast<int*>(sm + (size_t)rows * w);  // position -> physical row
+  int* pos = cur + rows;                                      // physical row -> position
+  unsigned char* done = reinterpret_cast<unsigned char*>(pos + rows);
   for (long long e = tid; e < (long long)rows * w; e += blockDim.x) {
     const int c = (int)(e / rows), r = (int)(e % rows);
     sm[e] = a.A[(long long)(k0 + c) * N + k0 + r];
   }
+  for (int r = tid; r < rows; r += blockDim.x) {
+    cur[r] = r;
+    pos[r] = r;
+    done[r] = 0;
+  }
   __syncthreads();
   for (int j = 0; j < w; ++j) {
-    double* cj = sm + (long long)j * rows;
+    const double* cj = sm + (long long)j * rows;
     double best = -1.0;
     int bi = rows;
-    for (int r = j + tid; r < rows; r += blockDim.x) amax_merge(best, bi, fabs(cj[r]), r);
+    for (int r = tid; r < rows; r += blockDim.x)
+      if (!done[r]) amax_merge(best, bi, fabs(cj[r]), r);
     for (int o = 16; o > 0; o >>= 1) {
       const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
       const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
       amax_merge(best, bi, v2, i2);
     }
     if (lane == 0) {
-      rv[warp] = best;
-      ri[warp] = bi;
+      rv[j & 1][warp] = best;
+      ri[j & 1][warp] = bi;
     }
     __syncthreads();
-    if (warp == 0) {
-      best = lane < nw ? rv[lane] : -1.0;
-      bi = lane < nw ? ri[lane] : rows;
-      for (int o = 16; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        amax_merge(best, bi, v2, i2);
-      }
-      if (lane == 0) {
-        s_p = bi;
-        s_piv[j] = bi;
-        a.piv[k0 + j] = k0 + bi;
-        s_pval = cj[bi];
-        if (cj[bi] == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
-      }
+    best = lane < nw ? rv[j & 1][lane] : -1.0;
+    bi = lane < nw ? ri[j & 1][lane] : rows;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      amax_merge(best, bi, v2, i2);
     }
-    __syncthreads();
-    const int p = s_p;
-    const double pv = s_pval;
-    if (p != j)
-      for (int c = tid; c < w; c += blockDim.x) {
-        double* cc = sm + (long long)c * rows;
-        const double t = cc[j];
-        cc[j] = cc[p];
-        cc[p] = t;
-      }
-    __syncthreads();
+    const int p = bi;  // physical pivot row (ties -> lowest physical index)
+    const double pv = cj[p];
+    if (tid == 0) {
+      // replay the interchange j <-> position of p (LAPACK order)
+      const int pp = pos[p];
+      a.piv[k0 + j] = k0 + pp;
+      const int rj = cur[j];
+      cur[j] = p;
+      cur[pp] = rj;
+      pos[p] = j;
+      pos[rj] = pp;
+      if (pv == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
+    }
     const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-    for (int r = j + 1 + tid; r < rows; r += blockDim.x) {
+    for (int r = tid; r < rows; r += blockDim.x) {
+      if (r == p) {
+        done[r] = 1;
+        continue;
+      }
+      if (done[r]) continue;
       const double l = pv != 0.0 ? cj[r] * inv : cj[r];
-      cj[r] = l;
+      sm[(long long)j * rows + r] = l;
       for (int c = j + 1; c < w; ++c) {
         double* cc = sm + (long long)c * rows;
-        cc[r] = fma(-l, cc[j], cc[r]);
+        cc[r] = fma(-l, cc[p], cc[r]);
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (long long e = tid; e < (long long)rows * w; e += blockDim.x) {
-    const int c = (int)(e / rows), r = (int)(e % rows);
-    a.A[(long long)(k0 + c) * N + k0 + r] = sm[e];
+    const int c = (int)(e / rows), i = (int)(e % rows);
+    a.A[(long long)(k0 + c) * N + k0 + i] = sm[(long long)c * rows + cur[i]];
   }
 }
 
@@ -279,7 +289,8 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
     T2S2_CUDA(cudaFuncSetAttribute(lu_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kPanelSmem));
   }
-  int w = (int)(kPanelSmem / (sizeof(double) * (size_t)N));
+  // panel doubles plus the row maps (2 ints + 1 byte per row)
+  int w = (int)((kPanelSmem - 9 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
   if (w < 1) return false;  // caller falls back to the multi-launch path
   LuArgs a{N, A, b, piv, info_dev, w};

@@ -55,3 +55,40 @@ def value_tol(res_a, res_b):
 def numerical_ranks(cores, tol=RANK_TOL):
     from oracle.tt_ops import tt_round
     return ranks_of(tt_round(cores, tol))
+
+
+def bond_spectra(cores):
+    """Singular values of every bond unfolding (left-to-right SVD sweep of
+    the right-orthonormalised train, i.e. tt_round with tol=0)."""
+    from oracle.tt_ops import right_orthonormalize
+
+    work = right_orthonormalize(cores)
+    out = []
+    for l in range(len(work) - 1):
+        r0, n, r1 = work[l].shape
+        u, s, vt = np.linalg.svd(work[l].reshape(r0 * n, r1), full_matrices=False)
+        out.append(s)
+        work[l + 1] = np.einsum("ab,bnc->anc", s[:, None] * vt, work[l + 1])
+    return out
+
+
+def ranks_agree(a, b, tol=RANK_TOL, band=10.0):
+    """Numerical bond ranks at ``tol`` (relative, tt_round's per-bond
+    threshold) agree, except where a singular value of either train lies
+    within a factor ``band`` of the threshold — that tail is the solver's
+    noise floor, not structure.  Returns (ok, per-bond (rank_a, rank_b))."""
+    d = len(a)
+    sa, sb = bond_spectra(a), bond_spectra(b)
+    detail, ok = [], True
+    for l in range(d - 1):
+        ta = tol * np.linalg.norm(sa[l]) / np.sqrt(d - 1)
+        tb = tol * np.linalg.norm(sb[l]) / np.sqrt(d - 1)
+        ka, kb = int(np.sum(sa[l] > ta)), int(np.sum(sb[l] > tb))
+        if ka != kb:
+            lo, hi = min(ka, kb), max(ka, kb)
+            cand = np.concatenate([sa[l][lo:hi], sb[l][lo:hi]])
+            thr = max(ta, tb)
+            if not np.all((cand > thr / band) & (cand < thr * band)):
+                ok = False
+        detail.append((ka, kb))
+    return ok, detail

@@ -241,6 +241,10 @@ def ref_march(recipe, n_keep):
         print(f"  step {k}: {walls[-1]:.2f}s ranks {state.ranks} res "
               f"{rep.residual_history[-1]:.3e} err {err:.3e}")
     st["walls"] = np.array(walls)
+    st["residual_tol"] = np.array(cfg.residual_tol)
+    st["rounding_tol"] = np.array(cfg.rounding_tol)
+    st["max_rank"] = np.array(cfg.max_rank)
+    st["step_tol"] = np.array(recipe.step_tol)
     return st
 
 
