@@ -30,13 +30,13 @@ __global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
                                        const double* __restrict__ pal,
                                        const double* __restrict__ ac,
                                        const double* __restrict__ par, double* __restrict__ B) {
-  const long long N = (long long)rx * n * ry;
-  const long long total = N * N;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long row = e % N, col = e / N;
-    const int y = (int)(row % ry), m = (int)((row / ry) % n), x = (int)(row / ((long long)ry * n));
-    const int Y = (int)(col % ry), nn = (int)((col / ry) % n), X = (int)(col / ((long long)ry * n));
+  const int N = rx * n * ry;
+  // one column per block-row of threads: (col, row) from 2-D indexing
+  for (int col = blockIdx.y; col < N; col += gridDim.y) {
+    const int Y = col % ry, nn = (col / ry) % n, X = col / (ry * n);
+    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < N; row += gridDim.x * blockDim.x) {
+    const int y = row % ry, m = (row / ry) % n, x = row / (ry * n);
+    const long long e = (long long)col * N + row;
     double s = 0.0;
     for (int a = 0; a < ra; ++a) {
       const double pl = pal[((long long)x * ra + a) * rx + X];
@@ -48,6 +48,7 @@ __global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
       s = fma(pl, t, s);
     }
     B[e] = s;
+    }
   }
 }
 
@@ -243,7 +244,7 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
   DTensor B({(int)N, (int)N});
   {
     LaunchScope ls("galerkin_build", 2.0*(double)N*N*ra*(rb+1), 8.0*(double)N*N);
-    galerkin_matrix_kernel<<<grid_of(N * N), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
+    galerkin_matrix_kernel<<<dim3(ceil_div(N, 256), N < 4096 ? (int)N : 4096), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
                                                                   par.p, B.p);
   }
   T2S2_CHECK_LAUNCH();

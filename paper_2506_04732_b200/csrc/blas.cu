@@ -83,15 +83,17 @@ struct PermArgs {
   long long in_stride[8];  // stride in the input of output axis k
 };
 
-__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out,
-                               long long n, PermArgs a) {
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n;
-       o += (long long)gridDim.x * blockDim.x) {
-    long long rem = o, off = 0;
+// 32-bit index math (every local tensor has < 2^31 entries).
+__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out, int n,
+                               PermArgs a) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+    unsigned rem = (unsigned)o;
+    unsigned off = 0;
     for (int k = a.nd - 1; k >= 0; --k) {
-      int i = (int)(rem % a.out_shape[k]);
-      rem /= a.out_shape[k];
-      off += i * a.in_stride[k];
+      const unsigned d = (unsigned)a.out_shape[k];
+      const unsigned q = rem / d;
+      off += (rem - q * d) * (unsigned)a.in_stride[k];
+      rem = q;
     }
     out[o] = in[off];
   }
@@ -230,7 +232,7 @@ DTensor permute(const DTensor& a, const std::vector<int>& perm) {
   long long n = (long long)a.size();
   {
     LaunchScope ls("permute", 0, 16.0*n);
-    permute_kernel<<<grid_for(n), 256, 0, stream()>>>(a.p, out.p, n, pa);
+    permute_kernel<<<grid_for(n), 256, 0, stream()>>>(a.p, out.p, (int)n, pa);
   }
   T2S2_CHECK_LAUNCH();
   return out;

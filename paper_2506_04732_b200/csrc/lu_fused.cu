@@ -21,6 +21,8 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "blas.h"
 #include "linalg.h"
@@ -34,6 +36,7 @@ constexpr int kThreads = 512;
 constexpr int kColBlock = 8;
 constexpr int kMaxPanel = 32;
 constexpr size_t kPanelSmem = 200 * 1024;
+constexpr int kMoveStride = 2 * (1 + 2 * 2 * kMaxPanel);
 
 __device__ __forceinline__ void amax_merge(double& v, int& i, double v2, int i2) {
   if (v2 > v || (v2 == v && i2 < i)) {
@@ -49,14 +52,23 @@ struct LuArgs {
   int* piv;      // N scratch (absolute pivot rows)
   int* info;     // 0 or 1 + first zero pivot
   int w;         // panel width
+  int* moves;    // per panel: count, then (dst, src) row offsets relative to k0
+  unsigned long long* prof;  // optional phase timers (ns): see lu_solve_fused
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Factor the panel A[k0:N, k0:k0+w] with partial pivoting inside one CTA,
 // one barrier per column: rows never move while factoring (a chosen pivot
 // row is flagged done and read in place), so each thread only touches its
 // own rows; the LAPACK-order interchanges are replayed on an index map and
 // applied when the panel is written back.
-__device__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv) {
+__device__ __noinline__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv,
+                                          int* mv) {
   const int N = a.N, rows = N - k0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ double rv[2][32];
@@ -64,9 +76,10 @@ __device__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_
   int* cur = reinterpret_cast<int*>(sm + (size_t)rows * w);  // position -> physical row
   int* pos = cur + rows;                                      // physical row -> position
   unsigned char* done = reinterpret_cast<unsigned char*>(pos + rows);
-  for (long long e = tid; e < (long long)rows * w; e += blockDim.x) {
-    const int c = (int)(e / rows), r = (int)(e % rows);
-    sm[e] = a.A[(long long)(k0 + c) * N + k0 + r];
+  for (int c = 0; c < w; ++c) {
+    const double* src = a.A + (long long)(k0 + c) * N + k0;
+    double* dst = sm + (long long)c * rows;
+    for (int r = tid; r < rows; r += blockDim.x) dst[r] = src[r];
   }
   for (int r = tid; r < rows; r += blockDim.x) {
     cur[r] = r;
@@ -111,94 +124,168 @@ __device__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_
       if (pv == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
     }
     const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
+    // multipliers of the thread's own live rows, then the rank-1 update in
+    // 4-column slabs (all loads of a slab issue before its stores)
     for (int r = tid; r < rows; r += blockDim.x) {
-      if (r == p) {
-        done[r] = 1;
-        continue;
-      }
-      if (done[r]) continue;
-      const double l = pv != 0.0 ? cj[r] * inv : cj[r];
-      sm[(long long)j * rows + r] = l;
-      for (int c = j + 1; c < w; ++c) {
-        double* cc = sm + (long long)c * rows;
-        cc[r] = fma(-l, cc[p], cc[r]);
+      if (r == p) done[r] = 1;
+      else if (!done[r])
+        sm[(long long)j * rows + r] = pv != 0.0 ? sm[(long long)j * rows + r] * inv
+                                                : sm[(long long)j * rows + r];
+    }
+    for (int c = j + 1; c < w; c += 4) {
+      const int nc4 = w - c < 4 ? w - c : 4;
+      double u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = q < nc4 ? sm[(long long)(c + q) * rows + p] : 0.0;
+      for (int r = tid; r < rows; r += blockDim.x) {
+        if (r == p || done[r]) continue;
+        const double l = sm[(long long)j * rows + r];
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = q < nc4 ? sm[(long long)(c + q) * rows + r] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nc4) sm[(long long)(c + q) * rows + r] = fma(-l, u[q], v[q]);
       }
     }
   }
   __syncthreads();
-  for (long long e = tid; e < (long long)rows * w; e += blockDim.x) {
-    const int c = (int)(e / rows), i = (int)(e % rows);
-    a.A[(long long)(k0 + c) * N + k0 + i] = sm[(long long)c * rows + cur[i]];
+  for (int c = 0; c < w; ++c) {
+    double* dst = a.A + (long long)(k0 + c) * N + k0;
+    const double* src = sm + (long long)c * rows;
+    for (int i = tid; i < rows; i += blockDim.x) dst[i] = src[cur[i]];
+  }
+  // rows whose position changed: at most 2w of them (the first w positions
+  // and the slots the pivots came from); other CTAs replay them per column
+  if (tid == 0) {
+    int m = 0;
+    for (int i = 0; i < w; ++i)
+      if (cur[i] != i) {
+        mv[1 + 2 * m] = i;
+        mv[2 + 2 * m] = cur[i];
+        ++m;
+      }
+    // displaced rows: physical row q (< w) that ended at position pos[q] >= w
+    for (int q = 0; q < w; ++q)
+      if (pos[q] >= w) {
+        mv[1 + 2 * m] = pos[q];
+        mv[2 + 2 * m] = q;
+        ++m;
+      }
+    mv[0] = m;
   }
 }
 
-// Interchanges, TRSM and rank-w update of the owned columns [c0, c1)
-// (at most kMaxPanel of them; column N is the right-hand side).
-__device__ void update_cols(const LuArgs& a, int k0, int w, int c0, int c1, double* sm) {
+// Interchanges, TRSM and rank-w update of the owned columns [c0, c1),
+// at most CB of them (column N is the right-hand side).  Loops over the
+// panel width stay rolled: the kernel must fit the instruction cache, since
+// every phase runs once per panel.
+template <int CB>
+__device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0, int c1,
+                                         double* sm, const int* mv) {
   const int N = a.N;
   const int tid = threadIdx.x;
   const int nc = c1 - c0;
   double* L11 = sm;                        // w x w (col-major)
-  double* U = sm + kMaxPanel * kMaxPanel;  // w x nc (row j, column c at j*kMaxPanel + c)
-  for (int c = tid; c < nc; c += blockDim.x) {
-    const int gc = c0 + c;
-    double* col = gc < N ? a.A + (long long)gc * N : a.b;
-    for (int j = 0; j < w; ++j) {
-      const int p = a.piv[k0 + j];
-      if (p != k0 + j) {
-        const double t = col[k0 + j];
-        col[k0 + j] = col[p];
-        col[p] = t;
+  double* U = sm + kMaxPanel * kMaxPanel;  // row j, column c at j * CB + c
+  {
+    // replay the panel's row moves: gather every moved value, then scatter
+    const int m = mv[0];
+    const int pairs = m * nc;
+    double v[4];
+    int dst[4], cc[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = tid + t * blockDim.x;
+      dst[t] = -1;
+      if (e < pairs) {
+        const int c = e / m, k = e % m;
+        const int gc = c0 + c;
+        const double* col = gc < N ? a.A + (long long)gc * N : a.b;
+        dst[t] = mv[1 + 2 * k];
+        cc[t] = c;
+        v[t] = col[k0 + mv[2 + 2 * k]];
       }
     }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (dst[t] >= 0) {
+        const int gc = c0 + cc[t];
+        double* col = gc < N ? a.A + (long long)gc * N : a.b;
+        col[k0 + dst[t]] = v[t];
+      }
   }
+  __syncthreads();
   for (int e = tid; e < w * w; e += blockDim.x) {
     const int c = e / w, r = e % w;
     L11[c * w + r] = a.A[(long long)(k0 + c) * N + k0 + r];
   }
-  __syncthreads();
-  for (int c = tid; c < nc; c += blockDim.x) {
+  for (int e = tid; e < w * nc; e += blockDim.x) {
+    const int c = e / w, j = e % w;
     const int gc = c0 + c;
-    double* col = gc < N ? a.A + (long long)gc * N : a.b;
-    double x[kMaxPanel];
-#pragma unroll
-    for (int j = 0; j < kMaxPanel; ++j) x[j] = j < w ? col[k0 + j] : 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxPanel; ++j) {
-      if (j < w) {
-#pragma unroll
-        for (int i = j + 1; i < kMaxPanel; ++i)
-          if (i < w) x[i] = fma(-L11[j * w + i], x[j], x[i]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kMaxPanel; ++j)
-      if (j < w) {
-        col[k0 + j] = x[j];
-        U[j * kMaxPanel + c] = x[j];
-      }
+    const double* col = gc < N ? a.A + (long long)gc * N : a.b;
+    U[j * CB + c] = col[k0 + j];
   }
   __syncthreads();
-  // A22[:, c0:c1] -= L21 U12: one thread per row keeps its L21 row in
-  // registers and sweeps the owned columns (U12 broadcast from smem).
+  // U12 = L11^{-1} A12: one warp per column, lane i holds row i
+  {
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int c = warp; c < nc; c += nwarps) {
+      double xi = lane < w ? U[lane * CB + c] : 0.0;
+      double lcol = 0.0;
+#pragma unroll 1
+      for (int j = 0; j < w; ++j) {
+        lcol = lane < w ? L11[j * w + lane] : 0.0;
+        const double xj = __shfl_sync(0xffffffffu, xi, j);
+        if (lane > j) xi = fma(-lcol, xj, xi);
+      }
+      if (lane < w) U[lane * CB + c] = xi;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < w * nc; e += blockDim.x) {
+    const int c = e / w, j = e % w;
+    const int gc = c0 + c;
+    double* col = gc < N ? a.A + (long long)gc * N : a.b;
+    col[k0 + j] = U[j * CB + c];
+  }
+  // A22[:, c0:c1] -= L21 U12: thread per row; its L21 row is prefetched into
+  // registers (independent loads), columns are processed 8 at a time.
   for (int r = k0 + w + tid; r < N; r += blockDim.x) {
     double l[kMaxPanel];
 #pragma unroll
     for (int j = 0; j < kMaxPanel; ++j) l[j] = j < w ? a.A[(long long)(k0 + j) * N + r] : 0.0;
-    for (int c = 0; c < nc; ++c) {
-      const int gc = c0 + c;
-      double* col = gc < N ? a.A + (long long)gc * N : a.b;
-      double acc = col[r];
+#pragma unroll 1
+    for (int cb = 0; cb < nc; cb += 8) {
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int gc = c0 + cb + c;
+        acc[c] = cb + c < nc ? (gc < N ? a.A[(long long)gc * N + r] : a.b[r]) : 0.0;
+      }
 #pragma unroll
       for (int j = 0; j < kMaxPanel; ++j)
-        if (j < w) acc = fma(-l[j], U[j * kMaxPanel + c], acc);
-      col[r] = acc;
+        if (j < w) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = fma(-l[j], U[j * CB + cb + c], acc[c]);
+        }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int gc = c0 + cb + c;
+        if (cb + c < nc) {
+          if (gc < N)
+            a.A[(long long)gc * N + r] = acc[c];
+          else
+            a.b[r] = acc[c];
+        }
+      }
     }
   }
   __syncthreads();
 }
 
-__device__ void back_substitute(const LuArgs& a, double* x) {
+__device__ __noinline__ void back_substitute(const LuArgs& a, double* x) {
   const int N = a.N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) x[i] = a.b[i];
@@ -247,18 +334,33 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) *a.info = 0;
     __syncthreads();
-    factor_panel(a, 0, N < a.w ? N : a.w, sm, s_piv);
+    factor_panel(a, 0, N < a.w ? N : a.w, sm, s_piv, a.moves);
   }
   grid.sync();
+  unsigned long long t0 = 0, acc_upd = 0, acc_fac = 0, acc_sync = 0, acc_work = 0;
   for (int k0 = 0; k0 < N; k0 += a.w) {
+    if (a.prof && threadIdx.x == 0) t0 = gtimer();
     const int w = N - k0 < a.w ? N - k0 : a.w;
     const int k1 = k0 + w;                               // next panel start
     const int w2 = N - k1 < a.w ? N - k1 : a.w;          // next panel width (0 at end)
     const int rest0 = k1 + w2;                           // columns for the other CTAs
+    const int pi = k0 / a.w;                             // panel index
+    const int* mv = a.moves + (pi & 1) * kMoveStride;
+    int* mv_next = a.moves + ((pi + 1) & 1) * kMoveStride;
     if (blockIdx.x == 0) {
       if (w2 > 0) {
-        update_cols(a, k0, w, k1, rest0, sm);
-        factor_panel(a, k1, w2, sm, s_piv);
+        update_cols<kMaxPanel>(a, k0, w, k1, rest0, sm, mv);
+        if (a.prof && threadIdx.x == 0) {
+          const unsigned long long t1 = gtimer();
+          acc_upd += t1 - t0;
+          t0 = t1;
+        }
+        factor_panel(a, k1, w2, sm, s_piv, mv_next);
+        if (a.prof && threadIdx.x == 0) {
+          const unsigned long long t1 = gtimer();
+          acc_fac += t1 - t0;
+          t0 = t1;
+        }
       }
     }
     const int workers = gridDim.x > 1 ? gridDim.x - 1 : 1;
@@ -269,10 +371,22 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
       for (int blk = wid; blk < nblk; blk += workers) {
         const int c0 = rest0 + blk * kColBlock;
         const int c1 = c0 + kColBlock < N + 1 ? c0 + kColBlock : N + 1;
-        update_cols(a, k0, w, c0, c1, sm);
+        update_cols<kColBlock>(a, k0, w, c0, c1, sm, mv);
+      }
+      if (a.prof && threadIdx.x == 0) {
+        const unsigned long long t1 = gtimer();
+        acc_work += t1 - t0;
+        t0 = t1;
       }
     }
     grid.sync();
+    if (a.prof && threadIdx.x == 0) acc_sync += gtimer() - t0;
+  }
+  if (a.prof && threadIdx.x == 0 && blockIdx.x < 2) {
+    a.prof[blockIdx.x * 4 + 0] = acc_upd;
+    a.prof[blockIdx.x * 4 + 1] = acc_fac;
+    a.prof[blockIdx.x * 4 + 2] = acc_work;
+    a.prof[blockIdx.x * 4 + 3] = acc_sync;
   }
   if (blockIdx.x == 0) back_substitute(a, sm);
 }
@@ -293,7 +407,14 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
   int w = (int)((kPanelSmem - 9 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
   if (w < 1) return false;  // caller falls back to the multi-launch path
-  LuArgs a{N, A, b, piv, info_dev, w};
+  int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride));
+  static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
+  unsigned long long* pbuf = nullptr;
+  if (prof) {
+    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(8));
+    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 64, stream()));
+  }
+  LuArgs a{N, A, b, piv, info_dev, w, moves, pbuf};
   void* params[] = {&a};
   {
     // algorithmic: 2/3 N^3 (factor) + 2 N^2 (solves); bytes: matrix read+write
@@ -301,6 +422,15 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
                    16.0 * (double)N * N);
     T2S2_CUDA(cudaLaunchCooperativeKernel((void*)lu_fused_kernel, dim3(g_num_sms), dim3(kThreads),
                                           params, kPanelSmem, stream()));
+  }
+  allocator().release(reinterpret_cast<double*>(moves));
+  if (prof) {
+    unsigned long long h[8];
+    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 64, cudaMemcpyDeviceToHost, stream()));
+    T2S2_CUDA(cudaStreamSynchronize(stream()));
+    fprintf(stderr, "lu N=%d w=%d cta0: upd %.1f fac %.1f sync %.1f us | cta1: work %.1f sync %.1f us\n",
+            N, w, h[0] / 1e3, h[1] / 1e3, h[3] / 1e3, h[6] / 1e3, h[7] / 1e3);
+    allocator().release(reinterpret_cast<double*>(pbuf));
   }
   return true;
 }
