@@ -423,11 +423,13 @@ def run_b200(args):
     cpu = None
     if not args.no_cpu_baseline and args.cpu_sample_steps > 0:
         problem = oracle_problem(recipe)
-        el, _ = cpu_march(recipe, args.cpu_sample_steps, problem=problem)
+        _, st = cpu_march(recipe, W, problem=problem)          # untimed warm-up steps
+        el, _ = cpu_march(recipe, args.cpu_sample_steps, start_step=W + 1, state=st,
+                          problem=problem)
         cpu = {"value": args.cpu_sample_steps / el, "unit": UNIT, "cores": blas_threads(),
                "kind": "port",
-               "sample": f"first {args.cpu_sample_steps} steps of the same config-2 march, "
-                         "oracle port (numpy/BLAS) on this host"}
+               "sample": f"steps {W + 1}..{W + args.cpu_sample_steps} of the same config-2 "
+                         f"march after {W} untimed steps, oracle port (numpy/BLAS) on this host"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
