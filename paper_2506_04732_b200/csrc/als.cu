@@ -56,10 +56,10 @@ __global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
 __global__ void gram_diag_kernel(int ra, int n, int rb, const double* __restrict__ ac,
                                  double* __restrict__ G) {
   const long long total = (long long)ra * ra * n * rb * rb;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)total;
+       e += gridDim.x * blockDim.x) {
     const int Q = (int)(e % rb);
-    long long t = e / rb;
+    int t = e / rb;
     const int P = (int)(t % rb);
     t /= rb;
     const int m = (int)(t % n);
@@ -77,8 +77,8 @@ __global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
                                    const double* __restrict__ pnl, const double* __restrict__ G,
                                    const double* __restrict__ pnr, double* __restrict__ out) {
   const long long total = (long long)rx * n * ry;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)total;
+       e += gridDim.x * blockDim.x) {
     const int y = (int)(e % ry), m = (int)((e / ry) % n), x = (int)(e / ((long long)ry * n));
     double s = 0.0;
     for (int a = 0; a < ra; ++a)
@@ -532,6 +532,8 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     sw.lg[0] = ones({1, 1, 1});
     sw.lb[0] = ones({1, 1});
 
+    DTensor end_grad;  // residual gradient of the last forward visit
+    int end_choice = 0;
     for (int l = 0; l < d; ++l) {
       DTensor u, grad;
       int choice;
@@ -539,6 +541,8 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       rep.choices.push_back(choice);
       if (l == d - 1) {
         cores[l] = std::move(u);
+        end_grad = std::move(grad);
+        end_choice = choice;
         break;
       }
       Split sp = split_forward(u, &grad, cfg, d);
@@ -558,7 +562,17 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     for (int l = d - 1; l >= 0; --l) {
       DTensor u, grad;
       int choice;
-      sw.update(l, cores, current_res, u, grad, choice);
+      if (l == d - 1 && d > 1 && end_choice == 1) {
+        // The backward pass re-visits core d-1 with unchanged interfaces:
+        // its Galerkin system is the one just solved, so the (deterministic)
+        // solve would return the current core bit for bit, q_gal == q_old
+        // and the candidate is accepted (tt_solver.py:383-387).  Reuse it.
+        u = cores[l].clone();
+        grad = std::move(end_grad);
+        choice = 1;
+      } else {
+        sw.update(l, cores, current_res, u, grad, choice);
+      }
       rep.choices.push_back(choice);
       if (l == 0) {
         cores[l] = std::move(u);

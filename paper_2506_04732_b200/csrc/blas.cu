@@ -120,8 +120,8 @@ __global__ void axpby_kernel(double a, const double* x, double b, double* y, lon
 __global__ void copy2d_kernel(double* dst, int ldd, const double* src, int lds, int rows,
                               int cols) {
   long long n = (long long)rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
+       e += gridDim.x * blockDim.x) {
     int r = (int)(e / cols), c = (int)(e % cols);
     dst[(long long)r * ldd + c] = src[(long long)r * lds + c];
   }
@@ -160,8 +160,8 @@ __global__ void sum_final_kernel(const double* part, int n, double* out) {
 
 __global__ void transpose_kernel(const double* in, double* out, int rows, int cols) {
   long long n = (long long)rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
+       e += gridDim.x * blockDim.x) {
     int r = (int)(e / cols), c = (int)(e % cols);
     out[(long long)c * rows + r] = in[e];
   }

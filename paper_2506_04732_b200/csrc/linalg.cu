@@ -14,6 +14,7 @@ namespace t2s2 {
 namespace {
 
 constexpr int kQrThreads = 512;
+constexpr size_t kSmemCap = 200 * 1024;
 
 __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -22,13 +23,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // A row-major (m x n) -> Q row-major (m x k), R row-major (k x n).
 // W: column-major m x n scratch, Qc: column-major m x k scratch, tau: k.
+// SM = true: the working copies live in dynamic shared memory (the caller
+// checked the size), so every column step is LDS/STS instead of L2 trips.
+template <bool SM>
 __global__ void __launch_bounds__(kQrThreads)
-    qr_kernel(int m, int n, const double* __restrict__ A, double* W, double* Qc, double* tau,
+    qr_kernel(int m, int n, const double* __restrict__ A, double* Wg, double* Qg, double* tg,
               double* Q, double* R) {
+  extern __shared__ double qsm[];
   const int k = m < n ? m : n;
+  double* W = SM ? qsm : Wg;
+  double* Qc = SM ? qsm + (size_t)m * n : Qg;
+  double* tau = SM ? qsm + (size_t)m * n + (size_t)m * k : tg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ double sh_tau, sh_scal, sh_beta;
-  for (long long e = tid; e < (long long)m * n; e += blockDim.x) {
+  for (int e = tid; e < (int)m * n; e += blockDim.x) {
     int i = (int)(e / n), j = (int)(e % n);
     W[(long long)j * m + i] = A[e];
   }
@@ -76,12 +84,12 @@ __global__ void __launch_bounds__(kQrThreads)
     __syncthreads();
   }
   // R
-  for (long long e = tid; e < (long long)k * n; e += blockDim.x) {
+  for (int e = tid; e < (int)k * n; e += blockDim.x) {
     int r = (int)(e / n), c = (int)(e % n);
     R[e] = c >= r ? W[(long long)c * m + r] : 0.0;
   }
   // Q = H_0 ... H_{k-1} [I_k; 0], accumulated backwards.
-  for (long long e = tid; e < (long long)m * k; e += blockDim.x) {
+  for (int e = tid; e < (int)m * k; e += blockDim.x) {
     int c = (int)(e / m), i = (int)(e % m);
     Qc[e] = i == c ? 1.0 : 0.0;
   }
@@ -101,7 +109,7 @@ __global__ void __launch_bounds__(kQrThreads)
     }
     __syncthreads();
   }
-  for (long long e = tid; e < (long long)m * k; e += blockDim.x) {
+  for (int e = tid; e < (int)m * k; e += blockDim.x) {
     int i = (int)(e / k), c = (int)(e % k);
     Q[e] = Qc[(long long)c * m + i];
   }
@@ -111,12 +119,21 @@ __global__ void __launch_bounds__(kQrThreads)
 // p >= q).  Circle-method ordering: each round rotates q/2 disjoint column
 // pairs, one warp per pair.  Outputs U (row-major p x q), s (q), Vt
 // (row-major q x q), singular values sorted descending.
+template <bool SM>
 __global__ void __launch_bounds__(kQrThreads)
-    jacobi_kernel(int p, int q, double* G, double* V, int* perm, double* U, double* s,
+    jacobi_kernel(int p, int q, double* Gg, double* Vg, int* perm, double* U, double* s,
                   double* Vt) {
+  extern __shared__ double jsm[];
+  double* G = Gg;
+  double* V = SM ? jsm + (size_t)p * q : Vg;
+  if (SM) {
+    for (int e = threadIdx.x; e < p * q; e += blockDim.x) jsm[e] = Gg[e];
+    G = jsm;
+    __syncthreads();
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ int sh_rot;
-  for (long long e = tid; e < (long long)q * q; e += blockDim.x) {
+  for (int e = tid; e < (int)q * q; e += blockDim.x) {
     int c = (int)(e / q), i = (int)(e % q);
     V[e] = i == c ? 1.0 : 0.0;
   }
@@ -207,12 +224,12 @@ __global__ void __launch_bounds__(kQrThreads)
   __syncthreads();
   for (int j = tid; j < q; j += blockDim.x) s[j] = sv[j];
   __syncthreads();
-  for (long long e = tid; e < (long long)p * q; e += blockDim.x) {
+  for (int e = tid; e < (int)p * q; e += blockDim.x) {
     int i = (int)(e / q), j = (int)(e % q);
     double sj = s[j];
     U[e] = sj > 0.0 ? G[(long long)perm[j] * p + i] / sj : 0.0;
   }
-  for (long long e = tid; e < (long long)q * q; e += blockDim.x) {
+  for (int e = tid; e < (int)q * q; e += blockDim.x) {
     int j = (int)(e / q), i = (int)(e % q);
     Vt[e] = V[(long long)perm[j] * q + i];
   }
@@ -230,7 +247,18 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
   double* tau = allocator().alloc(k);
   {
     LaunchScope ls("qr", 4.0*m*(double)n*(m<n?m:n), 16.0*m*(double)n);
-    qr_kernel<<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+    const size_t need = ((size_t)m * n + (size_t)m * k + k) * sizeof(double);
+    if (need <= kSmemCap) {
+      static bool attr = false;
+      if (!attr) {
+        T2S2_CUDA(cudaFuncSetAttribute(qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemCap));
+        attr = true;
+      }
+      qr_kernel<true><<<1, kQrThreads, need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+    } else {
+      qr_kernel<false><<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+    }
   }
   T2S2_CHECK_LAUNCH();
   allocator().release(W);
@@ -249,7 +277,18 @@ void jacobi_svd(int p, int q, double* G, DTensor& U, DTensor& s, DTensor& Vt) {
   int* perm = reinterpret_cast<int*>(allocator().alloc(q));
   {
     LaunchScope ls("svd_jacobi", 0, 0);
-    jacobi_kernel<<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+    const size_t need = ((size_t)p * q + (size_t)q * q + q) * sizeof(double);
+    if (need <= kSmemCap) {
+      static bool attr = false;
+      if (!attr) {
+        T2S2_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+        attr = true;
+      }
+      jacobi_kernel<true><<<1, kQrThreads, need, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+    } else {
+      jacobi_kernel<false><<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+    }
   }
   T2S2_CHECK_LAUNCH();
   allocator().release(V);

@@ -35,6 +35,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kColBlock = 8;
 constexpr int kMaxPanel = 32;
+constexpr int kRowsPerThread = 5;  // rows <= 5 * 512 = 2560
 constexpr size_t kPanelSmem = 200 * 1024;
 constexpr int kMoveStride = 2 * (1 + 2 * 2 * kMaxPanel);
 
@@ -62,20 +63,99 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Column loop of the panel factorisation: thread t owns rows t + k*kThreads
+// (k < RPT); liveness and multipliers stay in registers, values in smem.
+template <int RPT>
+__device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int* s_piv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kThreads / 32;
+  __shared__ unsigned rh[2][32], rl[2][32];
+  __shared__ int ri[2][32];
+  bool live[RPT];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) live[k] = tid + k * kThreads < rows;
+  for (int j = 0; j < w; ++j) {
+    const double* cj = sm + j * rows;
+    // argmax |a_rj| as integer keys: the IEEE bits of |a| order like |a|,
+    // so three single-instruction warp reductions (max hi word, max lo word,
+    // min row) replace a 5-step shuffle tree per level; ties -> lowest row
+    unsigned long long kb = 0ull;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < RPT; ++k)
+      if (live[k]) {
+        const unsigned long long b = __double_as_longlong(fabs(cj[tid + k * kThreads]));
+        if (b > kb || bi == 0x7fffffff) {
+          kb = b;
+          bi = tid + k * kThreads;
+        }
+      }
+    unsigned hi = bi == 0x7fffffff ? 0u : (unsigned)(kb >> 32);
+    unsigned lo = bi == 0x7fffffff ? 0u : (unsigned)kb;
+    {
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      const int mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
+      if (lane == 0) {
+        rh[j & 1][warp] = mh;
+        rl[j & 1][warp] = ml;
+        ri[j & 1][warp] = mi;
+      }
+    }
+    __syncthreads();
+    hi = lane < nw ? rh[j & 1][lane] : 0u;
+    lo = lane < nw ? rl[j & 1][lane] : 0u;
+    const int wi = lane < nw ? ri[j & 1][lane] : 0x7fffffff;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    bi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? wi : 0x7fffffff);
+    const int p = bi;  // physical pivot row (ties -> lowest physical index)
+    const double pv = cj[p];
+    if (tid == 0) s_piv[j] = p;
+    // LAPACK dgetf2 scales by the reciprocal; a zero pivot leaves the column
+    const double inv = pv != 0.0 ? __drcp_rn(pv) : 1.0;
+    double lk[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      if (tid + k * kThreads == p) live[k] = false;
+      lk[k] = 0.0;
+      if (live[k]) {
+        lk[k] = cj[tid + k * kThreads] * inv;
+        sm[j * rows + tid + k * kThreads] = lk[k];
+      }
+    }
+    // rank-1 update, 4 columns at a time: every load of a block issues
+    // before its stores (shared stores would otherwise serialise the loop)
+    for (int c = j + 1; c < w; c += 4) {
+      const int nb = w - c < 4 ? w - c : 4;
+      double u[4], v[RPT][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = q < nb ? sm[(c + q) * rows + p] : 0.0;
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          v[k][q] = live[k] && q < nb ? sm[(c + q) * rows + tid + k * kThreads] : 0.0;
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (live[k] && q < nb) sm[(c + q) * rows + tid + k * kThreads] = fma(-lk[k], u[q], v[k][q]);
+    }
+  }
+}
+
 // Factor the panel A[k0:N, k0:k0+w] with partial pivoting inside one CTA,
 // one barrier per column: rows never move while factoring (a chosen pivot
 // row is flagged done and read in place), so each thread only touches its
 // own rows; the LAPACK-order interchanges are replayed on an index map and
 // applied when the panel is written back.
-__device__ __noinline__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv,
+__device__ __forceinline__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv,
                                           int* mv) {
   const int N = a.N, rows = N - k0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ double rv[2][32];
-  __shared__ int ri[2][32];
+  const int tid = threadIdx.x;
   int* cur = reinterpret_cast<int*>(sm + (size_t)rows * w);  // position -> physical row
   int* pos = cur + rows;                                      // physical row -> position
-  unsigned char* done = reinterpret_cast<unsigned char*>(pos + rows);
   for (int c = 0; c < w; ++c) {
     const double* src = a.A + (long long)(k0 + c) * N + k0;
     double* dst = sm + (long long)c * rows;
@@ -84,36 +164,23 @@ __device__ __noinline__ void factor_panel(const LuArgs& a, int k0, int w, double
   for (int r = tid; r < rows; r += blockDim.x) {
     cur[r] = r;
     pos[r] = r;
-    done[r] = 0;
   }
   __syncthreads();
-  for (int j = 0; j < w; ++j) {
-    const double* cj = sm + (long long)j * rows;
-    double best = -1.0;
-    int bi = rows;
-    for (int r = tid; r < rows; r += blockDim.x)
-      if (!done[r]) amax_merge(best, bi, fabs(cj[r]), r);
-    for (int o = 16; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      amax_merge(best, bi, v2, i2);
-    }
-    if (lane == 0) {
-      rv[j & 1][warp] = best;
-      ri[j & 1][warp] = bi;
-    }
-    __syncthreads();
-    best = lane < nw ? rv[j & 1][lane] : -1.0;
-    bi = lane < nw ? ri[j & 1][lane] : rows;
-    for (int o = 16; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-      amax_merge(best, bi, v2, i2);
-    }
-    const int p = bi;  // physical pivot row (ties -> lowest physical index)
-    const double pv = cj[p];
-    if (tid == 0) {
-      // replay the interchange j <-> position of p (LAPACK order)
+  if (rows <= kThreads)
+    factor_columns<1>(rows, w, sm, s_piv);
+  else if (rows <= 2 * kThreads)
+    factor_columns<2>(rows, w, sm, s_piv);
+  else if (rows <= 3 * kThreads)
+    factor_columns<3>(rows, w, sm, s_piv);
+  else if (rows <= 4 * kThreads)
+    factor_columns<4>(rows, w, sm, s_piv);
+  else
+    factor_columns<5>(rows, w, sm, s_piv);
+  // replay the interchanges in LAPACK order on the index maps
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < w; ++j) {
+      const int p = s_piv[j];
       const int pp = pos[p];
       a.piv[k0 + j] = k0 + pp;
       const int rj = cur[j];
@@ -121,32 +188,7 @@ __device__ __noinline__ void factor_panel(const LuArgs& a, int k0, int w, double
       cur[pp] = rj;
       pos[p] = j;
       pos[rj] = pp;
-      if (pv == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
-    }
-    const double inv = pv != 0.0 ? 1.0 / pv : 0.0;
-    // multipliers of the thread's own live rows, then the rank-1 update in
-    // 4-column slabs (all loads of a slab issue before its stores)
-    for (int r = tid; r < rows; r += blockDim.x) {
-      if (r == p) done[r] = 1;
-      else if (!done[r])
-        sm[(long long)j * rows + r] = pv != 0.0 ? sm[(long long)j * rows + r] * inv
-                                                : sm[(long long)j * rows + r];
-    }
-    for (int c = j + 1; c < w; c += 4) {
-      const int nc4 = w - c < 4 ? w - c : 4;
-      double u[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) u[q] = q < nc4 ? sm[(long long)(c + q) * rows + p] : 0.0;
-      for (int r = tid; r < rows; r += blockDim.x) {
-        if (r == p || done[r]) continue;
-        const double l = sm[(long long)j * rows + r];
-        double v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = q < nc4 ? sm[(long long)(c + q) * rows + r] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < nc4) sm[(long long)(c + q) * rows + r] = fma(-l, u[q], v[q]);
-      }
+      if (sm[j * rows + p] == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
     }
   }
   __syncthreads();
@@ -181,7 +223,7 @@ __device__ __noinline__ void factor_panel(const LuArgs& a, int k0, int w, double
 // panel width stay rolled: the kernel must fit the instruction cache, since
 // every phase runs once per panel.
 template <int CB>
-__device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0, int c1,
+__device__ __forceinline__ void update_cols(const LuArgs& a, int k0, int w, int c0, int c1,
                                          double* sm, const int* mv) {
   const int N = a.N;
   const int tid = threadIdx.x;
@@ -227,6 +269,8 @@ __device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0,
     const double* col = gc < N ? a.A + (long long)gc * N : a.b;
     U[j * CB + c] = col[k0 + j];
   }
+  // rows w..31 of U take part in the 16-wide register blocks: keep them zero
+  for (int e = tid; e < (kMaxPanel - w) * CB; e += blockDim.x) U[w * CB + e] = 0.0;
   __syncthreads();
   // U12 = L11^{-1} A12: one warp per column, lane i holds row i
   {
@@ -253,9 +297,6 @@ __device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0,
   // A22[:, c0:c1] -= L21 U12: thread per row; its L21 row is prefetched into
   // registers (independent loads), columns are processed 8 at a time.
   for (int r = k0 + w + tid; r < N; r += blockDim.x) {
-    double l[kMaxPanel];
-#pragma unroll
-    for (int j = 0; j < kMaxPanel; ++j) l[j] = j < w ? a.A[(long long)(k0 + j) * N + r] : 0.0;
 #pragma unroll 1
     for (int cb = 0; cb < nc; cb += 8) {
       double acc[8];
@@ -264,12 +305,17 @@ __device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0,
         const int gc = c0 + cb + c;
         acc[c] = cb + c < nc ? (gc < N ? a.A[(long long)gc * N + r] : a.b[r]) : 0.0;
       }
+#pragma unroll 1
+      for (int j0 = 0; j0 < w; j0 += 16) {
+        double l[16];
 #pragma unroll
-      for (int j = 0; j < kMaxPanel; ++j)
-        if (j < w) {
+        for (int j = 0; j < 16; ++j)
+          l[j] = j0 + j < w ? a.A[(long long)(k0 + j0 + j) * N + r] : 0.0;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[c] = fma(-l[j], U[j * CB + cb + c], acc[c]);
-        }
+        for (int j = 0; j < 16; ++j)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = fma(-l[j], U[(j0 + j) * CB + cb + c], acc[c]);
+      }
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int gc = c0 + cb + c;
@@ -285,7 +331,7 @@ __device__ __noinline__ void update_cols(const LuArgs& a, int k0, int w, int c0,
   __syncthreads();
 }
 
-__device__ __noinline__ void back_substitute(const LuArgs& a, double* x) {
+__device__ __forceinline__ void back_substitute(const LuArgs& a, double* x) {
   const int N = a.N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < N; i += blockDim.x) x[i] = a.b[i];
@@ -331,41 +377,37 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
   extern __shared__ double sm[];
   __shared__ int s_piv[kMaxPanel];
   const int N = a.N;
-  if (blockIdx.x == 0) {
-    if (threadIdx.x == 0) *a.info = 0;
-    __syncthreads();
-    factor_panel(a, 0, N < a.w ? N : a.w, sm, s_piv, a.moves);
-  }
-  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.info = 0;
+  __syncthreads();
   unsigned long long t0 = 0, acc_upd = 0, acc_fac = 0, acc_sync = 0, acc_work = 0;
-  for (int k0 = 0; k0 < N; k0 += a.w) {
+  // iteration k0 = -a.w only factors panel 0; iteration k0 >= 0 applies
+  // panel [k0, k0+w) while CTA 0 prepares panel [k1, k1+w2).
+  for (int k0 = -a.w; k0 < N; k0 += a.w) {
     if (a.prof && threadIdx.x == 0) t0 = gtimer();
-    const int w = N - k0 < a.w ? N - k0 : a.w;
-    const int k1 = k0 + w;                               // next panel start
+    const int w = k0 < 0 ? 0 : (N - k0 < a.w ? N - k0 : a.w);
+    const int k1 = k0 < 0 ? 0 : k0 + w;                 // next panel start
     const int w2 = N - k1 < a.w ? N - k1 : a.w;          // next panel width (0 at end)
     const int rest0 = k1 + w2;                           // columns for the other CTAs
-    const int pi = k0 / a.w;                             // panel index
-    const int* mv = a.moves + (pi & 1) * kMoveStride;
-    int* mv_next = a.moves + ((pi + 1) & 1) * kMoveStride;
-    if (blockIdx.x == 0) {
-      if (w2 > 0) {
-        update_cols<kMaxPanel>(a, k0, w, k1, rest0, sm, mv);
-        if (a.prof && threadIdx.x == 0) {
-          const unsigned long long t1 = gtimer();
-          acc_upd += t1 - t0;
-          t0 = t1;
-        }
-        factor_panel(a, k1, w2, sm, s_piv, mv_next);
-        if (a.prof && threadIdx.x == 0) {
-          const unsigned long long t1 = gtimer();
-          acc_fac += t1 - t0;
-          t0 = t1;
-        }
+    const int pi = k0 < 0 ? -1 : k0 / a.w;               // panel index
+    const int* mv = a.moves + ((pi + 2) & 1) * kMoveStride;
+    int* mv_next = a.moves + ((pi + 3) & 1) * kMoveStride;
+    if (blockIdx.x == 0 && w2 > 0) {
+      if (w > 0) update_cols<kMaxPanel>(a, k0, w, k1, rest0, sm, mv);
+      if (a.prof && threadIdx.x == 0) {
+        const unsigned long long t1 = gtimer();
+        acc_upd += t1 - t0;
+        t0 = t1;
+      }
+      factor_panel(a, k1, w2, sm, s_piv, mv_next);
+      if (a.prof && threadIdx.x == 0) {
+        const unsigned long long t1 = gtimer();
+        acc_fac += t1 - t0;
+        t0 = t1;
       }
     }
     const int workers = gridDim.x > 1 ? gridDim.x - 1 : 1;
     const int wid = gridDim.x > 1 ? (int)blockIdx.x - 1 : 0;
-    if (gridDim.x == 1 || blockIdx.x > 0) {
+    if (w > 0 && (gridDim.x == 1 || blockIdx.x > 0)) {
       const int ncols = N + 1 - rest0;
       const int nblk = (ncols + kColBlock - 1) / kColBlock;
       for (int blk = wid; blk < nblk; blk += workers) {
@@ -406,13 +448,13 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
   // panel doubles plus the row maps (2 ints + 1 byte per row)
   int w = (int)((kPanelSmem - 9 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
-  if (w < 1) return false;  // caller falls back to the multi-launch path
+  if (w < 1 || N > kRowsPerThread * kThreads) return false;  // multi-launch fallback
   int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride));
   static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
   unsigned long long* pbuf = nullptr;
   if (prof) {
-    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(8));
-    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 64, stream()));
+    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
+    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
   }
   LuArgs a{N, A, b, piv, info_dev, w, moves, pbuf};
   void* params[] = {&a};
@@ -425,11 +467,12 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
   }
   allocator().release(reinterpret_cast<double*>(moves));
   if (prof) {
-    unsigned long long h[8];
-    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 64, cudaMemcpyDeviceToHost, stream()));
+    unsigned long long h[16];
+    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
     T2S2_CUDA(cudaStreamSynchronize(stream()));
     fprintf(stderr, "lu N=%d w=%d cta0: upd %.1f fac %.1f sync %.1f us | cta1: work %.1f sync %.1f us\n",
             N, w, h[0] / 1e3, h[1] / 1e3, h[3] / 1e3, h[6] / 1e3, h[7] / 1e3);
+
     allocator().release(reinterpret_cast<double*>(pbuf));
   }
   return true;

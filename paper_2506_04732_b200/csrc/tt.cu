@@ -10,8 +10,8 @@ namespace {
 
 __global__ void scale_rows_kernel(double* X, int rows, int cols, int ld, const double* s) {
   long long n = (long long)rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
+       e += gridDim.x * blockDim.x) {
     int r = (int)(e / cols), c = (int)(e % cols);
     X[(long long)r * ld + c] *= s[r];
   }
@@ -19,8 +19,8 @@ __global__ void scale_rows_kernel(double* X, int rows, int cols, int ld, const d
 
 __global__ void scale_cols_kernel(double* X, int rows, int cols, int ld, const double* s) {
   long long n = (long long)rows * cols;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
+       e += gridDim.x * blockDim.x) {
     int r = (int)(e / cols), c = (int)(e % cols);
     X[(long long)r * ld + c] *= s[c];
   }
@@ -30,10 +30,10 @@ __global__ void scale_cols_kernel(double* X, int rows, int cols, int ld, const d
 __global__ void place_block_kernel(double* out, int r0o, int mid, int r1o, const double* in,
                                    int r0i, int r1i, int off0, int off1, double scale) {
   long long n = (long long)r0i * mid * r1i;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
+       e += gridDim.x * blockDim.x) {
     int c = (int)(e % r1i);
-    long long t = e / r1i;
+    int t = e / r1i;
     int m = (int)(t % mid);
     int a = (int)(t / mid);
     out[((long long)(a + off0) * mid + m) * r1o + (c + off1)] = scale * in[e];
