@@ -213,3 +213,20 @@ def test_dense_local_solve_singular(pk):
     a = np.ones((4, 4))
     with pytest.raises(ValueError):
         _native.dense_solve(a, np.ones(4))
+
+
+def test_config4_sweep_small_matches_reference(golden, pk):
+    """Config 4 scaled (d=3, n=13, four seeded boundary-layer solves) through
+    the sweep driver on the device."""
+    from paper_2506_04732_b200 import sweep, workloads as wl
+
+    z = golden("config4_small.npz")
+    recipes = wl.sweep_recipes(count=int(z["count"]), dims=3, degree=12)
+    res = sweep.run_sweep(recipes, overrides={"max_sweeps": int(z["sweeps"])})
+    for i in range(int(z["count"])):
+        got, ref = res[i], np.array(z[f"res{i}"])
+        assert got["converged"] == bool(z[f"conv{i}"])
+        want = get_train(z, f"x{i}")
+        assert rel_diff(got["x"], want) <= value_tol(got["residuals"][-1], ref[-1])
+        ok, det = ranks_agree(got["x"], want)
+        assert ok, (i, det)

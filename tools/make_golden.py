@@ -206,6 +206,27 @@ def steady_config(index, fname, **over):
     save(fname, st)
 
 
+def sweep_small(fname, count=4, sweeps=30):
+    """Config 4 scaled: d=3, n=13, four seeded boundary-layer solves, a
+    bounded number of sweeps (the full d=6 solves take hours on the CPU)."""
+    st = {}
+    for i, r in enumerate(wl.sweep_recipes(count=count, dims=3, degree=12)):
+        a, b, exact = ref_steady(r)
+        cfg = rsol.SolverConfig(**r.solver, max_sweeps=sweeps)
+        x0 = rsol._default_initial_guess(b, cfg, np.random.default_rng(cfg.seed))
+        x, rep = rsol.solve(a, b, cfg=cfg)
+        put_train(st, f"a{i}", a.cores)
+        put_train(st, f"b{i}", b.cores)
+        put_train(st, f"x{i}", x.cores)
+        st[f"res{i}"] = np.array(rep.residual_history)
+        st[f"conv{i}"] = np.array(rep.converged)
+        st[f"eps{i}"] = np.array(r.eps)
+        print(fname, i, f"eps {r.eps:.2e}", x.ranks, rep.residual_history)
+    st["count"] = np.array(count)
+    st["sweeps"] = np.array(sweeps)
+    save(fname, st)
+
+
 def ref_march(recipe, n_keep):
     d = recipe.dims
     spec = spec_of(d, recipe.degree, recipe.eps, recipe.beta, 0.0, rhs=0.0)
@@ -269,6 +290,10 @@ if __name__ == "__main__":
         steady_config(0, "config0.npz")
     if "cfg1s" in which:
         steady_config(1, "config1_small.npz", degree=12)
+    if "cfg1" in which:
+        steady_config(1, "config1.npz")
+    if "cfg4s" in which:
+        sweep_small("config4_small.npz")
     if "cfg2" in which:
         march_config(2, "config2_steps.npz", 3)
     if "cfg2s" in which:
