@@ -15,61 +15,100 @@ namespace t2s2 {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16;
-
+// Tile TM x TN x TK, 256 threads on a 16x16 grid (RM x RN outputs each).
+// The next K-tile is fetched into registers while the current one is
+// consumed from shared memory, so each tile costs one exposed L2 latency at
+// most; small problems use 32x32x32 tiles to spread over more SMs.
+template <int TM, int TN, int TK>
 __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
                                                    double alpha, const double* __restrict__ A,
                                                    int lda, long long sA,
                                                    const double* __restrict__ B, int ldb,
                                                    long long sB, double beta, double* C, int ldc,
                                                    long long sC) {
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
+  constexpr int PA = TM * TK / 256, PB = TK * TN / 256, RM = TM / 16, RN = TN / 16;
+  __shared__ double As[TK][TM + 1];
+  __shared__ double Bs[TK][TN + 1];
   A += blockIdx.z * sA;
   B += blockIdx.z * sB;
   C += blockIdx.z * sC;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
-  double acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += BK) {
+  const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
+  double ra[PA], rb[PB];
+  auto fetch = [&](int k0) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      int e = threadIdx.x + t * 256;  // 0..1023
-      // A tile: BM x BK
-      int ar = e / BK, ak = e % BK;
-      int gi = row0 + ar, gk = k0 + ak;
-      double va = 0.0;
-      if (gi < M && gk < K) va = ta ? A[(long long)gk * lda + gi] : A[(long long)gi * lda + gk];
-      As[ak][ar] = va;
-      // B tile: BK x BN
-      int bk = e / BN, bc = e % BN;
-      int gk2 = k0 + bk, gj = col0 + bc;
-      double vb = 0.0;
-      if (gk2 < K && gj < N) vb = tb ? B[(long long)gj * ldb + gk2] : B[(long long)gk2 * ldb + gj];
-      Bs[bk][bc] = vb;
+    for (int t = 0; t < PA; ++t) {
+      const int e = threadIdx.x + t * 256;
+      int ar, ak;
+      if (ta) {  // A^T: contiguous along rows of op(A) -> consecutive threads walk i
+        ar = e % TM;
+        ak = e / TM;
+      } else {
+        ar = e / TK;
+        ak = e % TK;
+      }
+      const int gi = row0 + ar, gk = k0 + ak;
+      ra[t] = (gi < M && gk < K) ? (ta ? A[(long long)gk * lda + gi] : A[(long long)gi * lda + gk])
+                                 : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      const int e = threadIdx.x + t * 256;
+      int bk, bc;
+      if (tb) {
+        bk = e % TK;
+        bc = e / TK;
+      } else {
+        bk = e / TN;
+        bc = e % TN;
+      }
+      const int gk = k0 + bk, gj = col0 + bc;
+      rb[t] = (gk < K && gj < N) ? (tb ? B[(long long)gj * ldb + gk] : B[(long long)gk * ldb + gj])
+                                 : 0.0;
+    }
+  };
+  double acc[RM][RN] = {};
+  fetch(0);
+  for (int k0 = 0; k0 < K; k0 += TK) {
+#pragma unroll
+    for (int t = 0; t < PA; ++t) {
+      const int e = threadIdx.x + t * 256;
+      if (ta)
+        As[e / TM][e % TM] = ra[t];
+      else
+        As[e % TK][e / TK] = ra[t];
+    }
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      const int e = threadIdx.x + t * 256;
+      if (tb)
+        Bs[e % TK][e / TK] = rb[t];
+      else
+        Bs[e / TN][e % TN] = rb[t];
     }
     __syncthreads();
+    if (k0 + TK < K) fetch(k0 + TK);
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double a[4], b[4];
+    for (int kk = 0; kk < TK; ++kk) {
+      double a[RM], b[RN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < RM; ++i) a[i] = As[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int gi = row0 + ty + 16 * i;
+  for (int i = 0; i < RM; ++i) {
+    const int gi = row0 + ty + 16 * i;
     if (gi >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int gj = col0 + tx + 16 * j;
+    for (int j = 0; j < RN; ++j) {
+      const int gj = col0 + tx + 16 * j;
       if (gj >= N) continue;
       double* c = C + (long long)gi * ldc + gj;
       *c = beta == 0.0 ? alpha * acc[i][j] : alpha * acc[i][j] + beta * (*c);
@@ -191,11 +230,18 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
       }
     return;
   }
-  dim3 grid(ceil_div(N, BN), ceil_div(M, BM), batch);
+  const bool big = (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch >= 74;
   {
     LaunchScope ls("gemm", 2.0*M*N*(double)K*batch, 8.0*batch*((double)M*K+(double)K*N+2.0*M*N));
-    gemm_kernel<<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C,
-                                            ldc, sC);
+    if (big) {
+      dim3 grid(ceil_div(N, 64), ceil_div(M, 64), batch);
+      gemm_kernel<64, 64, 16><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B,
+                                                          ldb, sB, beta, C, ldc, sC);
+    } else {
+      dim3 grid(ceil_div(N, 32), ceil_div(M, 32), batch);
+      gemm_kernel<32, 32, 32><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B,
+                                                          ldb, sB, beta, C, ldc, sC);
+    }
   }
   T2S2_CHECK_LAUNCH();
 }

@@ -21,6 +21,22 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// sum_{i in [lo, hi)} x[i]*y[i]*s over the lanes of a warp, four
+// independent accumulators so the loads pipeline (result in every lane)
+__device__ __forceinline__ double warp_dot(const double* x, const double* y, int lo, int hi,
+                                           int lane, double s = 1.0) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int i = lo + lane;
+  for (; i + 96 < hi; i += 128) {
+    a0 = fma(x[i] * s, y[i], a0);
+    a1 = fma(x[i + 32] * s, y[i + 32], a1);
+    a2 = fma(x[i + 64] * s, y[i + 64], a2);
+    a3 = fma(x[i + 96] * s, y[i + 96], a3);
+  }
+  for (; i < hi; i += 32) a0 = fma(x[i] * s, y[i], a0);
+  return warp_sum((a0 + a1) + (a2 + a3));
+}
+
 // A row-major (m x n) -> Q row-major (m x k), R row-major (k x n).
 // W: column-major m x n scratch, Qc: column-major m x k scratch, tau: k.
 // SM = true: the working copies live in dynamic shared memory (the caller
@@ -44,9 +60,7 @@ __global__ void __launch_bounds__(kQrThreads)
   for (int j = 0; j < k; ++j) {
     double* v = W + (long long)j * m;
     if (warp == 0) {
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) s = fma(v[i], v[i], s);
-      s = warp_sum(s);
+      const double s = warp_dot(v, v, j + 1, m, lane);
       if (lane == 0) {
         double alpha = v[j];
         if (s == 0.0) {
@@ -68,9 +82,7 @@ __global__ void __launch_bounds__(kQrThreads)
     if (t != 0.0) {
       for (int c = j + 1 + warp; c < n; c += nwarps) {
         double* col = W + (long long)c * m;
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) w = fma(v[i] * sc, col[i], w);
-        w = warp_sum(w) + col[j];
+        const double w = warp_dot(v, col, j + 1, m, lane, sc) + col[j];
         double tw = t * w;
         if (lane == 0) col[j] -= tw;
         for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i] * sc, col[i]);
@@ -100,9 +112,7 @@ __global__ void __launch_bounds__(kQrThreads)
     const double* v = W + (long long)j * m;  // v_j = 1 implicit, v_i (i>j) stored
     for (int c = j + warp; c < k; c += nwarps) {
       double* col = Qc + (long long)c * m;
-      double w = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) w = fma(v[i], col[i], w);
-      w = warp_sum(w) + col[j];
+      const double w = warp_dot(v, col, j + 1, m, lane) + col[j];
       double tw = t * w;
       if (lane == 0) col[j] -= tw;
       for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i], col[i]);
@@ -112,6 +122,63 @@ __global__ void __launch_bounds__(kQrThreads)
   for (int e = tid; e < (int)m * k; e += blockDim.x) {
     int i = (int)(e / k), c = (int)(e % k);
     Q[e] = Qc[(long long)c * m + i];
+  }
+}
+
+// R factor only, one CTA per block of rows (TSQR leaf): CTA c takes rows
+// [c*chunk, min((c+1)*chunk, m)) of the row-major m x n matrix A, runs
+// Householder in shared memory and writes its upper-trapezoidal R (zero
+// padded to n rows) at rows [c*n, (c+1)*n) of Rout.
+__global__ void __launch_bounds__(kQrThreads)
+    qr_r_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Rout) {
+  extern __shared__ double W[];
+  const int r0 = blockIdx.x * chunk;
+  const int mr = m - r0 < chunk ? m - r0 : chunk;
+  const int k = mr < n ? mr : n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  __shared__ double sh_tau, sh_scal, sh_beta;
+  for (int e = tid; e < mr * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    W[j * mr + i] = A[(long long)(r0 + i) * n + j];
+  }
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    double* v = W + j * mr;
+    if (warp == 0) {
+      const double s = warp_dot(v, v, j + 1, mr, lane);
+      if (lane == 0) {
+        const double alpha = v[j];
+        if (s == 0.0) {
+          sh_tau = 0.0;
+          sh_scal = 1.0;
+          sh_beta = alpha;
+        } else {
+          const double nrm = sqrt(alpha * alpha + s);
+          const double beta = alpha >= 0.0 ? -nrm : nrm;
+          sh_tau = (beta - alpha) / beta;
+          sh_scal = 1.0 / (alpha - beta);
+          sh_beta = beta;
+        }
+      }
+    }
+    __syncthreads();
+    const double t = sh_tau, sc = sh_scal;
+    if (t != 0.0)
+      for (int c = j + 1 + warp; c < n; c += nwarps) {
+        double* col = W + c * mr;
+        const double w = warp_dot(v, col, j + 1, mr, lane, sc) + col[j];
+        const double tw = t * w;
+        if (lane == 0) col[j] -= tw;
+        for (int i = j + 1 + lane; i < mr; i += 32) col[i] = fma(-tw, v[i] * sc, col[i]);
+      }
+    __syncthreads();
+    if (t != 0.0 && tid == 0) v[j] = sh_beta;
+    __syncthreads();
+  }
+  double* R = Rout + (long long)blockIdx.x * n * n;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int r = e / n, c = e % n;
+    R[e] = (r < k && c >= r) ? W[c * mr + r] : 0.0;
   }
 }
 
@@ -161,16 +228,26 @@ __global__ void __launch_bounds__(kQrThreads)
         }
         double* ga = G + (long long)a * p;
         double* gb = G + (long long)b * p;
-        double al = 0.0, be = 0.0, ga_b = 0.0;
-        for (int i = lane; i < p; i += 32) {
-          double x = ga[i], y = gb[i];
+        double al = 0.0, be = 0.0, ga_b = 0.0, al2 = 0.0, be2 = 0.0, gab2 = 0.0;
+        int i = lane;
+        for (; i + 32 < p; i += 64) {
+          const double x = ga[i], y = gb[i], x2 = ga[i + 32], y2 = gb[i + 32];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga_b = fma(x, y, ga_b);
+          al2 = fma(x2, x2, al2);
+          be2 = fma(y2, y2, be2);
+          gab2 = fma(x2, y2, gab2);
+        }
+        for (; i < p; i += 32) {
+          const double x = ga[i], y = gb[i];
           al = fma(x, x, al);
           be = fma(y, y, be);
           ga_b = fma(x, y, ga_b);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga_b = warp_sum(ga_b);
+        al = warp_sum(al + al2);
+        be = warp_sum(be + be2);
+        ga_b = warp_sum(ga_b + gab2);
         if (ga_b == 0.0 || al == 0.0 || be == 0.0) continue;
         if (fabs(ga_b) <= tol * sqrt(al) * sqrt(be)) continue;
         double zeta = (be - al) / (2.0 * ga_b);
@@ -236,6 +313,35 @@ __global__ void __launch_bounds__(kQrThreads)
 }
 
 }  // namespace
+
+void qr_r(int m, int n, const double* A, DTensor& R) {
+  T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_r: empty matrix");
+  // rows per CTA so that the CTA's block fits the shared-memory budget
+  int chunk = (int)(kSmemCap / (sizeof(double) * (size_t)n));
+  T2S2_REQUIRE(chunk >= n, kErrCapacity, "qr_r: too many columns for shared memory");
+  if (chunk > m) chunk = m;
+  const int blocks = ceil_div(m, chunk);
+  static bool attr = false;
+  if (!attr) {
+    T2S2_CUDA(cudaFuncSetAttribute(qr_r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kSmemCap));
+    attr = true;
+  }
+  DTensor stacked({blocks * n, n});
+  {
+    LaunchScope ls("qr", 2.0 * m * (double)n * n, 8.0 * m * (double)n);
+    qr_r_kernel<<<blocks, kQrThreads, (size_t)chunk * n * sizeof(double), stream()>>>(
+        m, n, chunk, A, stacked.p);
+  }
+  T2S2_CHECK_LAUNCH();
+  if (blocks == 1) {
+    const int k = m < n ? m : n;
+    R = DTensor({k, n});
+    dcopy(R.p, stacked.p, (size_t)k * n);
+    return;
+  }
+  qr_r(blocks * n, n, stacked.p, R);  // TSQR: reduce the stacked leaf factors
+}
 
 void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_thin: empty matrix");

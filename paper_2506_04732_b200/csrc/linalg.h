@@ -12,6 +12,10 @@ namespace t2s2 {
 // the LAPACK dgeqrf/dorgqr convention.
 void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R);
 
+// R factor only (k x n, k = min(m, n)) of a row-major m x n matrix; tall
+// inputs are reduced by a TSQR tree of shared-memory Householder leaves.
+void qr_r(int m, int n, const double* A, DTensor& R);
+
 // Thin SVD A = U diag(s) Vt of a row-major m x n matrix, k = min(m, n),
 // singular values descending.  Tall case: QR, then one-sided Jacobi on R.
 void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt);

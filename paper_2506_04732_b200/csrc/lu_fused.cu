@@ -54,6 +54,7 @@ struct LuArgs {
   int* info;     // 0 or 1 + first zero pivot
   int w;         // panel width
   int* moves;    // per panel: count, then (dst, src) row offsets relative to k0
+  int* flag;     // next-panel chunk completion counter (zeroed by the host)
   unsigned long long* prof;  // optional phase timers (ns): see lu_solve_fused
 };
 
@@ -159,7 +160,7 @@ __device__ __forceinline__ void factor_panel(const LuArgs& a, int k0, int w, dou
   for (int c = 0; c < w; ++c) {
     const double* src = a.A + (long long)(k0 + c) * N + k0;
     double* dst = sm + (long long)c * rows;
-    for (int r = tid; r < rows; r += blockDim.x) dst[r] = src[r];
+    for (int r = tid; r < rows; r += blockDim.x) dst[r] = __ldcg(src + r);
   }
   for (int r = tid; r < rows; r += blockDim.x) {
     cur[r] = r;
@@ -372,6 +373,19 @@ __device__ __forceinline__ void back_substitute(const LuArgs& a, double* x) {
 // Lookahead schedule: while the other CTAs apply panel p to the trailing
 // columns, CTA 0 updates the columns of panel p+1 and factors it, so the
 // panel factorisations form the critical path with one grid barrier each.
+__device__ __forceinline__ int panel_width(int rows) {
+  // panel values plus the two int row maps must fit the dynamic smem
+  int w = (int)((kPanelSmem - 8 * (size_t)rows) / (8 * (size_t)rows));
+  return w > kMaxPanel ? kMaxPanel : (w < 1 ? 1 : w);
+}
+
+// Schedule per iteration (panel p = [k0, k0+w) already factored):
+//   workers (CTAs 1..G-1): first the <= 4 eight-column chunks of the next
+//     panel [k1, k1+w2) — each signals a global counter when done — then
+//     the trailing blocks [k1+w2, N] (column N = right-hand side);
+//   CTA 0: waits for the chunk counter, factors panel p+1 in shared memory.
+//   one grid barrier.
+// Panel widths adapt to the shrinking row count (wider panels later).
 __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
@@ -380,19 +394,23 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.info = 0;
   __syncthreads();
   unsigned long long t0 = 0, acc_upd = 0, acc_fac = 0, acc_sync = 0, acc_work = 0;
-  // iteration k0 = -a.w only factors panel 0; iteration k0 >= 0 applies
-  // panel [k0, k0+w) while CTA 0 prepares panel [k1, k1+w2).
-  for (int k0 = -a.w; k0 < N; k0 += a.w) {
+  int k0 = 0, w = 0;                                     // panel being applied
+  int k1 = 0, w2 = N < panel_width(N) ? N : panel_width(N);  // panel being factored
+  int pidx = -1, target = 0;
+  const int workers = gridDim.x > 1 ? gridDim.x - 1 : 1;
+  const int wid = gridDim.x > 1 ? (int)blockIdx.x - 1 : 0;
+  while (w > 0 || w2 > 0) {
     if (a.prof && threadIdx.x == 0) t0 = gtimer();
-    const int w = k0 < 0 ? 0 : (N - k0 < a.w ? N - k0 : a.w);
-    const int k1 = k0 < 0 ? 0 : k0 + w;                 // next panel start
-    const int w2 = N - k1 < a.w ? N - k1 : a.w;          // next panel width (0 at end)
-    const int rest0 = k1 + w2;                           // columns for the other CTAs
-    const int pi = k0 < 0 ? -1 : k0 / a.w;               // panel index
-    const int* mv = a.moves + ((pi + 2) & 1) * kMoveStride;
-    int* mv_next = a.moves + ((pi + 3) & 1) * kMoveStride;
+    const int* mv = a.moves + ((pidx + 2) & 1) * kMoveStride;
+    int* mv_next = a.moves + ((pidx + 3) & 1) * kMoveStride;
+    const int nchunk = (w > 0 && w2 > 0) ? (w2 + kColBlock - 1) / kColBlock : 0;
+    target += nchunk;
     if (blockIdx.x == 0 && w2 > 0) {
-      if (w > 0) update_cols<kMaxPanel>(a, k0, w, k1, rest0, sm, mv);
+      if (nchunk > 0) {
+        if (threadIdx.x == 0)
+          while (atomicAdd(a.flag, 0) < target) __nanosleep(32);
+        __syncthreads();
+      }
       if (a.prof && threadIdx.x == 0) {
         const unsigned long long t1 = gtimer();
         acc_upd += t1 - t0;
@@ -405,15 +423,23 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
         t0 = t1;
       }
     }
-    const int workers = gridDim.x > 1 ? gridDim.x - 1 : 1;
-    const int wid = gridDim.x > 1 ? (int)blockIdx.x - 1 : 0;
     if (w > 0 && (gridDim.x == 1 || blockIdx.x > 0)) {
-      const int ncols = N + 1 - rest0;
-      const int nblk = (ncols + kColBlock - 1) / kColBlock;
-      for (int blk = wid; blk < nblk; blk += workers) {
-        const int c0 = rest0 + blk * kColBlock;
-        const int c1 = c0 + kColBlock < N + 1 ? c0 + kColBlock : N + 1;
+      const int rest0 = k1 + w2;
+      const int ntrail = (N + 1 - rest0 + kColBlock - 1) / kColBlock;
+      for (int blk = wid; blk < nchunk + ntrail; blk += workers) {
+        int c0, c1;
+        if (blk < nchunk) {
+          c0 = k1 + blk * kColBlock;
+          c1 = c0 + kColBlock < rest0 ? c0 + kColBlock : rest0;
+        } else {
+          c0 = rest0 + (blk - nchunk) * kColBlock;
+          c1 = c0 + kColBlock < N + 1 ? c0 + kColBlock : N + 1;
+        }
         update_cols<kColBlock>(a, k0, w, c0, c1, sm, mv);
+        if (blk < nchunk && threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(a.flag, 1);
+        }
       }
       if (a.prof && threadIdx.x == 0) {
         const unsigned long long t1 = gtimer();
@@ -423,6 +449,13 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
     }
     grid.sync();
     if (a.prof && threadIdx.x == 0) acc_sync += gtimer() - t0;
+    // advance: the factored panel becomes the applied one
+    k0 = k1;
+    w = w2;
+    k1 = k0 + w;
+    w2 = k1 < N ? (N - k1 < panel_width(N - k1) ? N - k1 : panel_width(N - k1)) : 0;
+    ++pidx;
+    if (w == 0) break;
   }
   if (a.prof && threadIdx.x == 0 && blockIdx.x < 2) {
     a.prof[blockIdx.x * 4 + 0] = acc_upd;
@@ -445,18 +478,19 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
     T2S2_CUDA(cudaFuncSetAttribute(lu_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)kPanelSmem));
   }
-  // panel doubles plus the row maps (2 ints + 1 byte per row)
-  int w = (int)((kPanelSmem - 9 * (size_t)N) / (sizeof(double) * (size_t)N));
+  int w = (int)((kPanelSmem - 8 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
   if (w < 1 || N > kRowsPerThread * kThreads) return false;  // multi-launch fallback
-  int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride));
+  int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride + 1));
+  int* flag = moves + 2 * kMoveStride;
+  T2S2_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream()));
   static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
   unsigned long long* pbuf = nullptr;
   if (prof) {
     pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
     T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
   }
-  LuArgs a{N, A, b, piv, info_dev, w, moves, pbuf};
+  LuArgs a{N, A, b, piv, info_dev, w, moves, flag, pbuf};
   void* params[] = {&a};
   {
     // algorithmic: 2/3 N^3 (factor) + 2 N^2 (solves); bytes: matrix read+write

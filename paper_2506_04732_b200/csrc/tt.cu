@@ -120,11 +120,27 @@ void right_orthonormalize(std::vector<DTensor>& cores) {
 }
 
 double tt_norm(const Train& t) {
+  // ||t|| through the right-orthonormalisation R chain (tensor_train.py:
+  // 307-324) without forming the orthonormal cores: only the triangular
+  // factors travel to the left.
   if (t.d() == 1) return dnrm2(t.cores[0].p, t.cores[0].size());
-  std::vector<DTensor> w;
-  for (auto& c : t.cores) w.push_back(c.clone());
-  right_orthonormalize(w);
-  return dnrm2(w[0].p, w[0].size());
+  DTensor Rp;  // k x r1 factor of the part to the right of the current bond
+  for (int l = t.d() - 1; l >= 0; --l) {
+    const DTensor& c = t.cores[l];
+    const int r0 = c.dim(0), r1 = c.dim(-1);
+    const int mid = (int)(c.size() / ((size_t)r0 * r1));
+    const int k = l == t.d() - 1 ? r1 : Rp.dim(0);
+    DTensor Y({r0 * mid, k});
+    if (l == t.d() - 1)
+      dcopy(Y.p, c.p, c.size());
+    else
+      gemm(false, true, r0 * mid, k, r1, 1.0, c.p, r1, Rp.p, r1, 0.0, Y.p, k);
+    if (l == 0) return dnrm2(Y.p, Y.size());
+    DTensor Yt({mid * k, r0});
+    transpose(Y.p, Yt.p, r0, mid * k);
+    qr_r(mid * k, r0, Yt.p, Rp);
+  }
+  return 0.0;
 }
 
 Train tt_round(const Train& t, double tol, int max_rank) {
