@@ -318,8 +318,13 @@ void qr_r(int m, int n, const double* A, DTensor& R) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_r: empty matrix");
   // rows per CTA so that the CTA's block fits the shared-memory budget
   int chunk = (int)(kSmemCap / (sizeof(double) * (size_t)n));
-  T2S2_REQUIRE(chunk >= n, kErrCapacity, "qr_r: too many columns for shared memory");
   if (chunk > m) chunk = m;
+  if (chunk < m && chunk < 2 * n) {
+    // a TSQR leaf would not shrink the row count: one global-memory QR
+    DTensor Q;
+    qr_thin(m, n, A, Q, R);
+    return;
+  }
   const int blocks = ceil_div(m, chunk);
   static bool attr = false;
   if (!attr) {
