@@ -66,82 +66,143 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Column loop of the panel factorisation: thread t owns rows t + k*kThreads
 // (k < RPT); liveness and multipliers stay in registers, values in smem.
+// Column loop of the panel factorisation.  Thread t owns rows t + k*kThreads
+// (k < RPT).  The panel is processed in register sub-panels of SUB columns:
+// a sub-panel's values of the thread's rows live in registers, so a column
+// step touches shared memory only to publish candidate pivot rows; one CTA
+// barrier per column.  After a sub-panel, its pivot rows' U entries right of
+// it are formed (unit-lower forward substitution) and one rank-SUB update is
+// applied to the rest of the panel in shared memory.
+constexpr int SUB = 8;
+
 template <int RPT>
 __device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int* s_piv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nw = kThreads / 32;
-  __shared__ unsigned rh[2][32], rl[2][32];
-  __shared__ int ri[2][32];
+  __shared__ unsigned rh[2][nw], rl[2][nw];
+  __shared__ int ri[2][nw];
+  __shared__ double pub[2][nw][SUB];  // each warp's candidate pivot row (sub-panel part)
   bool live[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) live[k] = tid + k * kThreads < rows;
-  for (int j = 0; j < w; ++j) {
-    const double* cj = sm + j * rows;
-    // argmax |a_rj| as integer keys: the IEEE bits of |a| order like |a|,
-    // so three single-instruction warp reductions (max hi word, max lo word,
-    // min row) replace a 5-step shuffle tree per level; ties -> lowest row
-    unsigned long long kb = 0ull;
-    int bi = 0x7fffffff;
+  for (int j0 = 0; j0 < w; j0 += SUB) {
+    const int nsub = w - j0 < SUB ? w - j0 : SUB;
+    double a[RPT][SUB];
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
-      if (live[k]) {
-        const unsigned long long b = __double_as_longlong(fabs(cj[tid + k * kThreads]));
-        if (b > kb || bi == 0x7fffffff) {
-          kb = b;
-          bi = tid + k * kThreads;
+#pragma unroll
+      for (int t = 0; t < SUB; ++t)
+        a[k][t] = (tid + k * kThreads < rows && t < nsub) ? sm[(j0 + t) * rows + tid + k * kThreads]
+                                                         : 0.0;
+#pragma unroll
+    for (int t = 0; t < SUB; ++t) {
+      if (t >= nsub) break;
+      const int j = j0 + t;
+      const int buf = j & 1;
+      // local candidate: largest |a| among live own rows (first row on ties)
+      unsigned long long kb = 0ull;
+      int bi = 0x7fffffff, bk = 0;
+#pragma unroll
+      for (int k = 0; k < RPT; ++k)
+        if (live[k]) {
+          const unsigned long long b = __double_as_longlong(fabs(a[k][t]));
+          if (b > kb || bi == 0x7fffffff) {
+            kb = b;
+            bi = tid + k * kThreads;
+            bk = k;
+          }
         }
-      }
-    unsigned hi = bi == 0x7fffffff ? 0u : (unsigned)(kb >> 32);
-    unsigned lo = bi == 0x7fffffff ? 0u : (unsigned)kb;
-    {
+      const unsigned hi = bi == 0x7fffffff ? 0u : (unsigned)(kb >> 32);
+      const unsigned lo = bi == 0x7fffffff ? 0u : (unsigned)kb;
       const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
       const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
       const int mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
+      if (bi == mi && mi != 0x7fffffff) {
+        // the warp winner publishes its row's sub-panel values (cols >= t)
+#pragma unroll
+        for (int q = 0; q < SUB; ++q) {
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (k == bk) v = a[k][q];
+          if (q >= t) pub[buf][warp][q] = v;
+        }
+      }
       if (lane == 0) {
-        rh[j & 1][warp] = mh;
-        rl[j & 1][warp] = ml;
-        ri[j & 1][warp] = mi;
+        rh[buf][warp] = mh;
+        rl[buf][warp] = ml;
+        ri[buf][warp] = mi;
+      }
+      __syncthreads();
+      const unsigned h2 = lane < nw ? rh[buf][lane] : 0u;
+      const unsigned l2 = lane < nw ? rl[buf][lane] : 0u;
+      const int i2 = lane < nw ? ri[buf][lane] : 0x7fffffff;
+      const unsigned gh = __reduce_max_sync(0xffffffffu, h2);
+      const unsigned gl = __reduce_max_sync(0xffffffffu, h2 == gh ? l2 : 0u);
+      const int p = __reduce_min_sync(0xffffffffu, (h2 == gh && l2 == gl) ? i2 : 0x7fffffff);
+      const int pw = __ffs(__ballot_sync(0xffffffffu, lane < nw && i2 == p)) - 1;  // winner warp
+      double prow[SUB];
+#pragma unroll
+      for (int q = 0; q < SUB; ++q) prow[q] = q >= t ? pub[buf][pw][q] : 0.0;
+      const double pv = prow[t];
+      if (tid == 0) s_piv[j] = p;
+      const double inv = pv != 0.0 ? __drcp_rn(pv) : 1.0;
+#pragma unroll
+      for (int k = 0; k < RPT; ++k) {
+        if (tid + k * kThreads == p) live[k] = false;
+        if (live[k]) {
+          const double l = a[k][t] * inv;
+          a[k][t] = l;
+#pragma unroll
+          for (int q = 0; q < SUB; ++q)
+            if (q > t) a[k][q] = fma(-l, prow[q], a[k][q]);
+        }
       }
     }
-    __syncthreads();
-    hi = lane < nw ? rh[j & 1][lane] : 0u;
-    lo = lane < nw ? rl[j & 1][lane] : 0u;
-    const int wi = lane < nw ? ri[j & 1][lane] : 0x7fffffff;
-    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-    bi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? wi : 0x7fffffff);
-    const int p = bi;  // physical pivot row (ties -> lowest physical index)
-    const double pv = cj[p];
-    if (tid == 0) s_piv[j] = p;
-    // LAPACK dgetf2 scales by the reciprocal; a zero pivot leaves the column
-    const double inv = pv != 0.0 ? __drcp_rn(pv) : 1.0;
-    double lk[RPT];
+    // sub-panel back to shared memory (pivot rows keep their U entries,
+    // the others their multipliers)
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) {
-      if (tid + k * kThreads == p) live[k] = false;
-      lk[k] = 0.0;
-      if (live[k]) {
-        lk[k] = cj[tid + k * kThreads] * inv;
-        sm[j * rows + tid + k * kThreads] = lk[k];
+    for (int k = 0; k < RPT; ++k)
+#pragma unroll
+      for (int t = 0; t < SUB; ++t)
+        if (tid + k * kThreads < rows && t < nsub) sm[(j0 + t) * rows + tid + k * kThreads] = a[k][t];
+    const int je = j0 + nsub;
+    if (je < w) {
+      __syncthreads();
+      // U entries of the sub-panel's pivot rows right of it (one thread per
+      // column): u_t = a[p_t][c] - sum_{q<t} l[p_t][q] u_q
+      for (int c = je + tid; c < w; c += kThreads) {
+        double u[SUB];
+#pragma unroll
+        for (int t = 0; t < SUB; ++t) {
+          u[t] = 0.0;
+          if (t < nsub) {
+            const int pt = s_piv[j0 + t];
+            double x = sm[c * rows + pt];
+#pragma unroll
+            for (int q = 0; q < SUB; ++q)
+              if (q < t) x = fma(-sm[(j0 + q) * rows + pt], u[q], x);
+            u[t] = x;
+            sm[c * rows + pt] = x;
+          }
+        }
       }
-    }
-    // rank-1 update, 4 columns at a time: every load of a block issues
-    // before its stores (shared stores would otherwise serialise the loop)
-    for (int c = j + 1; c < w; c += 4) {
-      const int nb = w - c < 4 ? w - c : 4;
-      double u[4], v[RPT][4];
+      __syncthreads();
+      // rank-nsub update of the live rows, columns je..w-1
+      for (int c = je; c < w; ++c) {
+        double ut[SUB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) u[q] = q < nb ? sm[(c + q) * rows + p] : 0.0;
+        for (int t = 0; t < SUB; ++t) ut[t] = t < nsub ? sm[c * rows + s_piv[j0 + t]] : 0.0;
 #pragma unroll
-      for (int k = 0; k < RPT; ++k)
+        for (int k = 0; k < RPT; ++k)
+          if (live[k]) {
+            double x = sm[c * rows + tid + k * kThreads];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          v[k][q] = live[k] && q < nb ? sm[(c + q) * rows + tid + k * kThreads] : 0.0;
-#pragma unroll
-      for (int k = 0; k < RPT; ++k)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (live[k] && q < nb) sm[(c + q) * rows + tid + k * kThreads] = fma(-lk[k], u[q], v[k][q]);
+            for (int t = 0; t < SUB; ++t) x = fma(-a[k][t], ut[t], x);
+            sm[c * rows + tid + k * kThreads] = x;
+          }
+      }
+      __syncthreads();
     }
   }
 }
