@@ -214,6 +214,8 @@ void t2s2_context_destroy(t2s2_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->alloc.trim();
+  cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;

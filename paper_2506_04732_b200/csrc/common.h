@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace t2s2 {
@@ -49,17 +50,47 @@ enum ErrCode {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
-// Stream-ordered device allocation (cudaMallocAsync on the context stream).
+// Device allocation for one stream: a host-side caching allocator (size
+// classes of powers of two) over cudaMallocAsync.  All work of a context is
+// ordered on its stream, so a block released after its last use was
+// enqueued can be handed to the next request immediately — no driver call on
+// the hot path.
 struct Allocator {
   cudaStream_t stream = nullptr;
+  std::unordered_map<size_t, std::vector<double*>> free_lists;
+  std::unordered_map<double*, size_t> live;
+  static size_t size_class(size_t n) {
+    size_t c = 32;
+    while (c < n) c <<= 1;
+    return c;
+  }
   double* alloc(size_t n) {
     if (n == 0) n = 1;
-    void* p = nullptr;
-    T2S2_CUDA(cudaMallocAsync(&p, n * sizeof(double), stream));
-    return static_cast<double*>(p);
+    const size_t c = size_class(n);
+    auto& fl = free_lists[c];
+    double* p = nullptr;
+    if (!fl.empty()) {
+      p = fl.back();
+      fl.pop_back();
+    } else {
+      void* v = nullptr;
+      T2S2_CUDA(cudaMallocAsync(&v, c * sizeof(double), stream));
+      p = static_cast<double*>(v);
+    }
+    live[p] = c;
+    return p;
   }
   void release(double* p) {
-    if (p) cudaFreeAsync(p, stream);
+    if (!p) return;
+    auto it = live.find(p);
+    if (it == live.end()) return;
+    free_lists[it->second].push_back(p);
+    live.erase(it);
+  }
+  void trim() {  // return cached blocks to the driver pool
+    for (auto& kv : free_lists)
+      for (double* p : kv.second) cudaFreeAsync(p, stream);
+    free_lists.clear();
   }
 };
 

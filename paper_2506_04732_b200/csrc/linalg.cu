@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(kQrThreads)
   extern __shared__ double qsm[];
   const int k = m < n ? m : n;
   double* W = SM ? qsm : Wg;
-  double* Qc = SM ? qsm + (size_t)m * n : Qg;
-  double* tau = SM ? qsm + (size_t)m * n + (size_t)m * k : tg;
+  double* tau = SM ? qsm + (size_t)m * n : tg;
+  (void)Qg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ double sh_tau, sh_scal, sh_beta;
   for (int e = tid; e < (int)m * n; e += blockDim.x) {
@@ -100,28 +100,28 @@ __global__ void __launch_bounds__(kQrThreads)
     int r = (int)(e / n), c = (int)(e % n);
     R[e] = c >= r ? W[(long long)c * m + r] : 0.0;
   }
-  // Q = H_0 ... H_{k-1} [I_k; 0], accumulated backwards.
-  for (int e = tid; e < (int)m * k; e += blockDim.x) {
-    int c = (int)(e / m), i = (int)(e % m);
-    Qc[e] = i == c ? 1.0 : 0.0;
-  }
+  // Q = H_0 ... H_{k-1} [I_k; 0] formed in place over the reflectors
+  // (LAPACK dorg2r order): column j becomes e_j - tau_j v_j after H_j has
+  // been applied to the already-formed columns right of it.
   __syncthreads();
   for (int j = k - 1; j >= 0; --j) {
     const double t = tau[j];
-    if (t == 0.0) continue;
-    const double* v = W + (long long)j * m;  // v_j = 1 implicit, v_i (i>j) stored
-    for (int c = j + warp; c < k; c += nwarps) {
-      double* col = Qc + (long long)c * m;
-      const double w = warp_dot(v, col, j + 1, m, lane) + col[j];
-      double tw = t * w;
-      if (lane == 0) col[j] -= tw;
-      for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i], col[i]);
-    }
+    double* v = W + (long long)j * m;  // v_j = 1 implicit, v_i (i>j) stored
+    if (t != 0.0)
+      for (int c = j + 1 + warp; c < k; c += nwarps) {
+        double* col = W + (long long)c * m;
+        const double w = warp_dot(v, col, j + 1, m, lane) + col[j];
+        const double tw = t * w;
+        if (lane == 0) col[j] -= tw;
+        for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-tw, v[i], col[i]);
+      }
+    __syncthreads();
+    for (int i = tid; i < m; i += blockDim.x) v[i] = i < j ? 0.0 : (i == j ? 1.0 - t : -t * v[i]);
     __syncthreads();
   }
   for (int e = tid; e < (int)m * k; e += blockDim.x) {
     int i = (int)(e / k), c = (int)(e % k);
-    Q[e] = Qc[(long long)c * m + i];
+    Q[e] = W[(long long)c * m + i];
   }
 }
 
@@ -358,7 +358,7 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
   double* tau = allocator().alloc(k);
   {
     LaunchScope ls("qr", 4.0*m*(double)n*(m<n?m:n), 16.0*m*(double)n);
-    const size_t need = ((size_t)m * n + (size_t)m * k + k) * sizeof(double);
+    const size_t need = ((size_t)m * n + k) * sizeof(double);
     if (need <= kSmemCap) {
       static bool attr = false;
       if (!attr) {
