@@ -80,11 +80,10 @@ def blas_threads():
 # -- CPU legs (oracle = the reference's algorithm, pinned to its outputs) ----------
 
 
-def oracle_problem(recipe):
-    """Build the workload's trains with the oracle doing the setup numerics
-    (no GPU needed)."""
+def cpu_backend():
+    """Setup numerics on the CPU oracle (no GPU needed): a context manager."""
     from oracle import tt_ops as ot
-    from paper_2506_04732_b200 import assembly, tt, workloads as wl
+    from paper_2506_04732_b200 import assembly, tt
 
     def rnd(v, tol, max_rank=None):
         if isinstance(v, tt.TTOperator):
@@ -99,7 +98,14 @@ def oracle_problem(recipe):
     def app(op, v):
         return tt.TTVector(ot.tt_apply(op.cores, v.cores))
 
-    with assembly.setup_backend(round=rnd, add=add, apply=app):
+    return assembly.setup_backend(round=rnd, add=add, apply=app)
+
+
+def oracle_problem(recipe):
+    """The workload's trains built with the oracle doing the setup numerics."""
+    from paper_2506_04732_b200 import workloads as wl
+
+    with cpu_backend():
         return wl.march_problem(recipe)
 
 
@@ -110,9 +116,11 @@ def cpu_march(recipe, n_steps, start_step=1, state=None, problem=None):
     left, right, state0, forcing, _, _ = problem or oracle_problem(recipe)
     st = state if state is not None else state0.cores
     cfg = als.Config(**recipe.solver)
+    with cpu_backend():
+        forc = {k: forcing(k) for k in range(start_step, start_step + n_steps)}
     t0 = time.perf_counter()
     for k in range(start_step, start_step + n_steps):
-        bc, src = forcing(k)
+        bc, src = forc[k]
         st, _, _ = om.step(left.cores, right.cores, st, bc.cores, src.cores, recipe.step_tol, cfg,
                            index=k)
     return time.perf_counter() - t0, st
