@@ -1,0 +1,213 @@
+"""The reference's solver and time-integration contracts, exercised through
+this package's drop-in API on the device (the reference's own tests,
+pkg/tests/test_tt_solver.py and test_time_integration.py, state these
+properties; these are independent re-statements of them)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2506_04732_b200 import _native, assembly, coefficients, march, solver, tt
+
+    _native.context()
+    return dict(tt=tt, solver=solver, march=march, asm=assembly, co=coefficients)
+
+
+def _pde(api, dims, degree, eps=0.05, beta=1.0, rho=0.1):
+    asm, co = api["asm"], api["co"]
+    spec = asm.ProblemSpec(dims=dims, degrees=[degree] * dims,
+                           epsilon=co.constant_coefficient(eps, dims),
+                           beta=[co.constant_coefficient(beta, dims)] * dims,
+                           rho=co.constant_coefficient(rho, dims),
+                           rhs=co.constant_coefficient(1.0, dims))
+    return asm.impose_dirichlet(asm.assemble_opset(spec), spec)
+
+
+# -- solver (tt_solver.py) --------------------------------------------------------
+
+
+@pytest.mark.parametrize("dims,degree", [(1, 9), (2, 8), (2, 10), (3, 6)])
+def test_dense_equivalence(api, dims, degree):
+    tt, solver = api["tt"], api["solver"]
+    a, b = _pde(api, dims, degree)
+    x, rep = solver.solve(a, b, cfg=solver.SolverConfig(residual_tol=1e-10, max_rank=40))
+    dense = np.linalg.solve(tt.tt_op_full(a), tt.tt_full(b).ravel())
+    err = np.linalg.norm(tt.tt_full(x).ravel() - dense) / np.linalg.norm(dense)
+    assert rep.converged and err <= 1e-8
+
+
+def test_random_diagonal_system(api):
+    tt, solver = api["tt"], api["solver"]
+    rng = np.random.default_rng(2)
+    coeff = tt.tt_from_separable([(1.0, [rng.uniform(1.0, 2.0, n) for n in (5, 4, 6)])])
+    a = tt.tt_diag_operator(coeff)
+    b = tt.tt_random((5, 4, 6), 3, rng, norm=1.0)
+    x, rep = solver.solve(a, b, cfg=solver.SolverConfig(residual_tol=1e-11, max_rank=30))
+    want = tt.tt_full(b) / tt.tt_full(coeff)
+    assert rep.converged
+    assert np.abs(tt.tt_full(x) - want).max() <= 1e-9 * np.abs(want).max()
+
+
+def test_report_contracts_and_determinism(api):
+    solver = api["solver"]
+    a, b = _pde(api, 2, 8, eps=1e-3)
+    cfg = solver.SolverConfig(residual_tol=1e-12, max_sweeps=10, max_rank=24)
+    x1, r1 = solver.solve(a, b, cfg=cfg)
+    x2, r2 = solver.solve(a, b, cfg=cfg)
+    best = np.minimum.accumulate(r1.residual_history)
+    assert np.all(np.diff(best) <= 0)
+    assert len(r1.rank_history) == len(r1.residual_history) == len(r1.compression_history)
+    assert max(r1.rank_history) <= cfg.max_rank
+    # the engine is deterministic: identical inputs give bit-identical reports
+    assert r1.residual_history == r2.residual_history
+    assert r1.rank_history == r2.rank_history
+    for c1, c2 in zip(x1.cores, x2.cores):
+        np.testing.assert_array_equal(c1, c2)
+    assert r1.wall_time > 0
+    assert set(r1.to_dict()) == {"residuals", "ranks", "compression", "wall_time_s", "converged"}
+
+
+def test_stagnation_flag(api):
+    solver = api["solver"]
+    a, b = _pde(api, 2, 16, eps=1e-7, beta=1.0, rho=0.0)
+    cfg = solver.SolverConfig(residual_tol=1e-12, max_rank=2, max_sweeps=30, enrichment_rank=0)
+    x, rep = solver.solve(a, b, cfg=cfg)
+    assert not rep.converged and rep.stagnated
+    assert len(rep.residual_history) < 30
+    assert np.isfinite(rep.residual_history).all()
+
+
+def test_residual_contracts(api):
+    tt, solver = api["tt"], api["solver"]
+    rng = np.random.default_rng(5)
+    v = tt.tt_random((5, 4, 3), 2, rng, norm=1.0)
+    eye = tt.tt_identity_operator((5, 4, 3))
+    assert solver.residual(eye, v, v) <= 1e-14
+    assert solver.residual(eye, tt.tt_scale(v, 0.0), v) == pytest.approx(1.0)
+    p = tt.tt_random((5, 4, 3), 1, rng, norm=1e-4)
+    r1 = solver.residual(eye, tt.tt_add(v, p), v)
+    r2 = solver.residual(eye, tt.tt_add(v, tt.tt_scale(p, 2.0)), v)
+    assert r2 / r1 == pytest.approx(2.0, rel=1e-6)
+
+
+def test_config_validation(api):
+    solver = api["solver"]
+    for kw in (dict(residual_tol=0.0), dict(rounding_tol=-1.0), dict(max_rank=0),
+               dict(local_solver="magic")):
+        with pytest.raises(ValueError):
+            solver.SolverConfig(**kw)
+
+
+# -- time integration (time_integration.py) -------------------------------------------
+
+
+def _heat(api, n=12, eps=0.2):
+    asm, co = api["asm"], api["co"]
+    return asm.ProblemSpec(dims=1, degrees=[n], epsilon=co.constant_coefficient(eps, 1),
+                           beta=[co.constant_coefficient(0.0, 1)],
+                           rho=co.constant_coefficient(0.0, 1),
+                           rhs=co.constant_coefficient(0.0, 1),
+                           initial=co.Coefficient(1, [(1.0, [co.SinPiK(1)])]),
+                           time=asm.TimeSpec(t_end=0.5))
+
+
+def _rate(api, traj):
+    tt = api["tt"]
+    times = np.array([t for t, _ in traj[1:]])
+    peaks = np.array([np.abs(tt.tt_full(s)).max() for _, s in traj[1:]])
+    return -np.polyfit(times, np.log(peaks), 1)[0]
+
+
+def test_constant_trajectory(api):
+    asm, co, march, tt = api["asm"], api["co"], api["march"], api["tt"]
+    spec = asm.ProblemSpec(dims=1, degrees=[8], epsilon=co.constant_coefficient(1.0, 1),
+                           beta=[co.constant_coefficient(0.0, 1)],
+                           rho=co.constant_coefficient(0.0, 1),
+                           rhs=co.constant_coefficient(0.0, 1),
+                           initial=co.Coefficient(1, [(1.0, [co.Const(1.0)])]),
+                           dirichlet=co.Coefficient(1, [(1.0, [co.Const(1.0)])]),
+                           time=asm.TimeSpec(t_end=0.2))
+    traj, _ = march.backward_euler_march(asm.assemble_opset(spec), spec,
+                                         march.MarchConfig(dt=0.05, t_end=0.2))
+    assert len(traj) == 5
+    for _, s in traj:
+        np.testing.assert_allclose(tt.tt_full(s), np.ones(9), atol=1e-8)
+
+
+def test_heat_decay_orders(api):
+    asm, march = api["asm"], api["march"]
+    spec = _heat(api)
+    opset = asm.assemble_opset(spec)
+    lam = 0.2 * np.pi ** 2
+    be = [_rate(api, march.backward_euler_march(opset, spec, march.MarchConfig(dt=dt, t_end=0.5))[0])
+          for dt in (0.025, 0.0125)]
+    err = np.abs(np.array(be) - lam)
+    assert err[0] <= 0.2 * lam and err[1] <= 0.6 * err[0] and be[0] < lam
+    assert err[0] == pytest.approx(lam ** 2 * 0.025 / 2, rel=0.15)
+    cn = [abs(_rate(api, march.crank_nicolson_march(
+        opset, spec, march.MarchConfig(dt=dt, t_end=0.5, scheme="crank_nicolson"))[0]) - lam)
+        for dt in (0.05, 0.025)]
+    assert cn[1] <= 0.35 * cn[0] and cn[0] <= 0.02 * lam
+
+
+def test_boundary_and_diagnostics(api):
+    asm, march, tt, solver = api["asm"], api["march"], api["tt"], api["solver"]
+    spec = _heat(api, n=10)
+    opset = asm.assemble_opset(spec)
+    traj, diag = march.backward_euler_march(
+        opset, spec, march.MarchConfig(dt=0.05, t_end=0.25,
+                                       solver=solver.SolverConfig(residual_tol=1e-12)))
+    for _, s in traj:
+        v = tt.tt_full(s)
+        assert abs(v[0]) <= 1e-10 and abs(v[-1]) <= 1e-10
+    rows = diag.rows()
+    assert len(rows) == 6 and rows[0][0] == 0 and rows[-1][0] == 5
+    assert diag.HEADER.split(",") == ["step", "t", "peak_norm", "max_rank", "compression",
+                                      "residual"]
+
+
+def test_stagnation_names_the_step(api):
+    asm, march, solver = api["asm"], api["march"], api["solver"]
+    from paper_2506_04732_b200 import MarchStepError
+
+    spec = _heat(api, n=10)
+    cfg = march.MarchConfig(dt=0.1, t_end=0.3,
+                            solver=solver.SolverConfig(residual_tol=1e-30, max_rank=1,
+                                                       enrichment_rank=0, max_sweeps=8))
+    with pytest.raises(MarchStepError) as err:
+        march.backward_euler_march(asm.assemble_opset(spec), spec, cfg)
+    assert err.value.step == 1
+
+
+def test_spacetime(api):
+    asm, co, march, solver, tt = api["asm"], api["co"], api["march"], api["solver"], api["tt"]
+    # f = e^t, constant in space: f_t = e^t
+    spec = asm.ProblemSpec(dims=1, degrees=[4], epsilon=co.constant_coefficient(1.0, 1),
+                           beta=[co.constant_coefficient(0.0, 1)],
+                           rho=co.constant_coefficient(0.0, 1),
+                           rhs=co.Coefficient(2, [(1.0, [co.Exp(1.0), co.Const(1.0)])]),
+                           dirichlet=co.Coefficient(2, [(1.0, [co.Exp(1.0), co.Const(1.0)])]),
+                           initial=co.Coefficient(1, [(np.exp(-1.0), [co.Const(1.0)])]),
+                           time=asm.TimeSpec(t_end=2.0, degree=10))
+    x, rep, tgrid = march.spacetime_solve(asm.assemble_opset(spec), spec,
+                                          solver.SolverConfig(residual_tol=1e-11, max_rank=20))
+    assert rep.converged
+    t_phys = 0.5 * (tgrid.base.rep_nodes + 1.0) * 2.0
+    want = np.exp(t_phys)[:, None] * np.ones(5)[None, :]
+    assert np.abs(tt.tt_full(x) - want).max() <= 1e-8 * np.abs(want).max()
+    # heat: the t=-1 slice is the initial data; CN agrees with space-time to O(dt^2)
+    hs = _heat(api, n=10)
+    hs.time = asm.TimeSpec(t_end=0.5, degree=12)
+    opset = asm.assemble_opset(hs)
+    xst, _, _ = march.spacetime_solve(opset, hs, solver.SolverConfig(residual_tol=1e-11,
+                                                                     max_rank=20))
+    full = tt.tt_full(xst)
+    assert np.abs(full[0] - np.sin(np.pi * opset.grids[0].base.rep_nodes)).max() <= 1e-9
+    dt = 0.0125
+    cn = tt.tt_full(march.crank_nicolson_march(
+        opset, hs, march.MarchConfig(dt=dt, t_end=0.5, scheme="crank_nicolson"))[0][-1][1])
+    assert np.abs(cn - full[-1]).max() <= 20 * dt ** 2 * np.abs(full[-1]).max()
