@@ -96,6 +96,46 @@ __global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
   }
 }
 
+// probe[0] += u.nu, probe[1] += c.u, probe[2] += #non-finite(u): one
+// deterministic two-level reduction per candidate (tt_solver.py:332-334 and
+// the isfinite check at :370/:398), read back together with the LU info.
+__global__ void probe_partial_kernel(const double* __restrict__ u, const double* __restrict__ nu,
+                                     const double* __restrict__ c, int n, double* part) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = u[i];
+    s0 = fma(x, nu[i], s0);
+    s1 = fma(c[i], x, s1);
+    s2 += isfinite(x) ? 0.0 : 1.0;
+  }
+  __shared__ double red[3][32];
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = s0;
+    red[1][warp] = s1;
+    red[2][warp] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
+    part[blockIdx.x * 3 + threadIdx.x] = t;
+  }
+}
+
+__global__ void probe_final_kernel(const double* part, int nb, double* out) {
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) t += part[b * 3 + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+}
+
 __global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -251,23 +291,49 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
   return B;
 }
 
-// Dense direct solve of a column-major N x N system; false if singular.
-bool dense_solve(DTensor& M, const DTensor& rhs, DTensor& out) {
+// Dense direct solve of a column-major N x N system; the LU info (0, or
+// 1 + first zero pivot) lands in *info_dev and is read back by the caller.
+void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   const int N = M.dim(0);
   int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
-  int* info = reinterpret_cast<int*>(allocator().alloc(1));
   out = rhs.clone();
-  if (!lu_solve_fused(N, M.p, out.p, ipiv, info)) {
-    lu_factor(N, M.p, ipiv, info);
+  if (!lu_solve_fused(N, M.p, out.p, ipiv, info_dev)) {
+    lu_factor(N, M.p, ipiv, info_dev);
     lu_solve(N, M.p, ipiv, out.p);
   }
-  int h = 0;
-  T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
   allocator().release(reinterpret_cast<double*>(ipiv));
-  allocator().release(reinterpret_cast<double*>(info));
-  return h == 0;
 }
+
+// Device scratch for candidate scores: 3 doubles per probe slot + LU info.
+struct Probe {
+  DTensor buf{std::vector<int>{16}};
+  int* info() { return reinterpret_cast<int*>(buf.p + 12); }
+  void clear_info() { T2S2_CUDA(cudaMemsetAsync(info(), 0, sizeof(int), stream())); }
+  void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c) {
+    const int n = (int)u.size();
+    int nb = (n + 255) / 256;
+    if (nb > 148) nb = 148;
+    double* part = allocator().alloc((size_t)nb * 3);
+    {
+      LaunchScope ls("reduce", 4.0 * n, 24.0 * n);
+      probe_partial_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part);
+    }
+    {
+      LaunchScope ls("reduce", 0, 0);
+      probe_final_kernel<<<1, 32, 0, stream()>>>(part, nb, buf.p + 3 * slot);
+    }
+    T2S2_CHECK_LAUNCH();
+    allocator().release(part);
+  }
+  // one read-back: h[3*slot + {0,1,2}], info at h_info
+  void read(double* h, int* h_info) {
+    double tmp[16];
+    T2S2_CUDA(cudaMemcpyAsync(tmp, buf.p, sizeof tmp, cudaMemcpyDeviceToHost, stream()));
+    T2S2_CUDA(cudaStreamSynchronize(stream()));
+    for (int i = 0; i < 12; ++i) h[i] = tmp[i];
+    *h_info = *reinterpret_cast<int*>(tmp + 12);
+  }
+};
 
 // -- splits with enrichment (tt_solver.py:261-302) ------------------------------
 
@@ -407,12 +473,11 @@ struct Sweep {
       : A(a), rhs(b), cfg(c), d(a.d()), gal_cap(2 * a.d()),
         la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1) {}
 
-  double score(const DTensor& u, const DTensor& nu, const DTensor& c_ls) {
-    // u^T N u - 2 c^T u (tt_solver.py:332-334)
-    return ddot(u.p, nu.p, u.size()) - 2.0 * ddot(c_ls.p, u.p, u.size());
-  }
+  Probe probe;
 
-  // Guarded update of core l (tt_solver.py:337-422).
+  // Guarded update of core l (tt_solver.py:337-422).  Candidate scores
+  // q = u^T N u - 2 c^T u, the finiteness checks and the LU info travel to
+  // the host together: one read-back per candidate pair.
   void update(int l, std::vector<DTensor>& cores, double current_res, DTensor& best,
               DTensor& grad, int& choice) {
     const DTensor& ac = A.cores[l];
@@ -422,50 +487,55 @@ struct Sweep {
     DTensor c_gal = galerkin_rhs(lb[l], bc, rb[l + 1]);
     DTensor c_ls = normal_rhs(lg[l], ac, bc, rg[l + 1]);
     DTensor nu_old = normal_apply(ln[l], ac, rn[l + 1], u_old);
-    const double q_old = score(u_old, nu_old, c_ls);
+    probe.run(0, u_old, nu_old, c_ls);
+    probe.clear_info();
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
     const double inner_rtol = std::fmax(cfg.inner_tol_factor * current_res, 1e-12);
     const bool try_gal = gal_rejects < gal_cap;
-    bool have_gal = false;
-    DTensor u_gal;
+    DTensor u_gal, nu_gal;
     if (try_gal) {
       if (direct) {
         DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
-        have_gal = dense_solve(B, c_gal, u_gal);
+        dense_solve(B, c_gal, u_gal, probe.info());
       } else {
         // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
         u_gal = u_old.clone();
         const DTensor &pal = la[l], &par = ra[l + 1];
         gmres(as_matvec(u_old.shape, [&](const DTensor& u) { return galerkin_apply(pal, ac, par, u); }),
               (int)size, c_gal.p, u_gal.p, inner_rtol, 40, 10);
-        have_gal = true;
       }
-      if (have_gal) have_gal = all_finite(u_gal);
+      u_gal.view(u_old.shape);
+      nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
+      probe.run(1, u_gal, nu_gal, c_ls);
     }
+    double h[12];
+    int info = 0;
+    probe.read(h, &info);
+    const double q_old = h[0] - 2.0 * h[1];
     double best_q = q_old;
     choice = 0;
     DTensor nu_best;
-    if (have_gal) {
-      u_gal.view(u_old.shape);
-      DTensor nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
-      const double q_gal = score(u_gal, nu_gal, c_ls);
+    // a singular local matrix (numpy LinAlgError) or a non-finite candidate
+    // is no candidate (tt_solver.py:359-372)
+    if (try_gal && info == 0 && h[5] == 0.0) {
+      const double q_gal = h[3] - 2.0 * h[4];
       if (q_gal <= best_q) {
         best_q = q_gal;
         choice = 1;
         best = std::move(u_gal);
         nu_best = std::move(nu_gal);
         gal_rejects = 0;
-      } else if (try_gal) {
+      } else {
         gal_rejects += 1;
       }
     }
     if (choice == 0) {
       DTensor u_ls;
-      bool ok = true;
+      probe.clear_info();
       if (direct) {
         DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
         Nm.view({(int)size, (int)size});
-        ok = dense_solve(Nm, c_ls, u_ls);
+        dense_solve(Nm, c_ls, u_ls, probe.info());
       } else {
         // scipy cg(x0=u_old, rtol, atol=0, maxiter=250, M=diag^{-1})
         u_ls = u_old.clone();
@@ -474,10 +544,12 @@ struct Sweep {
         pcg(as_matvec(u_old.shape, [&](const DTensor& u) { return normal_apply(pnl, ac, pnr, u); }),
             (int)size, c_ls.p, u_ls.p, dg.p, inner_rtol, 250);
       }
-      if (ok && all_finite(u_ls)) {
-        u_ls.view(u_old.shape);
-        DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
-        const double q_ls = score(u_ls, nu_ls, c_ls);
+      u_ls.view(u_old.shape);
+      DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
+      probe.run(2, u_ls, nu_ls, c_ls);
+      probe.read(h, &info);
+      if (info == 0 && h[8] == 0.0) {
+        const double q_ls = h[6] - 2.0 * h[7];
         if (q_ls <= best_q) {
           best_q = q_ls;
           choice = 2;

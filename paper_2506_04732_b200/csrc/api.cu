@@ -32,6 +32,7 @@ struct t2s2_context {
   // launch accounting
   std::vector<t2s2::FamilyStat> fams;
   std::unordered_map<std::string, int> fam_index;
+  std::unordered_map<const char*, int> fam_by_ptr;  // call-site literal -> family
   bool profiling = false;
   std::vector<cudaEvent_t> event_pool;
   size_t pool_used = 0;
@@ -61,14 +62,20 @@ Allocator& allocator() { return g_ctx->alloc; }
 
 LaunchScope::LaunchScope(const char* family, double flops, double bytes) {
   t2s2_context* c = g_ctx;
-  auto it = c->fam_index.find(family);
   int f;
-  if (it == c->fam_index.end()) {
-    f = (int)c->fams.size();
-    c->fam_index.emplace(family, f);
-    c->fams.push_back(FamilyStat{family});
+  auto ip = c->fam_by_ptr.find(family);
+  if (ip != c->fam_by_ptr.end()) {
+    f = ip->second;
   } else {
-    f = it->second;
+    auto it = c->fam_index.find(family);
+    if (it == c->fam_index.end()) {
+      f = (int)c->fams.size();
+      c->fam_index.emplace(family, f);
+      c->fams.push_back(FamilyStat{family});
+    } else {
+      f = it->second;
+    }
+    c->fam_by_ptr.emplace(family, f);
   }
   FamilyStat& st = c->fams[f];
   st.launches += 1;
