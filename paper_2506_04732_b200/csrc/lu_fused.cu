@@ -82,6 +82,7 @@ __device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int*
   __shared__ unsigned rh[2][nw], rl[2][nw];
   __shared__ int ri[2][nw];
   __shared__ double pub[2][nw][SUB];  // each warp's candidate pivot row (sub-panel part)
+  __shared__ double pinv[2][nw];      // and the reciprocal of its pivot entry
   bool live[RPT];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) live[k] = tid + k * kThreads < rows;
@@ -118,14 +119,19 @@ __device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int*
       const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
       const int mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
       if (bi == mi && mi != 0x7fffffff) {
-        // the warp winner publishes its row's sub-panel values (cols >= t)
+        // the warp winner publishes its row's sub-panel values (cols > t)
+        // and the reciprocal of its candidate pivot (slot t)
 #pragma unroll
         for (int q = 0; q < SUB; ++q) {
           double v = 0.0;
 #pragma unroll
           for (int k = 0; k < RPT; ++k)
             if (k == bk) v = a[k][q];
-          if (q >= t) pub[buf][warp][q] = v;
+          if (q > t) pub[buf][warp][q] = v;
+          if (q == t) {
+            pub[buf][warp][q] = v;
+            pinv[buf][warp] = v != 0.0 ? __drcp_rn(v) : 1.0;
+          }
         }
       }
       if (lane == 0) {
@@ -144,9 +150,8 @@ __device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int*
       double prow[SUB];
 #pragma unroll
       for (int q = 0; q < SUB; ++q) prow[q] = q >= t ? pub[buf][pw][q] : 0.0;
-      const double pv = prow[t];
       if (tid == 0) s_piv[j] = p;
-      const double inv = pv != 0.0 ? __drcp_rn(pv) : 1.0;
+      const double inv = pinv[buf][pw];
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
         if (tid + k * kThreads == p) live[k] = false;
