@@ -304,6 +304,28 @@ void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   allocator().release(reinterpret_cast<double*>(ipiv));
 }
 
+// Minimum-norm least squares of a singular column-major N x N system, the
+// reference's fallback when numpy.linalg.solve raises (tt_solver.py:362,
+// :395 call numpy.linalg.lstsq with rcond=None: cutoff eps*N*s_max).
+void lstsq_dense(const DTensor& Mcm, const DTensor& rhs, DTensor& out) {
+  const int N = Mcm.dim(0);
+  DTensor U, sv, Vt;
+  svd_thin(N, N, Mcm.p, U, sv, Vt);  // column-major M read as row-major M^T = U S Vt
+  const int k = sv.dim(0);
+  std::vector<double> hs(k);
+  to_host(hs.data(), sv.p, k);
+  const double cutoff = 2.220446049250313e-16 * N * (k ? hs[0] : 0.0);
+  std::vector<double> inv(k);
+  for (int i = 0; i < k; ++i) inv[i] = hs[i] > cutoff ? 1.0 / hs[i] : 0.0;
+  DTensor dinv({k}), y({k, 1});
+  to_device(dinv.p, inv.data(), k);
+  // M = Vt^T S U^T  =>  x = U diag(1/s) Vt b
+  gemm(false, false, k, 1, N, 1.0, Vt.p, N, rhs.p, 1, 0.0, y.p, 1);
+  scale_rows(y.p, k, 1, 1, dinv.p);
+  out = DTensor(rhs.shape);
+  gemm(false, false, N, 1, k, 1.0, U.p, k, y.p, 1, 0.0, out.p, 1);
+}
+
 // Device scratch for candidate scores: 3 doubles per probe slot + LU info.
 struct Probe {
   DTensor buf{std::vector<int>{16}};
@@ -511,6 +533,16 @@ struct Sweep {
     double h[12];
     int info = 0;
     probe.read(h, &info);
+    if (try_gal && direct && info != 0) {
+      // singular Galerkin block: numpy.linalg.lstsq fallback (tt_solver.py:362)
+      DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+      lstsq_dense(B, c_gal, u_gal);
+      u_gal.view(u_old.shape);
+      nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
+      probe.clear_info();
+      probe.run(1, u_gal, nu_gal, c_ls);
+      probe.read(h, &info);
+    }
     const double q_old = h[0] - 2.0 * h[1];
     double best_q = q_old;
     choice = 0;
@@ -548,6 +580,17 @@ struct Sweep {
       DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
       probe.run(2, u_ls, nu_ls, c_ls);
       probe.read(h, &info);
+      if (direct && info != 0) {
+        // singular normal block: numpy.linalg.lstsq fallback (tt_solver.py:395)
+        DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
+        Nm.view({(int)size, (int)size});
+        lstsq_dense(Nm, c_ls, u_ls);
+        u_ls.view(u_old.shape);
+        nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
+        probe.clear_info();
+        probe.run(2, u_ls, nu_ls, c_ls);
+        probe.read(h, &info);
+      }
       if (info == 0 && h[8] == 0.0) {
         const double q_ls = h[6] - 2.0 * h[7];
         if (q_ls <= best_q) {

@@ -70,7 +70,7 @@ def _cfg(solver, z, tag):
     return solver.SolverConfig(**kw)
 
 
-@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7"])
+@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7", "s8"])
 def test_solve_small_matches_reference(golden, pk, tag):
     _, tt, solver, _ = pk
     z = golden("solve_small.npz")
@@ -254,3 +254,17 @@ def test_config1_full_matches_reference(golden, pk):
     a, b, exact, opset = wl.steady_problem(recipe)
     err = ot.tt_norm(ot.tt_add(x.cores, ot.tt_scale(exact.cores, -1.0))) / ot.tt_norm(exact.cores)
     assert err <= 1.01 * float(z["exact_err"]) + 1e-6
+
+
+def test_singular_local_systems_use_lstsq(golden, pk):
+    """Every local system of s8 is exactly singular: numpy raises and the
+    reference takes numpy.linalg.lstsq's minimum-norm solution; the engine's
+    SVD fallback must land on the same iterate."""
+    _, tt, solver, _ = pk
+    z = golden("solve_small.npz")
+    a, b = O(tt, get_train(z, "s8_a")), V(tt, get_train(z, "s8_b"))
+    x, rep = solver.solve(a, b, cfg=_cfg(solver, z, "s8"))
+    ref = np.array(z["s8_res"])
+    assert rep.stagnated and not rep.converged
+    np.testing.assert_allclose(rep.residual_history[-1], ref[-1], rtol=1e-9)
+    assert rel_diff(x.cores, get_train(z, "s8_x")) <= 1e-9

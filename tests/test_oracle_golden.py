@@ -27,7 +27,7 @@ def _cfg(z, tag):
     return als.Config(**kw)
 
 
-@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7"])
+@pytest.mark.parametrize("tag", ["s1", "s2", "s3", "s4", "s5", "s6", "s7", "s8"])
 def test_solve_small_matches_reference(golden, tag):
     z = golden("solve_small.npz")
     a, b, x0 = get_train(z, f"{tag}_a"), get_train(z, f"{tag}_b"), get_train(z, f"{tag}_x0")

@@ -145,13 +145,24 @@ SOLVE_CASES = [
     ("s6", (2, 16, 1e-7, 1.0, 0.0), dict(residual_tol=1e-12, max_rank=2, max_sweeps=30,
                                          enrichment_rank=0)),
     ("s7", (2, 7, 1e-3, 1.0, 0.1), dict(residual_tol=1e-11, seed=42, max_sweeps=8)),
+    ("s8", "singular", dict(residual_tol=1e-10, max_sweeps=8)),
 ]
+
+
+def singular_system():
+    """Diagonal operator with a zero slice: every local solve hits numpy's
+    LinAlgError and the reference falls back to lstsq (tt_solver.py:362)."""
+    rng = np.random.default_rng(9)
+    f = [rng.uniform(1, 2, n) for n in (5, 4, 6)]
+    f[0][2] = 0.0
+    a = rtt.tt_diag_operator(rtt.tt_from_separable([(1.0, f)]))
+    return a, rtt.tt_random((5, 4, 6), 2, rng, norm=1.0)
 
 
 def solves():
     st = {}
     for tag, sysargs, kw in SOLVE_CASES:
-        a, b = pde_system(*sysargs)
+        a, b = singular_system() if sysargs == "singular" else pde_system(*sysargs)
         cfg = rsol.SolverConfig(**kw)
         x0 = rsol._default_initial_guess(b, cfg, np.random.default_rng(cfg.seed))
         t0 = time.time()
