@@ -98,6 +98,11 @@ typedef struct {
 int t2s2_context_create(int device, t2s2_context** out);
 void t2s2_context_destroy(t2s2_context* ctx);
 const char* t2s2_last_error(const t2s2_context* ctx);
+/* Limit whole-GPU cooperative kernels (the local dense solves) to `sms`
+ * CTAs (0 = all SMs), so several contexts on one device — one per host
+ * thread, e.g. independent solves of a parameter sweep — can run their
+ * local solves concurrently. */
+int t2s2_context_set_sm_budget(t2s2_context* ctx, int sms);
 /* The cudaStream_t every kernel of the context is launched on (for
  * callers that time or order work around the engine). */
 void* t2s2_stream(t2s2_context* ctx);

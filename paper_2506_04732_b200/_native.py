@@ -102,6 +102,7 @@ _SIGNATURES = {
     "t2s2_last_error": (ctypes.c_char_p, [_P]),
     "t2s2_synchronize": (_I, [_P]),
     "t2s2_stream": (_P, [_P]),
+    "t2s2_context_set_sm_budget": (_I, [_P, _I]),
     "t2s2_stats_reset": (_I, [_P, _I]),
     "t2s2_stats_read": (_I, [_P, ctypes.POINTER(KernelStatC), _I, _IP]),
     "t2s2_train_upload": (_I, [_P, _I, _IP, _IP, _IP, _DP, ctypes.POINTER(_P)]),
@@ -129,7 +130,7 @@ EXPORTED = tuple(_SIGNATURES)
 
 _lock = threading.Lock()
 _lib = None
-_ctx = None
+_tls = threading.local()  # one engine context (and stream) per host thread
 
 
 def load_library(path=LIB_PATH):
@@ -159,21 +160,44 @@ def lib():
 
 
 def context():
-    """The process-wide engine context on device ``T2S2_DEVICE`` (default 0)."""
-    global _ctx
-    if _ctx is not None:
-        return _ctx
+    """This thread's engine context on device ``T2S2_DEVICE`` (default
+    ``LOCAL_RANK`` or 0).  Each host thread gets its own context and stream,
+    so independent solves can run concurrently on one device; a train belongs
+    to the thread that created it."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is not None:
+        return ctx
     l = lib()
-    with _lock:
-        if _ctx is None:
-            dev = int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
-            h = _P()
-            rc = l.t2s2_context_create(dev, ctypes.byref(h))
-            if rc != T2S2_OK:
-                raise NativeUnavailable(f"t2s2_context_create(device={dev}) failed with code {rc}"
-                                        " (no CUDA device?)")
-            _ctx = h
-    return _ctx
+    dev = int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    h = _P()
+    rc = l.t2s2_context_create(dev, ctypes.byref(h))
+    if rc != T2S2_OK:
+        raise NativeUnavailable(f"t2s2_context_create(device={dev}) failed with code {rc}"
+                                " (no CUDA device?)")
+    budget = getattr(_tls, "sm_budget", 0)
+    if budget:
+        l.t2s2_context_set_sm_budget(h, int(budget))
+    _tls.ctx = h
+    return h
+
+
+def num_sms():
+    """Multiprocessor count of this thread's device (via torch if present)."""
+    try:
+        import torch
+
+        dev = int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        return torch.cuda.get_device_properties(dev).multi_processor_count
+    except Exception:
+        return 148
+
+
+def set_thread_sm_budget(sms):
+    """Cap the cooperative local-solve kernels of this thread's context."""
+    _tls.sm_budget = int(sms)
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is not None:
+        lib().t2s2_context_set_sm_budget(ctx, int(sms))
 
 
 def check(rc, step=None):

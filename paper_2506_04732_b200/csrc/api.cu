@@ -26,6 +26,7 @@ struct Pending {
 
 struct t2s2_context {
   int device = 0;
+  int sm_budget = 0;  // 0: all SMs
   cudaStream_t stream = nullptr;
   t2s2::Allocator alloc;
   std::string last_error;
@@ -59,6 +60,7 @@ struct Bind {  // makes ctx current for the duration of an API call
 }  // namespace
 
 Allocator& allocator() { return g_ctx->alloc; }
+int sm_budget() { return g_ctx->sm_budget; }
 
 LaunchScope::LaunchScope(const char* family, double flops, double bytes) {
   t2s2_context* c = g_ctx;
@@ -230,6 +232,12 @@ void t2s2_context_destroy(t2s2_context* ctx) {
 
 const char* t2s2_last_error(const t2s2_context* ctx) {
   return ctx ? ctx->last_error.c_str() : "null context";
+}
+
+int t2s2_context_set_sm_budget(t2s2_context* ctx, int sms) {
+  if (!ctx || sms < 0) return T2S2_ERR_ARG;
+  ctx->sm_budget = sms;
+  return T2S2_OK;
 }
 
 void* t2s2_stream(t2s2_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }

@@ -105,6 +105,7 @@ struct LaunchScope {
 };
 
 Allocator& allocator();  // the current context's allocator
+int sm_budget();         // CTAs a whole-GPU cooperative kernel may use (context setting)
 cudaStream_t stream();   // the current context's stream
 
 // A dense row-major device array with a host-known shape.  Owns its

@@ -562,7 +562,8 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
     // algorithmic: 2/3 N^3 (factor) + 2 N^2 (solves); bytes: matrix read+write
     LaunchScope ls("lu_fused", 2.0 / 3.0 * (double)N * N * N + 2.0 * (double)N * N,
                    16.0 * (double)N * N);
-    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)lu_fused_kernel, dim3(g_num_sms), dim3(kThreads),
+    const int grid = sm_budget() > 0 && sm_budget() < g_num_sms ? sm_budget() : g_num_sms;
+    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)lu_fused_kernel, dim3(grid), dim3(kThreads),
                                           params, kPanelSmem, stream()));
   }
   allocator().release(reinterpret_cast<double*>(moves));

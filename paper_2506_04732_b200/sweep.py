@@ -30,7 +30,8 @@ def _default_solve(a, b, cfg_kwargs):
     return x, rep
 
 
-def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None):
+def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None,
+              concurrency=1):
     """Solve this rank's share of ``recipes`` (workloads.SteadyRecipe).
 
     Returns {index: dict(x=cores, residuals, ranks, converged, stagnated,
@@ -43,7 +44,9 @@ def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=
     solve_fn = solve_fn or _default_solve
     build_fn = build_fn or wl.steady_problem
     out = {}
-    for i in shard(len(recipes), rank, world):
+    mine = shard(len(recipes), rank, world)
+
+    def one(i):
         r = recipes[i]
         a, b, exact, _ = build_fn(r)
         cfg = dict(r.solver)
@@ -54,6 +57,43 @@ def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=
         out[i] = dict(x=[c.copy() for c in x.cores], residuals=list(rep.residual_history),
                       ranks=list(rep.rank_history), converged=bool(rep.converged),
                       stagnated=bool(rep.stagnated), wall_s=wall, eps=r.eps)
+
+    if concurrency <= 1:
+        for i in mine:
+            one(i)
+        return out
+    # several solves in flight on one device: one engine context (stream)
+    # per host thread, each thread's local dense solves capped to its share
+    # of the SMs so their cooperative kernels can be co-resident
+    import threading
+
+    from . import _native
+
+    queue = list(mine)
+    lock = threading.Lock()
+    errors = []
+
+    def worker():
+        _native.set_thread_sm_budget(max(1, _native.num_sms() // concurrency))
+        while True:
+            with lock:
+                if not queue or errors:
+                    return
+                i = queue.pop(0)
+            try:
+                one(i)
+            except Exception as exc:  # surface the first failure
+                with lock:
+                    errors.append(exc)
+                return
+
+    threads = [threading.Thread(target=worker) for _ in range(concurrency)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
     return out
 
 
