@@ -19,7 +19,16 @@ namespace {
 // The next K-tile is fetched into registers while the current one is
 // consumed from shared memory, so each tile costs one exposed L2 latency at
 // most; small problems use 32x32x32 tiles to spread over more SMs.
-template <int TM, int TN, int TK>
+// FP64 tensor-core MMA (DMMA, mma.sync m8n8k4): D[8x8] += A[8x4] B[4x8].
+// Fragments: lane holds A[lane/4][lane%4], B[lane%4][lane/4],
+// C/D[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int TM, int TN, int TK, bool TC>
 __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
                                                    double alpha, const double* __restrict__ A,
                                                    int lda, long long sA,
@@ -67,7 +76,13 @@ __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int 
                                  : 0.0;
     }
   };
+  // FFMA path: 16x16 threads, RM x RN outputs each.  TC path: 8 warps on a
+  // 4 x 2 grid of (TM/4) x (TN/2) warp tiles of 8x8 DMMA blocks.
+  constexpr int WM = TM / 4, WN = TN / 2, MB = WM / 8, NB = WN / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * WN;
   double acc[RM][RN] = {};
+  double tc[MB][NB][2] = {};
   fetch(0);
   for (int k0 = 0; k0 < K; k0 += TK) {
 #pragma unroll
@@ -88,19 +103,52 @@ __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int 
     }
     __syncthreads();
     if (k0 + TK < K) fetch(k0 + TK);
+    if (TC) {
 #pragma unroll
-    for (int kk = 0; kk < TK; ++kk) {
-      double a[RM], b[RN];
+      for (int kk = 0; kk < TK; kk += 4) {
+        const int kr = kk + (lane & 3);
+        double af[MB], bf[NB];
 #pragma unroll
-      for (int i = 0; i < RM; ++i) a[i] = As[kk][ty + 16 * i];
+        for (int i = 0; i < MB; ++i) af[i] = As[kr][wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx + 16 * j];
+        for (int j = 0; j < NB; ++j) bf[j] = Bs[kr][wn0 + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < RM; ++i)
+        for (int i = 0; i < MB; ++i)
 #pragma unroll
-        for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < NB; ++j) dmma_8x8x4(tc[i][j][0], tc[i][j][1], af[i], bf[j]);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        double a[RM], b[RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+        for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
     }
     __syncthreads();
+  }
+  if (TC) {
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+      const int gi = row0 + wm0 + i * 8 + (lane >> 2);
+      if (gi >= M) continue;
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gj = col0 + wn0 + j * 8 + (lane & 3) * 2 + h;
+          if (gj >= N) continue;
+          double* c = C + (long long)gi * ldc + gj;
+          *c = beta == 0.0 ? alpha * tc[i][j][h] : alpha * tc[i][j][h] + beta * (*c);
+        }
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < RM; ++i) {
@@ -235,12 +283,12 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
     LaunchScope ls("gemm", 2.0*M*N*(double)K*batch, 8.0*batch*((double)M*K+(double)K*N+2.0*M*N));
     if (big) {
       dim3 grid(ceil_div(N, 64), ceil_div(M, 64), batch);
-      gemm_kernel<64, 64, 16><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B,
-                                                          ldb, sB, beta, C, ldc, sC);
+      gemm_kernel<64, 64, 16, true><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA,
+                                                                B, ldb, sB, beta, C, ldc, sC);
     } else {
       dim3 grid(ceil_div(N, 32), ceil_div(M, 32), batch);
-      gemm_kernel<32, 32, 32><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA, B,
-                                                          ldb, sB, beta, C, ldc, sC);
+      gemm_kernel<32, 32, 32, true><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA,
+                                                                B, ldb, sB, beta, C, ldc, sC);
     }
   }
   T2S2_CHECK_LAUNCH();
