@@ -10,13 +10,16 @@ external dataset).
   0  d=2 steady, n=17 nodes, eps=1e-2, b=(1,1), Gaussian bump
   1  d=3 steady, n=33, eps=1e-6, b=(1,.5,.25), separable boundary layer
   2  d=6 + time, n=33, eps=1e-3, translating Gaussian, BE dt=1e-3, 100 steps
-
-"TT tolerance 1e-12" is applied to the solver's residual target, its SVD
-rounding and the step re-truncation alike: with the reference's march
-default residual_tol=1e-10 the 1e-12 step truncation keeps solver noise and
-the bond ranks drift with it.
   3  d=6 + time, n=65, eps=1e-12, translating Gaussian, dt=5e-4, 200 steps, cap 64
   4  64 independent d=6 steady boundary-layer solves, n=33
+
+"TT tolerance 1e-12" is the solver's SVD rounding tolerance (rounding_tol);
+the march keeps the reference's MarchConfig defaults (time_integration.py:
+54-60): inner residual_tol=1e-10 and step re-truncation 1e-8.  Tightening
+the residual target to 1e-12 is not sustainable over a 100-step march (the
+alternating solver stalls at its noise floor after ~60 steps and the bond
+ranks grow with every enrichment sweep), and truncating states at 1e-12
+with a 1e-10 solve keeps solver noise in the ranks.
 """
 
 from __future__ import annotations
@@ -103,7 +106,7 @@ class MarchRecipe:
     beta: list
     dt: float
     n_steps: int
-    step_tol: float = 1e-12
+    step_tol: float = 1e-8
     solver: dict = field(default_factory=dict)
 
     def u_factors(self, axes, t):
@@ -133,10 +136,10 @@ def config(index, **over):
                          solver=dict(residual_tol=1e-10, rounding_tol=1e-12))
     elif index == 2:
         r = MarchRecipe("d6_time_n33", 6, 32, 1e-3, unit_vector(6, 2), 1e-3, 100,
-                        solver=dict(residual_tol=1e-12, rounding_tol=1e-12))
+                        solver=dict(residual_tol=1e-10, rounding_tol=1e-12))
     elif index == 3:
         r = MarchRecipe("d6_time_n65", 6, 64, 1e-12, unit_vector(6, 3), 5e-4, 200,
-                        solver=dict(residual_tol=1e-12, rounding_tol=1e-12, max_rank=64))
+                        solver=dict(residual_tol=1e-10, rounding_tol=1e-12, max_rank=64))
     elif index == 4:
         raise ValueError("config 4 is a batch; use sweep_recipes()")
     else:

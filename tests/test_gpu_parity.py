@@ -128,7 +128,8 @@ def test_march_matches_reference(golden, pk, fname, steps):
         want = get_train(z, f"state{k}")
         ok, det = ranks_agree(got, want)
         assert ok, (k, det)
-        assert rel_diff(got, want) <= k * value_tol(rows[k - 1][3], z[f"res{k}"][-1]), k
+        tol = value_tol(rows[k - 1][3], z[f"res{k}"][-1]) + 2 * float(z["step_tol"])
+        assert rel_diff(got, want) <= k * tol, k
     for h in [left, right, state] + bcs + srcs + list(stored.values()):
         h.free()
 

@@ -86,6 +86,6 @@ def test_march_matches_reference(golden, fname, steps):
         want = get_train(z, f"state{k}")
         ok, det = ranks_agree(state, want)
         assert ok, (k, det)
-        tol = value_tol(rep.residual_history[-1], z[f"res{k}"][-1])
-        # states carry the previous steps' differences too
+        # solve accuracy plus the step re-truncation, accumulated over steps
+        tol = value_tol(rep.residual_history[-1], z[f"res{k}"][-1]) + 2 * float(z["step_tol"])
         assert rel_diff(state, want) <= k * tol, k
