@@ -64,97 +64,112 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// Column loop of the panel factorisation: thread t owns rows t + k*kThreads
-// (k < RPT); liveness and multipliers stay in registers, values in smem.
-// Column loop of the panel factorisation.  Thread t owns rows t + k*kThreads
-// (k < RPT).  The panel is processed in register sub-panels of SUB columns:
+// Column loop of the panel factorisation, run by the first nthr threads of
+// the CTA (nthr a power of two, nthr * RPT >= rows: only warps that own rows
+// take part, synchronised by named barrier 1).  Thread t owns rows
+// t + k*nthr.  The panel is processed in register sub-panels of SUB columns:
 // a sub-panel's values of the thread's rows live in registers, so a column
-// step touches shared memory only to publish candidate pivot rows; one CTA
-// barrier per column.  After a sub-panel, its pivot rows' U entries right of
-// it are formed (unit-lower forward substitution) and one rank-SUB update is
-// applied to the rest of the panel in shared memory.
-constexpr int SUB = 8;
+// step touches shared memory only to publish candidate pivot rows; one
+// barrier per column.
+//
+// Pivot search: one 32-bit key per row, (|a| hi word >> 11) << 12 | (4095 -
+// row): the magnitude to 2^-9 relative resolution, ties to the lowest row,
+// so one REDUX per level finds it.  (Any row within 0.2% of the column
+// maximum is an equally stable pivot: |multipliers| <= 1.002.)
+//
+// After a sub-panel, its pivot rows' U entries right of it are formed
+// (unit-lower forward substitution from preloaded values) and one rank-SUB
+// update is applied to the rest of the panel in shared memory.
+__device__ __forceinline__ void bar_panel(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
-template <int RPT>
-__device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int* s_piv) {
+struct PanelScratch {
+  double pub[2][kThreads / 32][10];  // each warp's candidate row; [8] = 1/pivot
+  double Lp[8][8];                   // multipliers of the sub-panel's pivot rows
+  double Us[kMaxPanel][8];           // U rows right of the sub-panel
+  unsigned rk[2][kThreads / 32];     // each warp's best key
+};
+
+__device__ __forceinline__ PanelScratch& panel_scratch() {
+  __shared__ __align__(16) PanelScratch ps;
+  return ps;
+}
+
+template <int RPT, int SUB>
+__device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int* s_piv, int nthr,
+                                            unsigned long long* prof) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nw = kThreads / 32;
-  __shared__ unsigned rh[2][nw], rl[2][nw];
-  __shared__ int ri[2][nw];
-  __shared__ double pub[2][nw][SUB];  // each warp's candidate pivot row (sub-panel part)
-  __shared__ double pinv[2][nw];      // and the reciprocal of its pivot entry
+  const int nw = nthr >> 5;
+  const unsigned full = 0xffffffffu;
+  PanelScratch& ps = panel_scratch();
+  auto& rk = ps.rk;
+  auto& pub = ps.pub;
+  auto& Lp = ps.Lp;
+  auto& Us = ps.Us;
+  long long c0 = clock64(), c_steps = 0, c_sub = 0;
+  int row[RPT];
   bool live[RPT];
+  unsigned tag[RPT];
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) live[k] = tid + k * kThreads < rows;
+  for (int k = 0; k < RPT; ++k) {
+    row[k] = tid + k * nthr;
+    live[k] = row[k] < rows;
+    tag[k] = 4095u - (unsigned)row[k];
+  }
   for (int j0 = 0; j0 < w; j0 += SUB) {
     const int nsub = w - j0 < SUB ? w - j0 : SUB;
     double a[RPT][SUB];
+    int pv[SUB];
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
 #pragma unroll
       for (int t = 0; t < SUB; ++t)
-        a[k][t] = (tid + k * kThreads < rows && t < nsub) ? sm[(j0 + t) * rows + tid + k * kThreads]
-                                                         : 0.0;
+        a[k][t] = (row[k] < rows && t < nsub) ? sm[(j0 + t) * rows + row[k]] : 0.0;
 #pragma unroll
     for (int t = 0; t < SUB; ++t) {
+      pv[t] = 0;
       if (t >= nsub) break;
-      const int j = j0 + t;
-      const int buf = j & 1;
-      // local candidate: largest |a| among live own rows (first row on ties)
-      unsigned long long kb = 0ull;
-      int bi = 0x7fffffff, bk = 0;
+      const int buf = (j0 + t) & 1;
+      unsigned key = 0u;
+      int bk = 0;
 #pragma unroll
       for (int k = 0; k < RPT; ++k)
         if (live[k]) {
-          const unsigned long long b = __double_as_longlong(fabs(a[k][t]));
-          if (b > kb || bi == 0x7fffffff) {
-            kb = b;
-            bi = tid + k * kThreads;
+          const unsigned kk = (((unsigned)__double2hiint(fabs(a[k][t])) >> 11) << 12) | tag[k];
+          if (kk > key) {
+            key = kk;
             bk = k;
           }
         }
-      const unsigned hi = bi == 0x7fffffff ? 0u : (unsigned)(kb >> 32);
-      const unsigned lo = bi == 0x7fffffff ? 0u : (unsigned)kb;
-      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-      const int mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
-      if (bi == mi && mi != 0x7fffffff) {
-        // the warp winner publishes its row's sub-panel values (cols > t)
-        // and the reciprocal of its candidate pivot (slot t)
+      const unsigned wk = __reduce_max_sync(full, key);
+      if (key == wk && key != 0u) {
+        // the warp's winner publishes its row (multipliers left of t,
+        // values from t on) and the reciprocal of its candidate pivot
+        double* dst = pub[buf][warp];
 #pragma unroll
         for (int q = 0; q < SUB; ++q) {
-          double v = 0.0;
+          double v = a[0][q];
 #pragma unroll
-          for (int k = 0; k < RPT; ++k)
+          for (int k = 1; k < RPT; ++k)
             if (k == bk) v = a[k][q];
-          if (q > t) pub[buf][warp][q] = v;
-          if (q == t) {
-            pub[buf][warp][q] = v;
-            pinv[buf][warp] = v != 0.0 ? __drcp_rn(v) : 1.0;
-          }
+          dst[q] = v;
+          if (q == t) dst[8] = v != 0.0 ? __drcp_rn(v) : 1.0;
         }
       }
-      if (lane == 0) {
-        rh[buf][warp] = mh;
-        rl[buf][warp] = ml;
-        ri[buf][warp] = mi;
-      }
-      __syncthreads();
-      const unsigned h2 = lane < nw ? rh[buf][lane] : 0u;
-      const unsigned l2 = lane < nw ? rl[buf][lane] : 0u;
-      const int i2 = lane < nw ? ri[buf][lane] : 0x7fffffff;
-      const unsigned gh = __reduce_max_sync(0xffffffffu, h2);
-      const unsigned gl = __reduce_max_sync(0xffffffffu, h2 == gh ? l2 : 0u);
-      const int p = __reduce_min_sync(0xffffffffu, (h2 == gh && l2 == gl) ? i2 : 0x7fffffff);
-      const int pw = __ffs(__ballot_sync(0xffffffffu, lane < nw && i2 == p)) - 1;  // winner warp
+      if (lane == 0) rk[buf][warp] = wk;
+      bar_panel(nthr);
+      const unsigned g = __reduce_max_sync(full, lane < nw ? rk[buf][lane] : 0u);
+      const int p = 4095 - (int)(g & 4095u);
+      pv[t] = p;
+      const double* src = pub[buf][(p & (nthr - 1)) >> 5];
       double prow[SUB];
 #pragma unroll
-      for (int q = 0; q < SUB; ++q) prow[q] = q >= t ? pub[buf][pw][q] : 0.0;
-      if (tid == 0) s_piv[j] = p;
-      const double inv = pinv[buf][pw];
+      for (int q = 0; q < SUB; ++q) prow[q] = q > t ? src[q] : 0.0;
+      const double inv = src[8];
+      if (tid < t) Lp[t][tid] = src[tid];
+      if (tid == 0) s_piv[j0 + t] = p;
 #pragma unroll
       for (int k = 0; k < RPT; ++k) {
-        if (tid + k * kThreads == p) live[k] = false;
+        if (row[k] == p) live[k] = false;
         if (live[k]) {
           const double l = a[k][t] * inv;
           a[k][t] = l;
@@ -164,125 +179,218 @@ __device__ __forceinline__ void factor_columns(int rows, int w, double* sm, int*
         }
       }
     }
+    if (prof) {
+      const long long c1 = clock64();
+      c_steps += c1 - c0;
+      c0 = c1;
+    }
     // sub-panel back to shared memory (pivot rows keep their U entries,
     // the others their multipliers)
 #pragma unroll
     for (int k = 0; k < RPT; ++k)
 #pragma unroll
       for (int t = 0; t < SUB; ++t)
-        if (tid + k * kThreads < rows && t < nsub) sm[(j0 + t) * rows + tid + k * kThreads] = a[k][t];
+        if (row[k] < rows && t < nsub) sm[(j0 + t) * rows + row[k]] = a[k][t];
     const int je = j0 + nsub;
     if (je < w) {
-      __syncthreads();
+      bar_panel(nthr);
       // U entries of the sub-panel's pivot rows right of it (one thread per
       // column): u_t = a[p_t][c] - sum_{q<t} l[p_t][q] u_q
-      for (int c = je + tid; c < w; c += kThreads) {
-        double u[SUB];
+      for (int c = je + tid; c < w; c += nthr) {
+        double x[SUB];
+#pragma unroll
+        for (int t = 0; t < SUB; ++t) x[t] = t < nsub ? sm[c * rows + pv[t]] : 0.0;
+#pragma unroll
+        for (int t = 1; t < SUB; ++t)
+#pragma unroll
+          for (int q = 0; q < t; ++q) x[t] = fma(-Lp[t][q], x[q], x[t]);
 #pragma unroll
         for (int t = 0; t < SUB; ++t) {
-          u[t] = 0.0;
-          if (t < nsub) {
-            const int pt = s_piv[j0 + t];
-            double x = sm[c * rows + pt];
-#pragma unroll
-            for (int q = 0; q < SUB; ++q)
-              if (q < t) x = fma(-sm[(j0 + q) * rows + pt], u[q], x);
-            u[t] = x;
-            sm[c * rows + pt] = x;
-          }
+          Us[c][t] = x[t];
+          if (t < nsub) sm[c * rows + pv[t]] = x[t];
         }
       }
-      __syncthreads();
-      // rank-nsub update of the live rows, columns je..w-1
-      for (int c = je; c < w; ++c) {
-        double ut[SUB];
+      bar_panel(nthr);
+      // rank-nsub update of the live rows, columns je..w-1, two at a time
+      int c = je;
+      for (; c + 1 < w; c += 2) {
+        double u0[SUB], u1[SUB], x0[RPT], x1[RPT];
 #pragma unroll
-        for (int t = 0; t < SUB; ++t) ut[t] = t < nsub ? sm[c * rows + s_piv[j0 + t]] : 0.0;
+        for (int t = 0; t < SUB; ++t) {
+          u0[t] = Us[c][t];
+          u1[t] = Us[c + 1][t];
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          x0[k] = live[k] ? sm[c * rows + row[k]] : 0.0;
+          x1[k] = live[k] ? sm[(c + 1) * rows + row[k]] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+#pragma unroll
+          for (int t = 0; t < SUB; ++t) {
+            x0[k] = fma(-a[k][t], u0[t], x0[k]);
+            x1[k] = fma(-a[k][t], u1[t], x1[k]);
+          }
 #pragma unroll
         for (int k = 0; k < RPT; ++k)
           if (live[k]) {
-            double x = sm[c * rows + tid + k * kThreads];
-#pragma unroll
-            for (int t = 0; t < SUB; ++t) x = fma(-a[k][t], ut[t], x);
-            sm[c * rows + tid + k * kThreads] = x;
+            sm[c * rows + row[k]] = x0[k];
+            sm[(c + 1) * rows + row[k]] = x1[k];
           }
       }
-      __syncthreads();
+      if (c < w) {
+        double ut[SUB];
+#pragma unroll
+        for (int t = 0; t < SUB; ++t) ut[t] = Us[c][t];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+          if (live[k]) {
+            double x = sm[c * rows + row[k]];
+#pragma unroll
+            for (int t = 0; t < SUB; ++t) x = fma(-a[k][t], ut[t], x);
+            sm[c * rows + row[k]] = x;
+          }
+      }
     }
+    if (prof) {
+      const long long c1 = clock64();
+      c_sub += c1 - c0;
+      c0 = c1;
+    }
+  }
+  if (prof && threadIdx.x == 0) {
+    prof[12] += c_steps;
+    prof[13] += c_sub;
+  }
+}
+
+// Smallest power-of-two thread count (>= one warp) giving each thread at
+// most rpt rows.
+__device__ __forceinline__ int panel_threads(int rows, int rpt) {
+  int n = 32;
+  while (n * rpt < rows) n <<= 1;
+  return n;
+}
+
+// Panel configurations measured on B200 (tools/micro/fc2_bench.cu): one row
+// per thread with as few warps as possible up to 512 rows, then SUB = 4 to
+// keep the larger register row blocks spill-free.
+__device__ __forceinline__ void factor_columns_any(int rows, int w, double* sm, int* s_piv,
+                                                unsigned long long* prof) {
+  const int tid = threadIdx.x;
+  if (rows <= kThreads) {
+    const int n = panel_threads(rows, 1);
+    if (tid < n) factor_columns<1, 8>(rows, w, sm, s_piv, n, prof);
+  } else if (rows <= 2 * kThreads) {
+    factor_columns<2, 4>(rows, w, sm, s_piv, kThreads, prof);
+  } else if (rows <= 3 * kThreads) {
+    factor_columns<3, 4>(rows, w, sm, s_piv, kThreads, prof);
+  } else if (rows <= 4 * kThreads) {
+    factor_columns<4, 4>(rows, w, sm, s_piv, kThreads, prof);
+  } else {
+    factor_columns<5, 4>(rows, w, sm, s_piv, kThreads, prof);
   }
 }
 
 // Factor the panel A[k0:N, k0:k0+w] with partial pivoting inside one CTA,
 // one barrier per column: rows never move while factoring (a chosen pivot
 // row is flagged done and read in place), so each thread only touches its
-// own rows; the LAPACK-order interchanges are replayed on an index map and
-// applied when the panel is written back.
+// own rows.  Afterwards positions 0..w-1 take the pivot rows in order and
+// each low row (physical index < w) that was not chosen takes the slot of a
+// chosen pivot from below the panel top: any such bijection is a valid row
+// permutation (the right-hand side rides along as column N, so no LAPACK
+// ipiv sequence is needed) and one warp computes it with ballots.
 __device__ __forceinline__ void factor_panel(const LuArgs& a, int k0, int w, double* sm, int* s_piv,
                                           int* mv) {
   const int N = a.N, rows = N - k0;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  unsigned long long tp = a.prof && tid == 0 ? gtimer() : 0;
+#define T2S2_PHASE(slot)                                 \
+  if (a.prof && tid == 0) {                              \
+    const unsigned long long tq = gtimer();              \
+    a.prof[8 + (slot)] += tq - tp;                       \
+    tp = tq;                                             \
+  }
   int* cur = reinterpret_cast<int*>(sm + (size_t)rows * w);  // position -> physical row
-  int* pos = cur + rows;                                      // physical row -> position
-  for (int c = 0; c < w; ++c) {
-    const double* src = a.A + (long long)(k0 + c) * N + k0;
-    double* dst = sm + (long long)c * rows;
-    for (int r = tid; r < rows; r += blockDim.x) dst[r] = __ldcg(src + r);
+  {
+    // every element of the panel in flight at once: asynchronous 8-byte
+    // copies global -> shared (the panel is L2-resident)
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+    int c = tid / rows, r = tid - c * rows;
+    const int step_c = kThreads / rows, step_r = kThreads - step_c * rows;
+    const double* col0 = a.A + (long long)k0 * N + k0;
+    for (int e = tid; e < rows * w; e += kThreads) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 8u * (unsigned)e),
+                   "l"(col0 + (long long)c * N + r)
+                   : "memory");
+      c += step_c;
+      r += step_r;
+      if (r >= rows) {
+        r -= rows;
+        ++c;
+      }
+    }
   }
-  for (int r = tid; r < rows; r += blockDim.x) {
-    cur[r] = r;
-    pos[r] = r;
+  for (int r = tid; r < rows; r += kThreads) cur[r] = r;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  T2S2_PHASE(0)
+  factor_columns_any(rows, w, sm, s_piv, a.prof);
+  __syncthreads();
+  T2S2_PHASE(1)
+  if (tid < 32) {
+    const unsigned full = 0xffffffffu;
+    const bool act = lane < w;
+    const int p = act ? s_piv[lane] : 0;
+    const unsigned wmask = w >= 32 ? full : ((1u << w) - 1u);
+    const unsigned chosen_low = __reduce_or_sync(full, (act && p < w) ? (1u << p) : 0u);
+    const unsigned free_low = ~chosen_low & wmask;  // low rows displaced by pivots
+    const bool high = act && p >= w;
+    const unsigned high_mask = __ballot_sync(full, high);
+    const unsigned lt = (1u << lane) - 1u;
+    const int k = __popc(high_mask & lt);
+    const unsigned moved = __ballot_sync(full, act && p != lane);
+    const int n1 = __popc(moved);
+    if (act) {
+      cur[lane] = p;
+      a.piv[k0 + lane] = k0 + p;
+    }
+    if (act && p != lane) {
+      const int m = __popc(moved & lt);
+      mv[1 + 2 * m] = lane;
+      mv[2 + 2 * m] = p;
+    }
+    if (high) {
+      const int q = __fns(free_low, 0, k + 1);
+      cur[p] = q;
+      mv[1 + 2 * (n1 + k)] = p;
+      mv[2 + 2 * (n1 + k)] = q;
+    }
+    if (lane == 0) mv[0] = n1 + __popc(high_mask);
+    const unsigned zero = __ballot_sync(full, act && sm[lane * rows + p] == 0.0);
+    if (lane == 0 && zero && *a.info == 0) *a.info = k0 + __ffs(zero);
   }
   __syncthreads();
-  if (rows <= kThreads)
-    factor_columns<1>(rows, w, sm, s_piv);
-  else if (rows <= 2 * kThreads)
-    factor_columns<2>(rows, w, sm, s_piv);
-  else if (rows <= 3 * kThreads)
-    factor_columns<3>(rows, w, sm, s_piv);
-  else if (rows <= 4 * kThreads)
-    factor_columns<4>(rows, w, sm, s_piv);
-  else
-    factor_columns<5>(rows, w, sm, s_piv);
-  // replay the interchanges in LAPACK order on the index maps
-  __syncthreads();
-  if (tid == 0) {
-    for (int j = 0; j < w; ++j) {
-      const int p = s_piv[j];
-      const int pp = pos[p];
-      a.piv[k0 + j] = k0 + pp;
-      const int rj = cur[j];
-      cur[j] = p;
-      cur[pp] = rj;
-      pos[p] = j;
-      pos[rj] = pp;
-      if (sm[j * rows + p] == 0.0 && *a.info == 0) *a.info = k0 + j + 1;
+  T2S2_PHASE(2)
+  {
+    int c = tid / rows, r = tid - c * rows;
+    const int step_c = kThreads / rows, step_r = kThreads - step_c * rows;
+    double* col0 = a.A + (long long)k0 * N + k0;
+#pragma unroll 4
+    for (int e = tid; e < rows * w; e += kThreads) {
+      col0[(long long)c * N + r] = sm[c * rows + cur[r]];
+      c += step_c;
+      r += step_r;
+      if (r >= rows) {
+        r -= rows;
+        ++c;
+      }
     }
   }
   __syncthreads();
-  for (int c = 0; c < w; ++c) {
-    double* dst = a.A + (long long)(k0 + c) * N + k0;
-    const double* src = sm + (long long)c * rows;
-    for (int i = tid; i < rows; i += blockDim.x) dst[i] = src[cur[i]];
-  }
-  // rows whose position changed: at most 2w of them (the first w positions
-  // and the slots the pivots came from); other CTAs replay them per column
-  if (tid == 0) {
-    int m = 0;
-    for (int i = 0; i < w; ++i)
-      if (cur[i] != i) {
-        mv[1 + 2 * m] = i;
-        mv[2 + 2 * m] = cur[i];
-        ++m;
-      }
-    // displaced rows: physical row q (< w) that ended at position pos[q] >= w
-    for (int q = 0; q < w; ++q)
-      if (pos[q] >= w) {
-        mv[1 + 2 * m] = pos[q];
-        mv[2 + 2 * m] = q;
-        ++m;
-      }
-    mv[0] = m;
-  }
+  T2S2_PHASE(3)
+#undef T2S2_PHASE
 }
 
 // Interchanges, TRSM and rank-w update of the owned columns [c0, c1),
@@ -398,10 +506,83 @@ __device__ __forceinline__ void update_cols(const LuArgs& a, int k0, int w, int 
   __syncthreads();
 }
 
+// One next-panel column c brought up to date with panel [k0, k0+w): the
+// critical path between two panel factorisations, so every input is loaded
+// in one asynchronous batch into shared memory (the factored panel and the
+// column), the row moves are applied there, the unit-lower TRSM runs in one
+// warp and the rank-w update reads L21 from shared memory; the column is
+// written back once.
+__device__ __forceinline__ void update_next_col(const LuArgs& a, int k0, int w, int c, double* sm,
+                                             const int* mv) {
+  const int N = a.N, rows = N - k0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  double* L = sm;                     // panel, positions k0.., ld = rows
+  double* X = sm + (size_t)rows * w;  // column c, positions k0..
+  {
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+    int cc = tid / rows, r = tid - cc * rows;
+    const int step_c = kThreads / rows, step_r = kThreads - step_c * rows;
+    const double* col0 = a.A + (long long)k0 * N + k0;
+    for (int e = tid; e < rows * w; e += kThreads) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 8u * (unsigned)e),
+                   "l"(col0 + (long long)cc * N + r)
+                   : "memory");
+      cc += step_c;
+      r += step_r;
+      if (r >= rows) {
+        r -= rows;
+        ++cc;
+      }
+    }
+    const double* xc = a.A + (long long)c * N + k0;
+    const unsigned xbase = sbase + 8u * (unsigned)(rows * w);
+    for (int e = tid; e < rows; e += kThreads)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(xbase + 8u * (unsigned)e),
+                   "l"(xc + e)
+                   : "memory");
+  }
+  const int m = __ldcg(mv);
+  int dst = -1, src = 0;
+  if (tid < m) {
+    dst = __ldcg(mv + 1 + 2 * tid);
+    src = __ldcg(mv + 2 + 2 * tid);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  double v = 0.0;
+  if (dst >= 0) v = X[src];
+  __syncthreads();
+  if (dst >= 0) X[dst] = v;
+  __syncthreads();
+  if (tid < 32) {
+    // U12 = L11^{-1} x[0:w]: lane i holds row i
+    double xi = lane < w ? X[lane] : 0.0;
+#pragma unroll 1
+    for (int j = 0; j < w; ++j) {
+      const double lij = lane < w ? L[j * rows + lane] : 0.0;
+      const double xj = __shfl_sync(0xffffffffu, xi, j);
+      if (lane > j) xi = fma(-lij, xj, xi);
+    }
+    if (lane < w) X[lane] = xi;
+  }
+  __syncthreads();
+  double* out = a.A + (long long)c * N + k0;
+  for (int i = tid; i < rows; i += kThreads) {
+    double x = X[i];
+    if (i >= w) {
+#pragma unroll 4
+      for (int j = 0; j < w; ++j) x = fma(-L[j * rows + i], X[j], x);
+    }
+    out[i] = x;
+  }
+  __threadfence();
+  __syncthreads();
+}
+
 __device__ __forceinline__ void back_substitute(const LuArgs& a, double* x) {
   const int N = a.N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < N; i += blockDim.x) x[i] = a.b[i];
+  for (int i = tid; i < N; i += blockDim.x) x[i] = __ldcg(a.b + i);
   __syncthreads();
   for (int j1 = N; j1 > 0; j1 -= 32) {
     const int j0 = j1 - 32 > 0 ? j1 - 32 : 0;
@@ -411,7 +592,7 @@ __device__ __forceinline__ void back_substitute(const LuArgs& a, double* x) {
       double u[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c)
-        u[c] = (lane < jb && c < jb) ? a.A[(long long)(j0 + c) * N + j0 + lane] : 0.0;
+        u[c] = (lane < jb && c < jb) ? __ldcg(a.A + (long long)(j0 + c) * N + j0 + lane) : 0.0;
       double xi = lane < jb ? x[j0 + lane] : 0.0;
 #pragma unroll
       for (int c = 31; c >= 0; --c) {
@@ -428,7 +609,7 @@ __device__ __forceinline__ void back_substitute(const LuArgs& a, double* x) {
     __syncthreads();
     for (int i = tid; i < j0; i += blockDim.x) {
       double acc = x[i];
-      for (int c = 0; c < jb; ++c) acc = fma(-a.A[(long long)(j0 + c) * N + i], x[j0 + c], acc);
+      for (int c = 0; c < jb; ++c) acc = fma(-__ldcg(a.A + (long long)(j0 + c) * N + i), x[j0 + c], acc);
       x[i] = acc;
     }
     __syncthreads();
@@ -469,7 +650,10 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
     if (a.prof && threadIdx.x == 0) t0 = gtimer();
     const int* mv = a.moves + ((pidx + 2) & 1) * kMoveStride;
     int* mv_next = a.moves + ((pidx + 3) & 1) * kMoveStride;
-    const int nchunk = (w > 0 && w2 > 0) ? (w2 + kColBlock - 1) / kColBlock : 0;
+    // next-panel columns are on the critical path: one column per worker
+    // when there are enough workers, so each one's update is short
+    const int cw = workers >= 2 * w2 ? 1 : kColBlock;
+    const int nchunk = (w > 0 && w2 > 0) ? (w2 + cw - 1) / cw : 0;
     target += nchunk;
     if (blockIdx.x == 0 && w2 > 0) {
       if (nchunk > 0) {
@@ -495,16 +679,21 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
       for (int blk = wid; blk < nchunk + ntrail; blk += workers) {
         int c0, c1;
         if (blk < nchunk) {
-          c0 = k1 + blk * kColBlock;
-          c1 = c0 + kColBlock < rest0 ? c0 + kColBlock : rest0;
+          c0 = k1 + blk * cw;
+          c1 = c0 + cw < rest0 ? c0 + cw : rest0;
         } else {
           c0 = rest0 + (blk - nchunk) * kColBlock;
           c1 = c0 + kColBlock < N + 1 ? c0 + kColBlock : N + 1;
         }
-        update_cols<kColBlock>(a, k0, w, c0, c1, sm, mv);
-        if (blk < nchunk && threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(a.flag, 1);
+        if (blk < nchunk && cw == 1) {
+          update_next_col(a, k0, w, c0, sm, mv);
+        } else {
+          update_cols<kColBlock>(a, k0, w, c0, c1, sm, mv);
+          if (blk < nchunk) __threadfence();
+        }
+        if (blk < nchunk) {
+          __syncthreads();
+          if (threadIdx.x == 0) atomicAdd(a.flag, 1);
         }
       }
       if (a.prof && threadIdx.x == 0) {
@@ -571,8 +760,11 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
     unsigned long long h[16];
     T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
     T2S2_CUDA(cudaStreamSynchronize(stream()));
-    fprintf(stderr, "lu N=%d w=%d cta0: upd %.1f fac %.1f sync %.1f us | cta1: work %.1f sync %.1f us\n",
-            N, w, h[0] / 1e3, h[1] / 1e3, h[3] / 1e3, h[6] / 1e3, h[7] / 1e3);
+    fprintf(stderr, "lu N=%d w=%d cta0: upd %.1f fac %.1f sync %.1f us | cta1: work %.1f sync %.1f us"
+            " | panel load %.1f cols %.1f replay %.1f store %.1f\n",
+            N, w, h[0] / 1e3, h[1] / 1e3, h[3] / 1e3, h[6] / 1e3, h[7] / 1e3, h[8] / 1e3, h[9] / 1e3,
+            h[10] / 1e3, h[11] / 1e3);
+    fprintf(stderr, "   cols: steps %.0f cyc/col, sub-panel %.0f cyc/col\n", (double)h[12] / N, (double)h[13] / N);
 
     allocator().release(reinterpret_cast<double*>(pbuf));
   }
