@@ -158,84 +158,228 @@ bool all_finite(const DTensor& t) {
   return h == 0;
 }
 
+// -- contractions as permute-free batched GEMM chains ---------------------------
+//
+// The reference contracts with numpy.tensordot, which transposes operands
+// into GEMM shape on every call.  Here each recurrence and local operator is
+// a chain of 2-4 strided-batched GEMMs whose intermediates are laid out so
+// that the next contraction reads them directly (op flags and batch strides
+// replace every transposition).  The only extra layout is, per operator core
+// ac[a, m, n, A] (row mode m, column mode n), the permuted copy
+// acg[m, A, a, n] built once per solve: as a matrix [(m A), (a n)] it applies
+// the core to a column-mode index, its transpose [(a n), (m A)] applies it to
+// a row-mode index.  ac itself, read as [(a m), (n A)], covers the other two
+// cases.  Interfaces keep the reference's layouts (tt_solver.py:94-96):
+// pa (test, op, trial), pn (test, op, op, trial), pg (test, op, rhs),
+// pb (test, rhs).
+
+// C = op(A) op(B) over a strided batch (alpha 1, beta 0).
+void bmm(bool ta, bool tb, int M, int N, int K, const double* A, int lda, long long sA,
+         const double* B, int ldb, long long sB, double* C, int ldc, long long sC, int batch) {
+  gemm_batched(ta, tb, M, N, K, 1.0, A, lda, sA, B, ldb, sB, 0.0, C, ldc, sC, batch);
+}
+
+DTensor op_layout(const DTensor& ac) { return permute(ac, {1, 3, 0, 2}); }  // (m, A, a, n)
+
 DTensor ones(std::vector<int> shape) {
   DTensor t(std::move(shape));
   dfill(t.p, 1.0, t.size());
   return t;
 }
 
+// Dimensions of an operator core (ra, nm, nn, rA).
+struct OpDims {
+  int ra, nm, nn, rA;
+  explicit OpDims(const DTensor& ac) : ra(ac.dim(0)), nm(ac.dim(1)), nn(ac.dim(2)), rA(ac.dim(3)) {}
+};
+
 // -- interface recurrences (tt_solver.py:98-151) -----------------------------
 
-DTensor step_a_left(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
-  DTensor t = tensordot(phi, {0}, xc, {0});    // (a, z, m, X)
-  t = tensordot(t, {0, 2}, ac, {0, 1});        // (z, X, n, A)
-  return tensordot(t, {0, 2}, xc, {0, 1});     // (X, A, Z)
+// pa[x,a,z] -> [X,A,Z] = sum pa[x,a,z] xc[x,m,X] ac[a,m,n,A] xc[z,n,Z]  (_left_a)
+DTensor step_a_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2);
+  DTensor t1({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
+  bmm(false, false, r0 * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1.p, o.nn * r1, 0, 1);
+  DTensor t2({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
+  bmm(false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, r1,
+      (long long)o.ra * o.nn * r1, t2.p, r1, (long long)o.nm * o.rA * r1, r0);
+  DTensor out({r1, o.rA, r1});
+  bmm(true, false, r1, o.rA * r1, r0 * o.nm, xc.p, r1, 0, t2.p, o.rA * r1, 0, out.p, o.rA * r1, 0, 1);
+  return out;
 }
 
-DTensor step_a_right(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
-  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, m, A, Z)
-  t = tensordot(ac, {1, 3}, t, {1, 2});        // (a, n, x, Z)
-  t = tensordot(t, {1, 3}, xc, {1, 2});        // (a, x, z)
-  return permute(t, {1, 0, 2});
+// pa[X,A,Z] -> [x,a,z]  (_right_a)
+DTensor step_a_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2);
+  DTensor t1({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
+  bmm(false, false, r0 * o.nm, o.rA * r1, r1, xc.p, r1, 0, phi.p, o.rA * r1, 0, t1.p, o.rA * r1, 0, 1);
+  DTensor t2({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
+  bmm(true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t1.p, r1,
+      (long long)o.nm * o.rA * r1, t2.p, r1, (long long)o.ra * o.nn * r1, r0);
+  DTensor out({r0, o.ra, r0});
+  bmm(false, true, r0 * o.ra, r0, o.nn * r1, t2.p, o.nn * r1, 0, xc.p, o.nn * r1, 0, out.p, r0, 0, 1);
+  return out;
 }
 
-DTensor step_n_left(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
-  DTensor t = tensordot(phi, {0}, xc, {0});    // (a1, a2, z, n1, X)
-  t = tensordot(t, {0, 3}, ac, {0, 2});        // (a2, z, X, k, A1)
-  t = tensordot(t, {0, 3}, ac, {0, 1});        // (z, X, A1, n2, A2)
-  return tensordot(t, {0, 3}, xc, {0, 1});     // (X, A1, A2, Z)
+// pn[x,a1,a2,z] -> [X,A1,A2,Z]: both copies act on column modes, contracted
+// over the shared row mode k (A^T A)  (_left_n)
+DTensor step_n_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2);
+  DTensor t1({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
+  bmm(false, false, r0 * o.ra * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1.p,
+      o.nn * r1, 0, 1);
+  DTensor t2({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
+  bmm(false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, r1,
+      (long long)o.ra * o.nn * r1, t2.p, r1, (long long)o.nm * o.rA * r1, r0 * o.ra);
+  DTensor t3({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
+  bmm(true, false, o.nn * o.rA, o.rA * r1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2.p, o.rA * r1,
+      (long long)o.ra * o.nm * o.rA * r1, t3.p, o.rA * r1, (long long)o.nn * o.rA * o.rA * r1, r0);
+  DTensor out({r1, o.rA, o.rA, r1});
+  bmm(true, false, r1, o.rA * o.rA * r1, r0 * o.nn, xc.p, r1, 0, t3.p, o.rA * o.rA * r1, 0, out.p,
+      o.rA * o.rA * r1, 0, 1);
+  return out;
 }
 
-DTensor step_n_right(const DTensor& phi, const DTensor& xc, const DTensor& ac) {
-  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, n1, A1, A2, Z)
-  t = tensordot(ac, {2, 3}, t, {1, 2});        // (a1, k, x, A2, Z)
-  t = tensordot(ac, {1, 3}, t, {1, 3});        // (a2, n2, a1, x, Z)
-  t = tensordot(t, {1, 4}, xc, {1, 2});        // (a2, a1, x, z)
-  return permute(t, {2, 1, 0, 3});
+// pn[X,A1,A2,Z] -> [x,a1,a2,z]  (_right_n)
+DTensor step_n_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2);
+  const int q = o.rA * o.rA * r1;
+  DTensor t1({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
+  bmm(false, false, r0 * o.nn, q, r1, xc.p, r1, 0, phi.p, q, 0, t1.p, q, 0, 1);
+  DTensor t2({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
+  bmm(false, false, o.ra * o.nm, o.rA * r1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1.p, o.rA * r1,
+      (long long)o.nn * q, t2.p, o.rA * r1, (long long)o.ra * o.nm * o.rA * r1, r0);
+  DTensor t3({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
+  bmm(true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t2.p, r1,
+      (long long)o.nm * o.rA * r1, t3.p, r1, (long long)o.ra * o.nn * r1, r0 * o.ra);
+  DTensor out({r0, o.ra, o.ra, r0});
+  bmm(false, true, r0 * o.ra * o.ra, r0, o.nn * r1, t3.p, o.nn * r1, 0, xc.p, o.nn * r1, 0, out.p,
+      r0, 0, 1);
+  return out;
 }
 
+// pg[x,a,b] -> [X,A,B] = sum pg xc[x,n,X] ac[a,k,n,A] bc[b,k,B]  (_left_g)
 DTensor step_g_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
-  DTensor t = tensordot(phi, {0}, xc, {0});    // (a, b, n, X)
-  t = tensordot(t, {0, 2}, ac, {0, 2});        // (b, X, k, A)
-  return tensordot(t, {0, 2}, bc, {0, 1});     // (X, A, B)
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
+  DTensor t1({r0, o.ra, o.nm, b1});  // [x, a, k, B]
+  bmm(false, false, r0 * o.ra, o.nm * b1, b0, phi.p, b0, 0, bc.p, o.nm * b1, 0, t1.p, o.nm * b1, 0, 1);
+  DTensor t2({r0, o.nn, o.rA, b1});  // [x, n, A, B]
+  bmm(true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1.p, b1,
+      (long long)o.ra * o.nm * b1, t2.p, b1, (long long)o.nn * o.rA * b1, r0);
+  DTensor out({r1, o.rA, b1});
+  bmm(true, false, r1, o.rA * b1, r0 * o.nn, xc.p, r1, 0, t2.p, o.rA * b1, 0, out.p, o.rA * b1, 0, 1);
+  return out;
 }
 
+// pg[X,A,B] -> [x,a,b]  (_right_g)
 DTensor step_g_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
-  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, n, A, B)
-  t = tensordot(ac, {2, 3}, t, {1, 2});        // (a, k, x, B)
-  t = tensordot(t, {1, 3}, bc, {1, 2});        // (a, x, b)
-  return permute(t, {1, 0, 2});
+  const OpDims o(ac);
+  const int r0 = xc.dim(0), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
+  DTensor t1({r0, o.nn, o.rA, b1});  // [x, n, A, B]
+  bmm(false, false, r0 * o.nn, o.rA * b1, r1, xc.p, r1, 0, phi.p, o.rA * b1, 0, t1.p, o.rA * b1, 0, 1);
+  DTensor t2({r0, o.ra, o.nm, b1});  // [x, a, k, B]
+  bmm(false, false, o.ra * o.nm, b1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1.p, b1,
+      (long long)o.nn * o.rA * b1, t2.p, b1, (long long)o.ra * o.nm * b1, r0);
+  DTensor out({r0, o.ra, b0});
+  bmm(false, true, r0 * o.ra, b0, o.nm * b1, t2.p, o.nm * b1, 0, bc.p, o.nm * b1, 0, out.p, b0, 0, 1);
+  return out;
 }
 
+// pb[x,b] -> [X,B]  (_left_b)
 DTensor step_b_left(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
-  DTensor t = tensordot(phi, {0}, xc, {0});    // (b, m, X)
-  return tensordot(t, {0, 1}, bc, {0, 1});     // (X, B)
+  const int r0 = xc.dim(0), n = xc.dim(1), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
+  DTensor t1({r0, n, b1});
+  bmm(false, false, r0, n * b1, b0, phi.p, b0, 0, bc.p, n * b1, 0, t1.p, n * b1, 0, 1);
+  DTensor out({r1, b1});
+  bmm(true, false, r1, b1, r0 * n, xc.p, r1, 0, t1.p, b1, 0, out.p, b1, 0, 1);
+  return out;
 }
 
+// pb[X,B] -> [x,b]  (_right_b)
 DTensor step_b_right(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
-  DTensor t = tensordot(xc, {2}, phi, {0});    // (x, m, B)
-  return tensordot(t, {1, 2}, bc, {1, 2});     // (x, b)
+  const int r0 = xc.dim(0), n = xc.dim(1), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
+  DTensor t1({r0, n, b1});
+  bmm(false, false, r0 * n, b1, r1, xc.p, r1, 0, phi.p, b1, 0, t1.p, b1, 0, 1);
+  DTensor out({r0, b0});
+  bmm(false, true, r0, b0, n * b1, t1.p, n * b1, 0, bc.p, n * b1, 0, out.p, b0, 0, 1);
+  return out;
 }
 
 // -- local systems (tt_solver.py:155-246) -------------------------------------
 
+// (x, m, y) = sum pbl[x,B] bc[B,m,C] pbr[y,C]  (_gal_rhs)
 DTensor galerkin_rhs(const DTensor& pbl, const DTensor& bc, const DTensor& pbr) {
-  DTensor t = tensordot(pbl, {1}, bc, {0});    // (x, m, c)
-  return tensordot(t, {2}, pbr, {1});          // (x, m, y)
+  const int rx = pbl.dim(0), b0 = bc.dim(0), n = bc.dim(1), b1 = bc.dim(2), ry = pbr.dim(0);
+  DTensor t1({rx, n, b1});
+  bmm(false, false, rx, n * b1, b0, pbl.p, b0, 0, bc.p, n * b1, 0, t1.p, n * b1, 0, 1);
+  DTensor out({rx, n, ry});
+  bmm(false, true, rx * n, ry, b1, t1.p, b1, 0, pbr.p, b1, 0, out.p, ry, 0, 1);
+  return out;
 }
 
+// projected A^T b (_ls_rhs)
 DTensor normal_rhs(const DTensor& pgl, const DTensor& ac, const DTensor& bc, const DTensor& pgr) {
-  DTensor t = tensordot(pgl, {2}, bc, {0});    // (x, a, k, B)
-  t = tensordot(t, {1, 2}, ac, {0, 1});        // (x, B, m, A)
-  return tensordot(t, {1, 3}, pgr, {2, 1});    // (x, m, y)
+  const OpDims o(ac);
+  const int rx = pgl.dim(0), b0 = bc.dim(0), b1 = bc.dim(2), ry = pgr.dim(0);
+  DTensor t1({rx, o.ra, o.nm, b1});  // [x, a, k, C]
+  bmm(false, false, rx * o.ra, o.nm * b1, b0, pgl.p, b0, 0, bc.p, o.nm * b1, 0, t1.p, o.nm * b1, 0, 1);
+  DTensor t2({rx, o.nn, o.rA, b1});  // [x, m, A, C]
+  bmm(true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1.p, b1,
+      (long long)o.ra * o.nm * b1, t2.p, b1, (long long)o.nn * o.rA * b1, rx);
+  DTensor out({rx, o.nn, ry});
+  bmm(false, true, rx * o.nn, ry, o.rA * b1, t2.p, o.rA * b1, 0, pgr.p, o.rA * b1, 0, out.p, ry, 0, 1);
+  return out;
 }
 
-DTensor normal_apply(const DTensor& pnl, const DTensor& ac, const DTensor& pnr, const DTensor& u) {
-  DTensor t = tensordot(pnl, {3}, u, {0});     // (x, a1, a2, n, w)
-  t = tensordot(t, {2, 3}, ac, {0, 2});        // (x, a1, w, k, A2)
-  t = tensordot(t, {1, 3}, ac, {0, 1});        // (x, w, A2, m, A1)
-  return tensordot(t, {1, 4, 2}, pnr, {3, 1, 2});  // (x, m, y)
-}
+// Local operators applied to raw device vectors (the Krylov matvecs and the
+// candidate scores); scratch is sized once per local system.
+struct NormalOp {  // (A^T A)-projected block (_ls_matvec / _LsApply)
+  const DTensor &pnl, &ac, &acg, &pnr;
+  OpDims o;
+  int rx, rz, ry, rw;
+  DTensor t1, t2, t3;
+  NormalOp(const DTensor& l, const DTensor& a, const DTensor& ag, const DTensor& r)
+      : pnl(l), ac(a), acg(ag), pnr(r), o(a), rx(l.dim(0)), rz(l.dim(3)), ry(r.dim(0)),
+        rw(r.dim(3)),
+        t1({rx, o.ra, o.ra, o.nn, rw}), t2({rx, o.ra, o.nm, o.rA, rw}),
+        t3({rx, o.nn, o.rA, o.rA, rw}) {}
+  void operator()(const double* u, double* out) {
+    bmm(false, false, rx * o.ra * o.ra, o.nn * rw, rz, pnl.p, rz, 0, u, o.nn * rw, 0, t1.p,
+        o.nn * rw, 0, 1);
+    bmm(false, false, o.nm * o.rA, rw, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rw,
+        (long long)o.ra * o.nn * rw, t2.p, rw, (long long)o.nm * o.rA * rw, rx * o.ra);
+    bmm(true, false, o.nn * o.rA, o.rA * rw, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2.p, o.rA * rw,
+        (long long)o.ra * o.nm * o.rA * rw, t3.p, o.rA * rw, (long long)o.nn * o.rA * o.rA * rw, rx);
+    const int q = o.rA * o.rA * rw;
+    bmm(false, true, rx * o.nn, ry, q, t3.p, q, 0, pnr.p, q, 0, out, ry, 0, 1);
+  }
+  DTensor apply(const DTensor& u) {
+    DTensor out({rx, o.nn, ry});
+    (*this)(u.p, out.p);
+    return out;
+  }
+};
+
+struct GalerkinOp {  // Galerkin block (_gal_matvec)
+  const DTensor &pal, &acg, &par;
+  OpDims o;
+  int rx, rX, ry, rY;
+  DTensor t1, t2;
+  GalerkinOp(const DTensor& l, const DTensor& a, const DTensor& ag, const DTensor& r)
+      : pal(l), acg(ag), par(r), o(a), rx(l.dim(0)), rX(l.dim(2)), ry(r.dim(0)), rY(r.dim(2)),
+        t1({rx, o.ra, o.nn, rY}), t2({rx, o.nm, o.rA, rY}) {}
+  void operator()(const double* u, double* out) {
+    bmm(false, false, rx * o.ra, o.nn * rY, rX, pal.p, rX, 0, u, o.nn * rY, 0, t1.p, o.nn * rY, 0, 1);
+    bmm(false, false, o.nm * o.rA, rY, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rY,
+        (long long)o.ra * o.nn * rY, t2.p, rY, (long long)o.nm * o.rA * rY, rx);
+    bmm(false, true, rx * o.nm, ry, o.rA * rY, t2.p, o.rA * rY, 0, par.p, o.rA * rY, 0, out, ry, 0, 1);
+  }
+};
 
 // Column-major normal-equation block N[(x,m,y),(z,n,w)] (tt_solver.py:239-246).
 DTensor normal_matrix(const DTensor& pnl, const DTensor& ac, const DTensor& pnr) {
@@ -243,12 +387,6 @@ DTensor normal_matrix(const DTensor& pnl, const DTensor& ac, const DTensor& pnr)
   DTensor t = tensordot(pnl, {1, 2}, g, {0, 3});  // (x, z, m, P, n, Q)
   t = tensordot(t, {3, 5}, pnr, {1, 2});       // (x, z, m, n, y, w)
   return permute(t, {1, 3, 5, 0, 2, 4});       // (z, n, w | x, m, y): column-major
-}
-
-DTensor galerkin_apply(const DTensor& pal, const DTensor& ac, const DTensor& par, const DTensor& u) {
-  DTensor t = tensordot(pal, {2}, u, {0});     // (x, a, n, w)
-  t = tensordot(t, {1, 2}, ac, {0, 2});        // (x, w, m, b)
-  return tensordot(t, {1, 3}, par, {2, 1});    // (x, m, y)
 }
 
 DTensor normal_diagonal(const DTensor& pnl, const DTensor& ac, const DTensor& pnr) {
@@ -266,16 +404,6 @@ DTensor normal_diagonal(const DTensor& pnl, const DTensor& ac, const DTensor& pn
   }
   T2S2_CHECK_LAUNCH();
   return out;
-}
-
-// Wrap a tensor-valued local operator as a flat device matvec.
-MatVec as_matvec(std::vector<int> shape, std::function<DTensor(const DTensor&)> f) {
-  return [shape, f](const double* in, double* out) {
-    DTensor u(shape);
-    dcopy(u.p, in, u.size());
-    DTensor r = f(u);
-    dcopy(out, r.p, r.size());
-  };
 }
 
 DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& par) {
@@ -460,11 +588,11 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
 
 // -- residual (tt_solver.py:305-329) ----------------------------------------------
 
-double measure_residual(const Train& A, const std::vector<DTensor>& x, const Train& rhs,
-                        double bnorm) {
+double measure_residual(const Train& A, const std::vector<DTensor>& acg,
+                        const std::vector<DTensor>& x, const Train& rhs, double bnorm) {
   const int d = A.d();
   DTensor phi = ones({1, 1, 1, 1});
-  for (int l = 0; l < d; ++l) phi = step_n_left(phi, x[l], A.cores[l]);
+  for (int l = 0; l < d; ++l) phi = step_n_left(phi, x[l], A.cores[l], acg[l]);
   const double axax = scalar_to_host(phi.p);
   DTensor psi = ones({1, 1, 1});
   for (int l = 0; l < d; ++l) psi = step_g_left(psi, x[l], A.cores[l], rhs.cores[l]);
@@ -491,9 +619,12 @@ struct Sweep {
   int gal_rejects = 0;
   int gal_cap;
   std::vector<DTensor> la, ln, lg, lb, ra, rn, rg, rb;
+  std::vector<DTensor> acg;  // per-core operator layout (m, A, a, n)
   Sweep(const Train& a, const Train& b, const SolverConfig& c)
       : A(a), rhs(b), cfg(c), d(a.d()), gal_cap(2 * a.d()),
-        la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1) {}
+        la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1) {
+    for (const DTensor& ac : a.cores) acg.push_back(op_layout(ac));
+  }
 
   Probe probe;
 
@@ -508,7 +639,8 @@ struct Sweep {
     const long long size = (long long)u_old.size();
     DTensor c_gal = galerkin_rhs(lb[l], bc, rb[l + 1]);
     DTensor c_ls = normal_rhs(lg[l], ac, bc, rg[l + 1]);
-    DTensor nu_old = normal_apply(ln[l], ac, rn[l + 1], u_old);
+    NormalOp nop(ln[l], ac, acg[l], rn[l + 1]);
+    DTensor nu_old = nop.apply(u_old);
     probe.run(0, u_old, nu_old, c_ls);
     probe.clear_info();
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
@@ -522,12 +654,12 @@ struct Sweep {
       } else {
         // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
         u_gal = u_old.clone();
-        const DTensor &pal = la[l], &par = ra[l + 1];
-        gmres(as_matvec(u_old.shape, [&](const DTensor& u) { return galerkin_apply(pal, ac, par, u); }),
-              (int)size, c_gal.p, u_gal.p, inner_rtol, 40, 10);
+        GalerkinOp gop(la[l], ac, acg[l], ra[l + 1]);
+        gmres([&](const double* in, double* out) { gop(in, out); }, (int)size, c_gal.p, u_gal.p,
+              inner_rtol, 40, 10);
       }
       u_gal.view(u_old.shape);
-      nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
+      nu_gal = nop.apply(u_gal);
       probe.run(1, u_gal, nu_gal, c_ls);
     }
     double h[12];
@@ -538,7 +670,7 @@ struct Sweep {
       DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
       lstsq_dense(B, c_gal, u_gal);
       u_gal.view(u_old.shape);
-      nu_gal = normal_apply(ln[l], ac, rn[l + 1], u_gal);
+      nu_gal = nop.apply(u_gal);
       probe.clear_info();
       probe.run(1, u_gal, nu_gal, c_ls);
       probe.read(h, &info);
@@ -571,13 +703,12 @@ struct Sweep {
       } else {
         // scipy cg(x0=u_old, rtol, atol=0, maxiter=250, M=diag^{-1})
         u_ls = u_old.clone();
-        const DTensor &pnl = ln[l], &pnr = rn[l + 1];
-        DTensor dg = normal_diagonal(pnl, ac, pnr);
-        pcg(as_matvec(u_old.shape, [&](const DTensor& u) { return normal_apply(pnl, ac, pnr, u); }),
-            (int)size, c_ls.p, u_ls.p, dg.p, inner_rtol, 250);
+        DTensor dg = normal_diagonal(ln[l], ac, rn[l + 1]);
+        pcg([&](const double* in, double* out) { nop(in, out); }, (int)size, c_ls.p, u_ls.p, dg.p,
+            inner_rtol, 250);
       }
       u_ls.view(u_old.shape);
-      DTensor nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
+      DTensor nu_ls = nop.apply(u_ls);
       probe.run(2, u_ls, nu_ls, c_ls);
       probe.read(h, &info);
       if (direct && info != 0) {
@@ -586,7 +717,7 @@ struct Sweep {
         Nm.view({(int)size, (int)size});
         lstsq_dense(Nm, c_ls, u_ls);
         u_ls.view(u_old.shape);
-        nu_ls = normal_apply(ln[l], ac, rn[l + 1], u_ls);
+        nu_ls = nop.apply(u_ls);
         probe.clear_info();
         probe.run(2, u_ls, nu_ls, c_ls);
         probe.read(h, &info);
@@ -637,8 +768,8 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     sw.rg[d] = ones({1, 1, 1});
     sw.rb[d] = ones({1, 1});
     for (int l = d - 1; l > 0; --l) {
-      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l]);
-      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l]);
+      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
+      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
       sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
       sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
     }
@@ -669,8 +800,8 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       gemm(false, false, keep, rest, r1, 1.0, sp.carry.p, r1, nx.p, rest, 0.0, nn.p, rest);
       if (sp.extra > 0) dfill(nn.p + (size_t)keep * rest, 0.0, (size_t)sp.extra * rest);
       cores[l + 1] = std::move(nn);
-      sw.la[l + 1] = step_a_left(sw.la[l], cores[l], A.cores[l]);
-      sw.ln[l + 1] = step_n_left(sw.ln[l], cores[l], A.cores[l]);
+      sw.la[l + 1] = step_a_left(sw.la[l], cores[l], A.cores[l], sw.acg[l]);
+      sw.ln[l + 1] = step_n_left(sw.ln[l], cores[l], A.cores[l], sw.acg[l]);
       sw.lg[l + 1] = step_g_left(sw.lg[l], cores[l], A.cores[l], rhs.cores[l]);
       sw.lb[l + 1] = step_b_left(sw.lb[l], cores[l], rhs.cores[l]);
     }
@@ -703,12 +834,12 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       if (sp.extra > 0) dfill(np.p, 0.0, np.size());
       gemm(false, false, rows, keep, r0, 1.0, pv.p, r0, sp.carry.p, keep, 0.0, np.p, nk);
       cores[l - 1] = std::move(np);
-      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l]);
-      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l]);
+      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
+      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
       sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
       sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
     }
-    current_res = measure_residual(A, cores, rhs, bnorm);
+    current_res = measure_residual(A, sw.acg, cores, rhs, bnorm);
     rep.residuals.push_back(current_res);
     int mr = 1;
     double stored = 0.0, dense = 1.0;

@@ -18,9 +18,14 @@ bcs = [to_device(b) for b, _ in fs]; srcs = [to_device(s) for _, s in fs]
 cfg = SolverConfig(**recipe.solver)
 _native.check(_native.lib().t2s2_synchronize(_native.context()))
 prof = len(sys.argv) > 3 and sys.argv[3] == "prof"
+# T2S2_PROFILE_FROM=k: cudaProfilerStart before step k (ncu --profile-from-start off)
+prof_from = int(os.environ.get("T2S2_PROFILE_FROM", "-1"))
 state = hs
 tot = 0.0
 for k in range(steps):
+    if k == prof_from:
+        import ctypes
+        ctypes.CDLL("libcudart.so.12").cudaProfilerStart()
     _native.stats_reset(profile_events=prof)
     t0 = time.time()
     stored, rows = march_device(hl, hr, state, 1, [bcs[k]], [srcs[k]], recipe.step_tol, cfg, store_stride=1)
