@@ -421,7 +421,8 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
 
 // Dense direct solve of a column-major N x N system; the LU info (0, or
 // 1 + first zero pivot) lands in *info_dev and is read back by the caller.
-void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
+// Partial-pivoting dense solve (the reference's numpy.linalg.solve).
+void dense_solve_pivoted(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   const int N = M.dim(0);
   int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
   out = rhs.clone();
@@ -430,6 +431,16 @@ void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
     lu_solve(N, M.p, ipiv, out.p);
   }
   allocator().release(reinterpret_cast<double*>(ipiv));
+}
+
+// Local dense solve: the verified no-pivot LU first (identical factors when
+// partial pivoting would not interchange rows); *info_dev == -1 afterwards
+// means it declined and the caller must rebuild M and call
+// dense_solve_pivoted.
+void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
+  out = rhs.clone();
+  if (lu_solve_nopivot(M.dim(0), M.p, out.p, info_dev)) return;
+  dense_solve_pivoted(M, rhs, out, info_dev);
 }
 
 // Minimum-norm least squares of a singular column-major N x N system, the
@@ -665,6 +676,16 @@ struct Sweep {
     double h[12];
     int info = 0;
     probe.read(h, &info);
+    if (try_gal && direct && info == -1) {
+      // the block needs row interchanges: rebuild it, partial pivoting
+      DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+      probe.clear_info();
+      dense_solve_pivoted(B, c_gal, u_gal, probe.info());
+      u_gal.view(u_old.shape);
+      nu_gal = nop.apply(u_gal);
+      probe.run(1, u_gal, nu_gal, c_ls);
+      probe.read(h, &info);
+    }
     if (try_gal && direct && info != 0) {
       // singular Galerkin block: numpy.linalg.lstsq fallback (tt_solver.py:362)
       DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
@@ -711,6 +732,16 @@ struct Sweep {
       DTensor nu_ls = nop.apply(u_ls);
       probe.run(2, u_ls, nu_ls, c_ls);
       probe.read(h, &info);
+      if (direct && info == -1) {
+        DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
+        Nm.view({(int)size, (int)size});
+        probe.clear_info();
+        dense_solve_pivoted(Nm, c_ls, u_ls, probe.info());
+        u_ls.view(u_old.shape);
+        nu_ls = nop.apply(u_ls);
+        probe.run(2, u_ls, nu_ls, c_ls);
+        probe.read(h, &info);
+      }
       if (direct && info != 0) {
         // singular normal block: numpy.linalg.lstsq fallback (tt_solver.py:395)
         DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);

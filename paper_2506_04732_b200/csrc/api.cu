@@ -397,12 +397,24 @@ int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const d
     to_device(rhs.p, b, n);
     int* piv = reinterpret_cast<int*>(allocator().alloc((size_t)n / 2 + 1));
     int* info = reinterpret_cast<int*>(allocator().alloc(1));
-    if (!lu_solve_fused(n, A.p, rhs.p, piv, info)) {
+    int h = 0;
+    // verified no-pivot LU first, as the local solves do; on refusal the
+    // pivoting kernel runs on a fresh copy
+    DTensor A2({n, n}), rhs2({n});
+    dcopy(A2.p, A.p, (size_t)n * n);
+    dcopy(rhs2.p, rhs.p, n);
+    if (lu_solve_nopivot(n, A2.p, rhs2.p, info)) {
+      T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+      T2S2_CUDA(cudaStreamSynchronize(stream()));
+      if (h == 0) dcopy(rhs.p, rhs2.p, n);
+    } else {
+      h = -1;
+    }
+    if (h == -1 && !lu_solve_fused(n, A.p, rhs.p, piv, info)) {
       lu_factor(n, A.p, piv, info);
       lu_solve(n, A.p, piv, rhs.p);
     }
-    int h = 0;
-    T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    if (h == -1) T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     to_host(x, rhs.p, n);
     allocator().release(reinterpret_cast<double*>(piv));
     allocator().release(reinterpret_cast<double*>(info));

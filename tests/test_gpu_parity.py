@@ -208,6 +208,27 @@ def test_dense_local_solve_kernel(pk, n):
     assert np.linalg.norm(a @ x - b) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(x)
 
 
+@pytest.mark.parametrize("n", [7, 64, 65, 300, 1000])
+def test_dense_local_solve_without_interchanges(pk, n):
+    """Column diagonally dominant matrices: partial pivoting makes no
+    interchange, so the verified no-pivot kernel alone must solve them, to
+    LAPACK's accuracy."""
+    from paper_2506_04732_b200 import _native
+
+    rng = np.random.default_rng(100 + n)
+    a = rng.standard_normal((n, n))
+    a += np.diag(np.abs(a).sum(0))
+    b = rng.standard_normal(n)
+    _native.stats_reset()
+    x = _native.dense_solve(a, b)
+    st = _native.stats_read()
+    assert st["lu_nopivot"]["launches"] == 1
+    assert st.get("lu_fused", {}).get("launches", 0) == 0
+    want = np.linalg.solve(a, b)
+    assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
+    assert np.linalg.norm(a @ x - b) <= 1e-13 * np.linalg.norm(a) * np.linalg.norm(x)
+
+
 def test_dense_local_solve_singular(pk):
     from paper_2506_04732_b200 import _native
 
