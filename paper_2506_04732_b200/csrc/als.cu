@@ -194,145 +194,156 @@ struct OpDims {
 };
 
 // -- interface recurrences (tt_solver.py:98-151) -----------------------------
+//
+// Each recurrence adds its GEMMs to a GemmBatch at stages s0, s0+1, ...:
+// the four families of a move (and the chains of successive cores) run as
+// one program.  Outputs are allocated here; intermediates belong to the batch.
 
 // pa[x,a,z] -> [X,A,Z] = sum pa[x,a,z] xc[x,m,X] ac[a,m,n,A] xc[z,n,Z]  (_left_a)
-DTensor step_a_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+DTensor step_a_left(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                    const DTensor& acg) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2);
-  DTensor t1({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
-  bmm(false, false, r0 * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1.p, o.nn * r1, 0, 1);
-  DTensor t2({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
-  bmm(false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, r1,
-      (long long)o.ra * o.nn * r1, t2.p, r1, (long long)o.nm * o.rA * r1, r0);
+  double* t1 = gb.temp({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
+  gb.add(s0, false, false, r0 * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1, o.nn * r1, 0);
+  double* t2 = gb.temp({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
+  gb.add(s0 + 1, false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1, r1,
+         (long long)o.ra * o.nn * r1, t2, r1, (long long)o.nm * o.rA * r1, r0);
   DTensor out({r1, o.rA, r1});
-  bmm(true, false, r1, o.rA * r1, r0 * o.nm, xc.p, r1, 0, t2.p, o.rA * r1, 0, out.p, o.rA * r1, 0, 1);
+  gb.add(s0 + 2, true, false, r1, o.rA * r1, r0 * o.nm, xc.p, r1, 0, t2, o.rA * r1, 0, out.p, o.rA * r1, 0);
   return out;
 }
 
 // pa[X,A,Z] -> [x,a,z]  (_right_a)
-DTensor step_a_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+DTensor step_a_right(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                     const DTensor& acg) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2);
-  DTensor t1({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
-  bmm(false, false, r0 * o.nm, o.rA * r1, r1, xc.p, r1, 0, phi.p, o.rA * r1, 0, t1.p, o.rA * r1, 0, 1);
-  DTensor t2({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
-  bmm(true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t1.p, r1,
-      (long long)o.nm * o.rA * r1, t2.p, r1, (long long)o.ra * o.nn * r1, r0);
+  double* t1 = gb.temp({r0, o.nm, o.rA, r1});  // [x, m, A, Z]
+  gb.add(s0, false, false, r0 * o.nm, o.rA * r1, r1, xc.p, r1, 0, phi.p, o.rA * r1, 0, t1, o.rA * r1, 0);
+  double* t2 = gb.temp({r0, o.ra, o.nn, r1});  // [x, a, n, Z]
+  gb.add(s0 + 1, true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t1, r1,
+         (long long)o.nm * o.rA * r1, t2, r1, (long long)o.ra * o.nn * r1, r0);
   DTensor out({r0, o.ra, r0});
-  bmm(false, true, r0 * o.ra, r0, o.nn * r1, t2.p, o.nn * r1, 0, xc.p, o.nn * r1, 0, out.p, r0, 0, 1);
+  gb.add(s0 + 2, false, true, r0 * o.ra, r0, o.nn * r1, t2, o.nn * r1, 0, xc.p, o.nn * r1, 0, out.p, r0, 0);
   return out;
 }
 
 // pn[x,a1,a2,z] -> [X,A1,A2,Z]: both copies act on column modes, contracted
 // over the shared row mode k (A^T A)  (_left_n)
-DTensor step_n_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+DTensor step_n_left(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                    const DTensor& acg) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2);
-  DTensor t1({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
-  bmm(false, false, r0 * o.ra * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1.p,
-      o.nn * r1, 0, 1);
-  DTensor t2({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
-  bmm(false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, r1,
-      (long long)o.ra * o.nn * r1, t2.p, r1, (long long)o.nm * o.rA * r1, r0 * o.ra);
-  DTensor t3({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
-  bmm(true, false, o.nn * o.rA, o.rA * r1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2.p, o.rA * r1,
-      (long long)o.ra * o.nm * o.rA * r1, t3.p, o.rA * r1, (long long)o.nn * o.rA * o.rA * r1, r0);
+  double* t1 = gb.temp({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
+  gb.add(s0, false, false, r0 * o.ra * o.ra, o.nn * r1, r0, phi.p, r0, 0, xc.p, o.nn * r1, 0, t1,
+         o.nn * r1, 0);
+  double* t2 = gb.temp({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
+  gb.add(s0 + 1, false, false, o.nm * o.rA, r1, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1, r1,
+         (long long)o.ra * o.nn * r1, t2, r1, (long long)o.nm * o.rA * r1, r0 * o.ra);
+  double* t3 = gb.temp({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
+  gb.add(s0 + 2, true, false, o.nn * o.rA, o.rA * r1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2, o.rA * r1,
+         (long long)o.ra * o.nm * o.rA * r1, t3, o.rA * r1, (long long)o.nn * o.rA * o.rA * r1, r0);
   DTensor out({r1, o.rA, o.rA, r1});
-  bmm(true, false, r1, o.rA * o.rA * r1, r0 * o.nn, xc.p, r1, 0, t3.p, o.rA * o.rA * r1, 0, out.p,
-      o.rA * o.rA * r1, 0, 1);
+  gb.add(s0 + 3, true, false, r1, o.rA * o.rA * r1, r0 * o.nn, xc.p, r1, 0, t3, o.rA * o.rA * r1, 0,
+         out.p, o.rA * o.rA * r1, 0);
   return out;
 }
 
 // pn[X,A1,A2,Z] -> [x,a1,a2,z]  (_right_n)
-DTensor step_n_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& acg) {
+DTensor step_n_right(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                     const DTensor& acg) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2);
   const int q = o.rA * o.rA * r1;
-  DTensor t1({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
-  bmm(false, false, r0 * o.nn, q, r1, xc.p, r1, 0, phi.p, q, 0, t1.p, q, 0, 1);
-  DTensor t2({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
-  bmm(false, false, o.ra * o.nm, o.rA * r1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1.p, o.rA * r1,
-      (long long)o.nn * q, t2.p, o.rA * r1, (long long)o.ra * o.nm * o.rA * r1, r0);
-  DTensor t3({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
-  bmm(true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t2.p, r1,
-      (long long)o.nm * o.rA * r1, t3.p, r1, (long long)o.ra * o.nn * r1, r0 * o.ra);
+  double* t1 = gb.temp({r0, o.nn, o.rA, o.rA, r1});  // [x, n1, A1, A2, Z]
+  gb.add(s0, false, false, r0 * o.nn, q, r1, xc.p, r1, 0, phi.p, q, 0, t1, q, 0);
+  double* t2 = gb.temp({r0, o.ra, o.nm, o.rA, r1});  // [x, a1, k, A2, Z]
+  gb.add(s0 + 1, false, false, o.ra * o.nm, o.rA * r1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1, o.rA * r1,
+         (long long)o.nn * q, t2, o.rA * r1, (long long)o.ra * o.nm * o.rA * r1, r0);
+  double* t3 = gb.temp({r0, o.ra, o.ra, o.nn, r1});  // [x, a1, a2, n2, Z]
+  gb.add(s0 + 2, true, false, o.ra * o.nn, r1, o.nm * o.rA, acg.p, o.ra * o.nn, 0, t2, r1,
+         (long long)o.nm * o.rA * r1, t3, r1, (long long)o.ra * o.nn * r1, r0 * o.ra);
   DTensor out({r0, o.ra, o.ra, r0});
-  bmm(false, true, r0 * o.ra * o.ra, r0, o.nn * r1, t3.p, o.nn * r1, 0, xc.p, o.nn * r1, 0, out.p,
-      r0, 0, 1);
+  gb.add(s0 + 3, false, true, r0 * o.ra * o.ra, r0, o.nn * r1, t3, o.nn * r1, 0, xc.p, o.nn * r1, 0,
+         out.p, r0, 0);
   return out;
 }
 
 // pg[x,a,b] -> [X,A,B] = sum pg xc[x,n,X] ac[a,k,n,A] bc[b,k,B]  (_left_g)
-DTensor step_g_left(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
+DTensor step_g_left(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                    const DTensor& bc) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
-  DTensor t1({r0, o.ra, o.nm, b1});  // [x, a, k, B]
-  bmm(false, false, r0 * o.ra, o.nm * b1, b0, phi.p, b0, 0, bc.p, o.nm * b1, 0, t1.p, o.nm * b1, 0, 1);
-  DTensor t2({r0, o.nn, o.rA, b1});  // [x, n, A, B]
-  bmm(true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1.p, b1,
-      (long long)o.ra * o.nm * b1, t2.p, b1, (long long)o.nn * o.rA * b1, r0);
+  double* t1 = gb.temp({r0, o.ra, o.nm, b1});  // [x, a, k, B]
+  gb.add(s0, false, false, r0 * o.ra, o.nm * b1, b0, phi.p, b0, 0, bc.p, o.nm * b1, 0, t1, o.nm * b1, 0);
+  double* t2 = gb.temp({r0, o.nn, o.rA, b1});  // [x, n, A, B]
+  gb.add(s0 + 1, true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1, b1,
+         (long long)o.ra * o.nm * b1, t2, b1, (long long)o.nn * o.rA * b1, r0);
   DTensor out({r1, o.rA, b1});
-  bmm(true, false, r1, o.rA * b1, r0 * o.nn, xc.p, r1, 0, t2.p, o.rA * b1, 0, out.p, o.rA * b1, 0, 1);
+  gb.add(s0 + 2, true, false, r1, o.rA * b1, r0 * o.nn, xc.p, r1, 0, t2, o.rA * b1, 0, out.p, o.rA * b1, 0);
   return out;
 }
 
 // pg[X,A,B] -> [x,a,b]  (_right_g)
-DTensor step_g_right(const DTensor& phi, const DTensor& xc, const DTensor& ac, const DTensor& bc) {
+DTensor step_g_right(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& ac,
+                     const DTensor& bc) {
   const OpDims o(ac);
   const int r0 = xc.dim(0), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
-  DTensor t1({r0, o.nn, o.rA, b1});  // [x, n, A, B]
-  bmm(false, false, r0 * o.nn, o.rA * b1, r1, xc.p, r1, 0, phi.p, o.rA * b1, 0, t1.p, o.rA * b1, 0, 1);
-  DTensor t2({r0, o.ra, o.nm, b1});  // [x, a, k, B]
-  bmm(false, false, o.ra * o.nm, b1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1.p, b1,
-      (long long)o.nn * o.rA * b1, t2.p, b1, (long long)o.ra * o.nm * b1, r0);
+  double* t1 = gb.temp({r0, o.nn, o.rA, b1});  // [x, n, A, B]
+  gb.add(s0, false, false, r0 * o.nn, o.rA * b1, r1, xc.p, r1, 0, phi.p, o.rA * b1, 0, t1, o.rA * b1, 0);
+  double* t2 = gb.temp({r0, o.ra, o.nm, b1});  // [x, a, k, B]
+  gb.add(s0 + 1, false, false, o.ra * o.nm, b1, o.nn * o.rA, ac.p, o.nn * o.rA, 0, t1, b1,
+         (long long)o.nn * o.rA * b1, t2, b1, (long long)o.ra * o.nm * b1, r0);
   DTensor out({r0, o.ra, b0});
-  bmm(false, true, r0 * o.ra, b0, o.nm * b1, t2.p, o.nm * b1, 0, bc.p, o.nm * b1, 0, out.p, b0, 0, 1);
+  gb.add(s0 + 2, false, true, r0 * o.ra, b0, o.nm * b1, t2, o.nm * b1, 0, bc.p, o.nm * b1, 0, out.p, b0, 0);
   return out;
 }
 
 // pb[x,b] -> [X,B]  (_left_b)
-DTensor step_b_left(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
+DTensor step_b_left(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& bc) {
   const int r0 = xc.dim(0), n = xc.dim(1), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
-  DTensor t1({r0, n, b1});
-  bmm(false, false, r0, n * b1, b0, phi.p, b0, 0, bc.p, n * b1, 0, t1.p, n * b1, 0, 1);
+  double* t1 = gb.temp({r0, n, b1});
+  gb.add(s0, false, false, r0, n * b1, b0, phi.p, b0, 0, bc.p, n * b1, 0, t1, n * b1, 0);
   DTensor out({r1, b1});
-  bmm(true, false, r1, b1, r0 * n, xc.p, r1, 0, t1.p, b1, 0, out.p, b1, 0, 1);
+  gb.add(s0 + 1, true, false, r1, b1, r0 * n, xc.p, r1, 0, t1, b1, 0, out.p, b1, 0);
   return out;
 }
 
 // pb[X,B] -> [x,b]  (_right_b)
-DTensor step_b_right(const DTensor& phi, const DTensor& xc, const DTensor& bc) {
+DTensor step_b_right(GemmBatch& gb, int s0, const DTensor& phi, const DTensor& xc, const DTensor& bc) {
   const int r0 = xc.dim(0), n = xc.dim(1), r1 = xc.dim(2), b0 = bc.dim(0), b1 = bc.dim(2);
-  DTensor t1({r0, n, b1});
-  bmm(false, false, r0 * n, b1, r1, xc.p, r1, 0, phi.p, b1, 0, t1.p, b1, 0, 1);
+  double* t1 = gb.temp({r0, n, b1});
+  gb.add(s0, false, false, r0 * n, b1, r1, xc.p, r1, 0, phi.p, b1, 0, t1, b1, 0);
   DTensor out({r0, b0});
-  bmm(false, true, r0, b0, n * b1, t1.p, n * b1, 0, bc.p, n * b1, 0, out.p, b0, 0, 1);
+  gb.add(s0 + 1, false, true, r0, b0, n * b1, t1, n * b1, 0, bc.p, n * b1, 0, out.p, b0, 0);
   return out;
 }
 
 // -- local systems (tt_solver.py:155-246) -------------------------------------
 
 // (x, m, y) = sum pbl[x,B] bc[B,m,C] pbr[y,C]  (_gal_rhs)
-DTensor galerkin_rhs(const DTensor& pbl, const DTensor& bc, const DTensor& pbr) {
+DTensor galerkin_rhs(GemmBatch& gb, int s0, const DTensor& pbl, const DTensor& bc, const DTensor& pbr) {
   const int rx = pbl.dim(0), b0 = bc.dim(0), n = bc.dim(1), b1 = bc.dim(2), ry = pbr.dim(0);
-  DTensor t1({rx, n, b1});
-  bmm(false, false, rx, n * b1, b0, pbl.p, b0, 0, bc.p, n * b1, 0, t1.p, n * b1, 0, 1);
+  double* t1 = gb.temp({rx, n, b1});
+  gb.add(s0, false, false, rx, n * b1, b0, pbl.p, b0, 0, bc.p, n * b1, 0, t1, n * b1, 0);
   DTensor out({rx, n, ry});
-  bmm(false, true, rx * n, ry, b1, t1.p, b1, 0, pbr.p, b1, 0, out.p, ry, 0, 1);
+  gb.add(s0 + 1, false, true, rx * n, ry, b1, t1, b1, 0, pbr.p, b1, 0, out.p, ry, 0);
   return out;
 }
 
 // projected A^T b (_ls_rhs)
-DTensor normal_rhs(const DTensor& pgl, const DTensor& ac, const DTensor& bc, const DTensor& pgr) {
+DTensor normal_rhs(GemmBatch& gb, int s0, const DTensor& pgl, const DTensor& ac, const DTensor& bc,
+                   const DTensor& pgr) {
   const OpDims o(ac);
   const int rx = pgl.dim(0), b0 = bc.dim(0), b1 = bc.dim(2), ry = pgr.dim(0);
-  DTensor t1({rx, o.ra, o.nm, b1});  // [x, a, k, C]
-  bmm(false, false, rx * o.ra, o.nm * b1, b0, pgl.p, b0, 0, bc.p, o.nm * b1, 0, t1.p, o.nm * b1, 0, 1);
-  DTensor t2({rx, o.nn, o.rA, b1});  // [x, m, A, C]
-  bmm(true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1.p, b1,
-      (long long)o.ra * o.nm * b1, t2.p, b1, (long long)o.nn * o.rA * b1, rx);
+  double* t1 = gb.temp({rx, o.ra, o.nm, b1});  // [x, a, k, C]
+  gb.add(s0, false, false, rx * o.ra, o.nm * b1, b0, pgl.p, b0, 0, bc.p, o.nm * b1, 0, t1, o.nm * b1, 0);
+  double* t2 = gb.temp({rx, o.nn, o.rA, b1});  // [x, m, A, C]
+  gb.add(s0 + 1, true, false, o.nn * o.rA, b1, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t1, b1,
+         (long long)o.ra * o.nm * b1, t2, b1, (long long)o.nn * o.rA * b1, rx);
   DTensor out({rx, o.nn, ry});
-  bmm(false, true, rx * o.nn, ry, o.rA * b1, t2.p, o.rA * b1, 0, pgr.p, o.rA * b1, 0, out.p, ry, 0, 1);
+  gb.add(s0 + 2, false, true, rx * o.nn, ry, o.rA * b1, t2, o.rA * b1, 0, pgr.p, o.rA * b1, 0, out.p, ry, 0);
   return out;
 }
 
@@ -348,15 +359,22 @@ struct NormalOp {  // (A^T A)-projected block (_ls_matvec / _LsApply)
         rw(r.dim(3)),
         t1({rx, o.ra, o.ra, o.nn, rw}), t2({rx, o.ra, o.nm, o.rA, rw}),
         t3({rx, o.nn, o.rA, o.rA, rw}) {}
-  void operator()(const double* u, double* out) {
-    bmm(false, false, rx * o.ra * o.ra, o.nn * rw, rz, pnl.p, rz, 0, u, o.nn * rw, 0, t1.p,
-        o.nn * rw, 0, 1);
-    bmm(false, false, o.nm * o.rA, rw, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rw,
-        (long long)o.ra * o.nn * rw, t2.p, rw, (long long)o.nm * o.rA * rw, rx * o.ra);
-    bmm(true, false, o.nn * o.rA, o.rA * rw, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2.p, o.rA * rw,
-        (long long)o.ra * o.nm * o.rA * rw, t3.p, o.rA * rw, (long long)o.nn * o.rA * o.rA * rw, rx);
+  // 4 stages from s0; the scratch is shared, so one application per batch
+  void add(GemmBatch& gb, int s0, const double* u, double* out) {
+    gb.add(s0, false, false, rx * o.ra * o.ra, o.nn * rw, rz, pnl.p, rz, 0, u, o.nn * rw, 0, t1.p,
+           o.nn * rw, 0);
+    gb.add(s0 + 1, false, false, o.nm * o.rA, rw, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rw,
+           (long long)o.ra * o.nn * rw, t2.p, rw, (long long)o.nm * o.rA * rw, rx * o.ra);
+    gb.add(s0 + 2, true, false, o.nn * o.rA, o.rA * rw, o.ra * o.nm, ac.p, o.nn * o.rA, 0, t2.p,
+           o.rA * rw, (long long)o.ra * o.nm * o.rA * rw, t3.p, o.rA * rw,
+           (long long)o.nn * o.rA * o.rA * rw, rx);
     const int q = o.rA * o.rA * rw;
-    bmm(false, true, rx * o.nn, ry, q, t3.p, q, 0, pnr.p, q, 0, out, ry, 0, 1);
+    gb.add(s0 + 3, false, true, rx * o.nn, ry, q, t3.p, q, 0, pnr.p, q, 0, out, ry, 0);
+  }
+  void operator()(const double* u, double* out) {
+    GemmBatch gb;
+    add(gb, 0, u, out);
+    gb.run();
   }
   DTensor apply(const DTensor& u) {
     DTensor out({rx, o.nn, ry});
@@ -374,10 +392,12 @@ struct GalerkinOp {  // Galerkin block (_gal_matvec)
       : pal(l), acg(ag), par(r), o(a), rx(l.dim(0)), rX(l.dim(2)), ry(r.dim(0)), rY(r.dim(2)),
         t1({rx, o.ra, o.nn, rY}), t2({rx, o.nm, o.rA, rY}) {}
   void operator()(const double* u, double* out) {
-    bmm(false, false, rx * o.ra, o.nn * rY, rX, pal.p, rX, 0, u, o.nn * rY, 0, t1.p, o.nn * rY, 0, 1);
-    bmm(false, false, o.nm * o.rA, rY, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rY,
-        (long long)o.ra * o.nn * rY, t2.p, rY, (long long)o.nm * o.rA * rY, rx);
-    bmm(false, true, rx * o.nm, ry, o.rA * rY, t2.p, o.rA * rY, 0, par.p, o.rA * rY, 0, out, ry, 0, 1);
+    GemmBatch gb;
+    gb.add(0, false, false, rx * o.ra, o.nn * rY, rX, pal.p, rX, 0, u, o.nn * rY, 0, t1.p, o.nn * rY, 0);
+    gb.add(1, false, false, o.nm * o.rA, rY, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rY,
+           (long long)o.ra * o.nn * rY, t2.p, rY, (long long)o.nm * o.rA * rY, rx);
+    gb.add(2, false, true, rx * o.nm, ry, o.rA * rY, t2.p, o.rA * rY, 0, par.p, o.rA * rY, 0, out, ry, 0);
+    gb.run();
   }
 };
 
@@ -602,12 +622,29 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
 double measure_residual(const Train& A, const std::vector<DTensor>& acg,
                         const std::vector<DTensor>& x, const Train& rhs, double bnorm) {
   const int d = A.d();
+  // both Gram chains in one program (4 stages per core for <Ax,Ax>, 3 for <Ax,b>)
+  GemmBatch gb;
   DTensor phi = ones({1, 1, 1, 1});
-  for (int l = 0; l < d; ++l) phi = step_n_left(phi, x[l], A.cores[l], acg[l]);
-  const double axax = scalar_to_host(phi.p);
   DTensor psi = ones({1, 1, 1});
-  for (int l = 0; l < d; ++l) psi = step_g_left(psi, x[l], A.cores[l], rhs.cores[l]);
-  const double axb = scalar_to_host(psi.p);
+  std::vector<DTensor> keep;
+  for (int l = 0; l < d; ++l) {
+    DTensor nphi = step_n_left(gb, 4 * l, phi, x[l], A.cores[l], acg[l]);
+    DTensor npsi = step_g_left(gb, 4 * l, psi, x[l], A.cores[l], rhs.cores[l]);
+    keep.push_back(std::move(phi));
+    keep.push_back(std::move(psi));
+    phi = std::move(nphi);
+    psi = std::move(npsi);
+  }
+  gb.run();
+  keep.clear();
+  double hv[2];
+  {
+    DTensor two({2});
+    dcopy(two.p, phi.p, 1);
+    dcopy(two.p + 1, psi.p, 1);
+    to_host(hv, two.p, 2);
+  }
+  const double axax = hv[0], axb = hv[1];
   const double est_sq = axax - 2.0 * axb + bnorm * bnorm;
   const double est = std::sqrt(est_sq > 0.0 ? est_sq : 0.0) / bnorm;
   if (est_sq <= 0.0 || est < 1e-6) {
@@ -648,10 +685,16 @@ struct Sweep {
     const DTensor& bc = rhs.cores[l];
     const DTensor& u_old = cores[l];
     const long long size = (long long)u_old.size();
-    DTensor c_gal = galerkin_rhs(lb[l], bc, rb[l + 1]);
-    DTensor c_ls = normal_rhs(lg[l], ac, bc, rg[l + 1]);
     NormalOp nop(ln[l], ac, acg[l], rn[l + 1]);
-    DTensor nu_old = nop.apply(u_old);
+    DTensor nu_old({nop.rx, nop.o.nn, nop.ry});
+    DTensor c_gal, c_ls;
+    {
+      GemmBatch gb;
+      c_gal = galerkin_rhs(gb, 0, lb[l], bc, rb[l + 1]);
+      c_ls = normal_rhs(gb, 0, lg[l], ac, bc, rg[l + 1]);
+      nop.add(gb, 0, u_old.p, nu_old.p);
+      gb.run();
+    }
     probe.run(0, u_old, nu_old, c_ls);
     probe.clear_info();
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
@@ -798,11 +841,15 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     sw.rn[d] = ones({1, 1, 1, 1});
     sw.rg[d] = ones({1, 1, 1});
     sw.rb[d] = ones({1, 1});
-    for (int l = d - 1; l > 0; --l) {
-      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
-      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
-      sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
-      sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
+    {
+      GemmBatch gb;  // all four chains over the cores: 4 stages per core
+      for (int l = d - 1, s0 = 0; l > 0; --l, s0 += 4) {
+        sw.ra[l] = step_a_right(gb, s0, sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
+        sw.rn[l] = step_n_right(gb, s0, sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
+        sw.rg[l] = step_g_right(gb, s0, sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
+        sw.rb[l] = step_b_right(gb, s0, sw.rb[l + 1], cores[l], rhs.cores[l]);
+      }
+      gb.run();
     }
     sw.la[0] = ones({1, 1, 1});
     sw.ln[0] = ones({1, 1, 1, 1});
@@ -831,10 +878,14 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       gemm(false, false, keep, rest, r1, 1.0, sp.carry.p, r1, nx.p, rest, 0.0, nn.p, rest);
       if (sp.extra > 0) dfill(nn.p + (size_t)keep * rest, 0.0, (size_t)sp.extra * rest);
       cores[l + 1] = std::move(nn);
-      sw.la[l + 1] = step_a_left(sw.la[l], cores[l], A.cores[l], sw.acg[l]);
-      sw.ln[l + 1] = step_n_left(sw.ln[l], cores[l], A.cores[l], sw.acg[l]);
-      sw.lg[l + 1] = step_g_left(sw.lg[l], cores[l], A.cores[l], rhs.cores[l]);
-      sw.lb[l + 1] = step_b_left(sw.lb[l], cores[l], rhs.cores[l]);
+      {
+        GemmBatch gb;
+        sw.la[l + 1] = step_a_left(gb, 0, sw.la[l], cores[l], A.cores[l], sw.acg[l]);
+        sw.ln[l + 1] = step_n_left(gb, 0, sw.ln[l], cores[l], A.cores[l], sw.acg[l]);
+        sw.lg[l + 1] = step_g_left(gb, 0, sw.lg[l], cores[l], A.cores[l], rhs.cores[l]);
+        sw.lb[l + 1] = step_b_left(gb, 0, sw.lb[l], cores[l], rhs.cores[l]);
+        gb.run();
+      }
     }
     for (int l = d - 1; l >= 0; --l) {
       DTensor u, grad;
@@ -865,10 +916,14 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       if (sp.extra > 0) dfill(np.p, 0.0, np.size());
       gemm(false, false, rows, keep, r0, 1.0, pv.p, r0, sp.carry.p, keep, 0.0, np.p, nk);
       cores[l - 1] = std::move(np);
-      sw.ra[l] = step_a_right(sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
-      sw.rn[l] = step_n_right(sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
-      sw.rg[l] = step_g_right(sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
-      sw.rb[l] = step_b_right(sw.rb[l + 1], cores[l], rhs.cores[l]);
+      {
+        GemmBatch gb;
+        sw.ra[l] = step_a_right(gb, 0, sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
+        sw.rn[l] = step_n_right(gb, 0, sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
+        sw.rg[l] = step_g_right(gb, 0, sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
+        sw.rb[l] = step_b_right(gb, 0, sw.rb[l + 1], cores[l], rhs.cores[l]);
+        gb.run();
+      }
     }
     current_res = measure_residual(A, sw.acg, cores, rhs, bnorm);
     rep.residuals.push_back(current_res);

@@ -2,7 +2,12 @@
 // deterministic reductions.
 #include "blas.h"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cmath>
+
+namespace cg = cooperative_groups;
 
 namespace t2s2 {
 
@@ -28,21 +33,21 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// One TM x TN output tile (tile coordinates bx, by of batch entry bz).
 template <int TM, int TN, int TK, bool TC>
-__global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
-                                                   double alpha, const double* __restrict__ A,
-                                                   int lda, long long sA,
-                                                   const double* __restrict__ B, int ldb,
-                                                   long long sB, double beta, double* C, int ldc,
-                                                   long long sC) {
+__device__ __forceinline__ void gemm_tile(bool ta, bool tb, int M, int N, int K, double alpha,
+                                          const double* __restrict__ A, int lda, long long sA,
+                                          const double* __restrict__ B, int ldb, long long sB,
+                                          double beta, double* C, int ldc, long long sC, int bx,
+                                          int by, int bz) {
   constexpr int PA = TM * TK / 256, PB = TK * TN / 256, RM = TM / 16, RN = TN / 16;
   __shared__ double As[TK][TM + 1];
   __shared__ double Bs[TK][TN + 1];
-  A += blockIdx.z * sA;
-  B += blockIdx.z * sB;
-  C += blockIdx.z * sC;
+  A += bz * sA;
+  B += bz * sB;
+  C += bz * sC;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
+  const int row0 = by * TM, col0 = bx * TN;
   double ra[PA], rb[PB];
   auto fetch = [&](int k0) {
 #pragma unroll
@@ -161,6 +166,44 @@ __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int 
       double* c = C + (long long)gi * ldc + gj;
       *c = beta == 0.0 ? alpha * acc[i][j] : alpha * acc[i][j] + beta * (*c);
     }
+  }
+}
+
+template <int TM, int TN, int TK, bool TC>
+__global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
+                                                   double alpha, const double* __restrict__ A,
+                                                   int lda, long long sA,
+                                                   const double* __restrict__ B, int ldb,
+                                                   long long sB, double beta, double* C, int ldc,
+                                                   long long sC) {
+  gemm_tile<TM, TN, TK, TC>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
+                            blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// A GEMM program: stages of independent strided-batched GEMMs, one
+// cooperative launch, a grid barrier between stages.  Chains of small
+// contractions (the interface recurrences of a move, the local right-hand
+// sides, the operator applications) run as one kernel instead of one launch
+// per GEMM.
+__global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
+  cg::grid_group grid = cg::this_grid();
+  for (int s = 0; s < prog.nstage; ++s) {
+    const int q0 = prog.stage_first[s], q1 = prog.stage_first[s + 1];
+    int total = 0;
+    for (int q = q0; q < q1; ++q) total += prog.p[q].tiles;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int q = q0, tt = t;
+      while (tt >= prog.p[q].tiles) {
+        tt -= prog.p[q].tiles;
+        ++q;
+      }
+      const GemmProb& g = prog.p[q];
+      const int tn = (g.N + 31) / 32, tm = (g.M + 31) / 32;
+      const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
+      gemm_tile<32, 32, 32, true>(g.ta, g.tb, g.M, g.N, g.K, g.alpha, g.A, g.lda, g.sA, g.B, g.ldb,
+                                  g.sB, g.beta, g.C, g.ldc, g.sC, rem % tn, rem / tn, bz);
+    }
+    if (s + 1 < prog.nstage) grid.sync();
   }
 }
 
@@ -292,6 +335,89 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
     }
   }
   T2S2_CHECK_LAUNCH();
+}
+
+double* GemmBatch::temp(std::vector<int> shape) {
+  temps_.emplace_back(std::move(shape));
+  return temps_.back().p;
+}
+
+void GemmBatch::add(int stage, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
+                    long long sA, const double* B, int ldb, long long sB, double* C, int ldc,
+                    long long sC, int batch, double alpha, double beta) {
+  if (M <= 0 || N <= 0 || batch <= 0) return;
+  T2S2_REQUIRE(K > 0, kErrShape, "GemmBatch: empty contraction");
+  GemmProb g{};
+  g.A = A;
+  g.B = B;
+  g.C = C;
+  g.sA = sA;
+  g.sB = sB;
+  g.sC = sC;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.lda = lda;
+  g.ldb = ldb;
+  g.ldc = ldc;
+  g.batch = batch;
+  g.ta = ta;
+  g.tb = tb;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.tiles = ceil_div(M, 32) * ceil_div(N, 32) * batch;
+  items_.push_back({stage, g});
+  flops_ += 2.0 * M * N * (double)K * batch;
+}
+
+void GemmBatch::run() {
+  if (items_.empty()) return;
+  std::stable_sort(items_.begin(), items_.end(),
+                   [](const Item& x, const Item& y) { return x.stage < y.stage; });
+  // split into programs of at most kProgMaxProb problems / kProgMaxStage stages
+  size_t i = 0;
+  while (i < items_.size()) {
+    GemmProgram prog{};
+    int last_stage = -1, max_tiles = 0, stage_tiles = 0;
+    while (i < items_.size() && prog.nprob < kProgMaxProb) {
+      const Item& it = items_[i];
+      if (it.stage != last_stage) {
+        if (prog.nstage == kProgMaxStage) break;
+        prog.stage_first[prog.nstage++] = prog.nprob;
+        last_stage = it.stage;
+        stage_tiles = 0;
+      }
+      prog.p[prog.nprob++] = it.g;
+      stage_tiles += it.g.tiles;
+      max_tiles = stage_tiles > max_tiles ? stage_tiles : max_tiles;
+      ++i;
+    }
+    // a stage cut by the problem limit continues in the next program
+    prog.stage_first[prog.nstage] = prog.nprob;
+    static int nsm = 0;
+    if (nsm == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int grid = max_tiles < nsm ? max_tiles : nsm;
+    if (sm_budget() > 0 && grid > sm_budget()) grid = sm_budget();
+    if (grid < 1) grid = 1;
+    {
+      LaunchScope ls("gemm", flops_ * prog.nprob / (double)items_.size(), 0.0);
+      if (prog.nstage == 1) {
+        gemm_program_kernel<<<grid, 256, 0, stream()>>>(prog);
+      } else {
+        void* params[] = {&prog};
+        T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gemm_program_kernel, dim3(grid), dim3(256),
+                                              params, 0, stream()));
+      }
+    }
+    T2S2_CHECK_LAUNCH();
+  }
+  items_.clear();
+  temps_.clear();  // stream-ordered: safe to recycle once the launch is enqueued
+  flops_ = 0.0;
 }
 
 void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,

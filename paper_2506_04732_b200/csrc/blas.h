@@ -16,6 +16,45 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
                   long long sA, const double* B, int ldb, long long sB, double beta, double* C,
                   int ldc, long long sC, int batch);
 
+// A program of strided-batched GEMMs in stages: the problems of a stage are
+// independent, stage s+1 may read what stage s wrote.  One (cooperative)
+// launch per program with a grid barrier between stages.
+constexpr int kProgMaxProb = 24;
+constexpr int kProgMaxStage = 24;
+struct GemmProb {
+  const double* A;
+  const double* B;
+  double* C;
+  long long sA, sB, sC;
+  int M, N, K, lda, ldb, ldc, batch, tiles;
+  int ta, tb;
+  double alpha, beta;
+};
+struct GemmProgram {
+  int nprob, nstage;
+  int stage_first[kProgMaxStage + 1];
+  GemmProb p[kProgMaxProb];
+};
+
+class GemmBatch {
+ public:
+  // scratch that lives until run() has enqueued the program
+  double* temp(std::vector<int> shape);
+  void add(int stage, bool ta, bool tb, int M, int N, int K, const double* A, int lda, long long sA,
+           const double* B, int ldb, long long sB, double* C, int ldc, long long sC, int batch = 1,
+           double alpha = 1.0, double beta = 0.0);
+  void run();
+
+ private:
+  struct Item {
+    int stage;
+    GemmProb g;
+  };
+  std::vector<Item> items_;
+  std::vector<DTensor> temps_;
+  double flops_ = 0.0;
+};
+
 DTensor permute(const DTensor& a, const std::vector<int>& perm);
 
 // numpy.tensordot semantics: result axes are the free axes of a (in order)
