@@ -150,6 +150,12 @@ int t2s2_solve(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* rhs,
  * (numpy.linalg.solve's LinAlgError). */
 int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const double* b,
                      double* x);
+/* Row-major fp64 GEMM on device pointers, C = op(A) op(B) (op = transpose
+ * when the flag is set), through the engine's GEMM-program kernel — the
+ * contraction engine behind every tensordot of tt_solver.py, exposed for
+ * testing and benchmarking.  Enqueued on the context stream. */
+int t2s2_gemm(t2s2_context* ctx, int ta, int tb, int m, int n, int k, const double* a, int lda,
+              const double* b, int ldb, double* c, int ldc);
 int t2s2_residual(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* x,
                   const t2s2_train* rhs, double tol, double* out);
 

@@ -120,6 +120,7 @@ _SIGNATURES = {
     "t2s2_solve": (_I, [_P, _P, _P, _P, ctypes.POINTER(SolverConfigC), ctypes.POINTER(_P),
                         ctypes.POINTER(SolveReportC)]),
     "t2s2_dense_solve": (_I, [_P, _I, _DP, _DP, _DP]),
+    "t2s2_gemm": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I]),
     "t2s2_residual": (_I, [_P, _P, _P, _P, _D, _DP]),
     "t2s2_march": (_I, [_P, _P, _P, _P, _I, ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _D,
                         ctypes.POINTER(SolverConfigC), _I, ctypes.POINTER(_P),
@@ -238,6 +239,13 @@ def dense_solve(a, b):
     check(lib().t2s2_dense_solve(context(), n, a.ravel(order="F").ctypes.data_as(_DP),
                                  b.ctypes.data_as(_DP), x.ctypes.data_as(_DP)))
     return x
+
+
+def gemm_device(ta, tb, m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc):
+    """C = op(A) op(B) on device pointers (row-major fp64) through the
+    engine's GEMM program kernel (testing / benchmarking hook)."""
+    check(lib().t2s2_gemm(context(), int(ta), int(tb), m, n, k, ctypes.c_void_p(a_ptr), lda,
+                          ctypes.c_void_p(b_ptr), ldb, ctypes.c_void_p(c_ptr), ldc))
 
 
 def synchronize():

@@ -422,6 +422,16 @@ int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const d
   });
 }
 
+int t2s2_gemm(t2s2_context* ctx, int ta, int tb, int m, int n, int k, const double* a, int lda,
+              const double* b, int ldb, double* c, int ldc) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(m >= 1 && n >= 1 && k >= 1 && a && b && c, kErrArg, "bad gemm arguments");
+    GemmBatch gb;
+    gb.add(0, ta != 0, tb != 0, m, n, k, a, lda, 0, b, ldb, 0, c, ldc, 0);
+    gb.run();
+  });
+}
+
 int t2s2_residual(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* x,
                   const t2s2_train* rhs, double tol, double* out) {
   return guarded(ctx, [&] {

@@ -33,151 +33,105 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// One TM x TN output tile (tile coordinates bx, by of batch entry bz).
-template <int TM, int TN, int TK, bool TC>
-__device__ __forceinline__ void gemm_tile(bool ta, bool tb, int M, int N, int K, double alpha,
-                                          const double* __restrict__ A, int lda, long long sA,
-                                          const double* __restrict__ B, int ldb, long long sB,
-                                          double beta, double* C, int ldc, long long sC, int bx,
-                                          int by, int bz) {
-  constexpr int PA = TM * TK / 256, PB = TK * TN / 256, RM = TM / 16, RN = TN / 16;
+// Row offset of a 2-level row index: i -> (i / d) * hi + (i % d) * lo.
+__device__ __forceinline__ long long row_off(int i, int d, long long hi, long long lo) {
+  const int q = i / d;
+  return q * hi + (long long)(i - q * d) * lo;
+}
+
+// One TM x TN output tile (tile coordinates bx, by of batch entry bz) of a
+// general GEMM: A(i,k) = A[row(i) + k*ak], B(k,j) = B[k*bk + j*bj],
+// C(i,j) = C[crow(i) + j*cj] (row() two-level, see GemmProb).  Operand
+// tiles are fetched with consecutive threads on the contiguous index, into
+// registers one K-tile ahead of the DMMA on shared memory.
+template <int TM, int TN, int TK>
+__device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz) {
+  constexpr int PA = TM * TK / 256, PB = TK * TN / 256;
   __shared__ double As[TK][TM + 1];
   __shared__ double Bs[TK][TN + 1];
-  A += bz * sA;
-  B += bz * sB;
-  C += bz * sC;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const double* A = g.A + bz * g.sA;
+  const double* B = g.B + bz * g.sB;
+  double* C = g.C + bz * g.sC;
+  const int M = g.M, N = g.N, K = g.K;
   const int row0 = by * TM, col0 = bx * TN;
+  const int tid = threadIdx.x;
+  const bool a_ifast = g.alo == 1;  // rows contiguous: threads walk i
+  const bool b_jfast = g.bj == 1;
+  // loop-invariant per-thread row offsets
+  long long aoff[PA];
+  int ai[PA], akk[PA];
+#pragma unroll
+  for (int t = 0; t < PA; ++t) {
+    const int e = tid + t * 256;
+    ai[t] = a_ifast ? e % TM : e / TK;
+    akk[t] = a_ifast ? e / TM : e % TK;
+    const int gi = row0 + ai[t];
+    aoff[t] = gi < M ? row_off(gi, g.ad, g.ahi, g.alo) : 0;
+  }
+  int bkk[PB], bjj[PB];
+#pragma unroll
+  for (int t = 0; t < PB; ++t) {
+    const int e = tid + t * 256;
+    bjj[t] = b_jfast ? e % TN : e / TK;
+    bkk[t] = b_jfast ? e / TN : e % TK;
+  }
   double ra[PA], rb[PB];
   auto fetch = [&](int k0) {
 #pragma unroll
     for (int t = 0; t < PA; ++t) {
-      const int e = threadIdx.x + t * 256;
-      int ar, ak;
-      if (ta) {  // A^T: contiguous along rows of op(A) -> consecutive threads walk i
-        ar = e % TM;
-        ak = e / TM;
-      } else {
-        ar = e / TK;
-        ak = e % TK;
-      }
-      const int gi = row0 + ar, gk = k0 + ak;
-      ra[t] = (gi < M && gk < K) ? (ta ? A[(long long)gk * lda + gi] : A[(long long)gi * lda + gk])
-                                 : 0.0;
+      const int gi = row0 + ai[t], gk = k0 + akk[t];
+      ra[t] = (gi < M && gk < K) ? A[aoff[t] + (long long)gk * g.ak] : 0.0;
     }
 #pragma unroll
     for (int t = 0; t < PB; ++t) {
-      const int e = threadIdx.x + t * 256;
-      int bk, bc;
-      if (tb) {
-        bk = e % TK;
-        bc = e / TK;
-      } else {
-        bk = e / TN;
-        bc = e % TN;
-      }
-      const int gk = k0 + bk, gj = col0 + bc;
-      rb[t] = (gk < K && gj < N) ? (tb ? B[(long long)gj * ldb + gk] : B[(long long)gk * ldb + gj])
-                                 : 0.0;
+      const int gk = k0 + bkk[t], gj = col0 + bjj[t];
+      rb[t] = (gk < K && gj < N) ? B[(long long)gk * g.bk + (long long)gj * g.bj] : 0.0;
     }
   };
-  // FFMA path: 16x16 threads, RM x RN outputs each.  TC path: 8 warps on a
-  // 4 x 2 grid of (TM/4) x (TN/2) warp tiles of 8x8 DMMA blocks.
+  // 8 warps on a 4 x 2 grid of (TM/4) x (TN/2) warp tiles of 8x8 DMMA blocks
   constexpr int WM = TM / 4, WN = TN / 2, MB = WM / 8, NB = WN / 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * WN;
-  double acc[RM][RN] = {};
   double tc[MB][NB][2] = {};
   fetch(0);
   for (int k0 = 0; k0 < K; k0 += TK) {
 #pragma unroll
-    for (int t = 0; t < PA; ++t) {
-      const int e = threadIdx.x + t * 256;
-      if (ta)
-        As[e / TM][e % TM] = ra[t];
-      else
-        As[e % TK][e / TK] = ra[t];
-    }
+    for (int t = 0; t < PA; ++t) As[akk[t]][ai[t]] = ra[t];
 #pragma unroll
-    for (int t = 0; t < PB; ++t) {
-      const int e = threadIdx.x + t * 256;
-      if (tb)
-        Bs[e % TK][e / TK] = rb[t];
-      else
-        Bs[e / TN][e % TN] = rb[t];
-    }
+    for (int t = 0; t < PB; ++t) Bs[bkk[t]][bjj[t]] = rb[t];
     __syncthreads();
     if (k0 + TK < K) fetch(k0 + TK);
-    if (TC) {
 #pragma unroll
-      for (int kk = 0; kk < TK; kk += 4) {
-        const int kr = kk + (lane & 3);
-        double af[MB], bf[NB];
+    for (int kk = 0; kk < TK; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[MB], bf[NB];
 #pragma unroll
-        for (int i = 0; i < MB; ++i) af[i] = As[kr][wm0 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < MB; ++i) af[i] = As[kr][wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
-        for (int j = 0; j < NB; ++j) bf[j] = Bs[kr][wn0 + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NB; ++j) bf[j] = Bs[kr][wn0 + j * 8 + (lane >> 2)];
 #pragma unroll
-        for (int i = 0; i < MB; ++i)
+      for (int i = 0; i < MB; ++i)
 #pragma unroll
-          for (int j = 0; j < NB; ++j) dmma_8x8x4(tc[i][j][0], tc[i][j][1], af[i], bf[j]);
-      }
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < TK; ++kk) {
-        double a[RM], b[RN];
-#pragma unroll
-        for (int i = 0; i < RM; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < RN; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < RM; ++i)
-#pragma unroll
-          for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-      }
+        for (int j = 0; j < NB; ++j) dmma_8x8x4(tc[i][j][0], tc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
-  if (TC) {
+  const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
-    for (int i = 0; i < MB; ++i) {
-      const int gi = row0 + wm0 + i * 8 + (lane >> 2);
-      if (gi >= M) continue;
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gj = col0 + wn0 + j * 8 + (lane & 3) * 2 + h;
-          if (gj >= N) continue;
-          double* c = C + (long long)gi * ldc + gj;
-          *c = beta == 0.0 ? alpha * tc[i][j][h] : alpha * tc[i][j][h] + beta * (*c);
-        }
-    }
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < RM; ++i) {
-    const int gi = row0 + ty + 16 * i;
+  for (int i = 0; i < MB; ++i) {
+    const int gi = row0 + wm0 + i * 8 + (lane >> 2);
     if (gi >= M) continue;
+    const long long co = row_off(gi, g.cd, g.chi, g.clo);
 #pragma unroll
-    for (int j = 0; j < RN; ++j) {
-      const int gj = col0 + tx + 16 * j;
-      if (gj >= N) continue;
-      double* c = C + (long long)gi * ldc + gj;
-      *c = beta == 0.0 ? alpha * acc[i][j] : alpha * acc[i][j] + beta * (*c);
-    }
+    for (int j = 0; j < NB; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = col0 + wn0 + j * 8 + (lane & 3) * 2 + h;
+        if (gj >= N) continue;
+        double* c = C + co + (long long)gj * g.cj;
+        *c = beta == 0.0 ? alpha * tc[i][j][h] : alpha * tc[i][j][h] + beta * (*c);
+      }
   }
-}
-
-template <int TM, int TN, int TK, bool TC>
-__global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int N, int K,
-                                                   double alpha, const double* __restrict__ A,
-                                                   int lda, long long sA,
-                                                   const double* __restrict__ B, int ldb,
-                                                   long long sB, double beta, double* C, int ldc,
-                                                   long long sC) {
-  gemm_tile<TM, TN, TK, TC>(ta, tb, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC,
-                            blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
 // A GEMM program: stages of independent strided-batched GEMMs, one
@@ -185,8 +139,11 @@ __global__ void __launch_bounds__(256) gemm_kernel(bool ta, bool tb, int M, int 
 // contractions (the interface recurrences of a move, the local right-hand
 // sides, the operator applications) run as one kernel instead of one launch
 // per GEMM.
+constexpr int kReduceTile = 4096;
+
 __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
   cg::grid_group grid = cg::this_grid();
+  if (prog.guard && *prog.guard == 0) return;  // uniform over the grid: flag set by an earlier kernel
   for (int s = 0; s < prog.nstage; ++s) {
     const int q0 = prog.stage_first[s], q1 = prog.stage_first[s + 1];
     int total = 0;
@@ -198,10 +155,26 @@ __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant
         ++q;
       }
       const GemmProb& g = prog.p[q];
-      const int tn = (g.N + 31) / 32, tm = (g.M + 31) / 32;
-      const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
-      gemm_tile<32, 32, 32, true>(g.ta, g.tb, g.M, g.N, g.K, g.alpha, g.A, g.lda, g.sA, g.B, g.ldb,
-                                  g.sB, g.beta, g.C, g.ldc, g.sC, rem % tn, rem / tn, bz);
+      if (g.kind == 1) {
+        const long long mn = (long long)g.M * g.N;
+        const long long e0 = (long long)tt * kReduceTile;
+        for (long long e = e0 + threadIdx.x; e < e0 + kReduceTile && e < mn; e += blockDim.x) {
+          double acc = 0.0;
+          for (int j = 0; j < g.batch; ++j) acc += g.A[j * mn + e];
+          const int i = (int)(e / g.N), c = (int)(e - (long long)i * g.N);
+          double* cp = g.C + row_off(i, g.cd, g.chi, g.clo) + (long long)c * g.cj;
+          *cp = g.beta == 0.0 ? g.alpha * acc : g.alpha * acc + g.beta * *cp;
+        }
+        __syncthreads();
+      } else if (g.big) {
+        const int tn = (g.N + 63) / 64, tm = (g.M + 63) / 64;
+        const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
+        gemm_tile<64, 64, 16>(g, rem % tn, rem / tn, bz);
+      } else {
+        const int tn = (g.N + 31) / 32, tm = (g.M + 31) / 32;
+        const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
+        gemm_tile<32, 32, 32>(g, rem % tn, rem / tn, bz);
+      }
     }
     if (s + 1 < prog.nstage) grid.sync();
   }
@@ -321,20 +294,9 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
       }
     return;
   }
-  const bool big = (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch >= 74;
-  {
-    LaunchScope ls("gemm", 2.0*M*N*(double)K*batch, 8.0*batch*((double)M*K+(double)K*N+2.0*M*N));
-    if (big) {
-      dim3 grid(ceil_div(N, 64), ceil_div(M, 64), batch);
-      gemm_kernel<64, 64, 16, true><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA,
-                                                                B, ldb, sB, beta, C, ldc, sC);
-    } else {
-      dim3 grid(ceil_div(N, 32), ceil_div(M, 32), batch);
-      gemm_kernel<32, 32, 32, true><<<grid, 256, 0, stream()>>>(ta, tb, M, N, K, alpha, A, lda, sA,
-                                                                B, ldb, sB, beta, C, ldc, sC);
-    }
-  }
-  T2S2_CHECK_LAUNCH();
+  GemmBatch gb;
+  gb.add(0, ta, tb, M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, alpha, beta);
+  gb.run();
 }
 
 double* GemmBatch::temp(std::vector<int> shape) {
@@ -345,29 +307,90 @@ double* GemmBatch::temp(std::vector<int> shape) {
 void GemmBatch::add(int stage, bool ta, bool tb, int M, int N, int K, const double* A, int lda,
                     long long sA, const double* B, int ldb, long long sB, double* C, int ldc,
                     long long sC, int batch, double alpha, double beta) {
+  if (batch > 1 && sA == 0) {
+    // shared left factor: the batch folds into the rows of one GEMM,
+    // C_b^T = B_b^T A^T stacked over b (two-level row index (b, n))
+    GemmOperand a2{B, N, sB, tb ? (long long)ldb : 1, tb ? 1 : (long long)ldb, 0};
+    GemmOperand c2{C, N, sC, 1, ldc, 0};
+    add_general(stage, batch * N, M, K, a2, A, ta ? (long long)lda : 1, ta ? 1 : (long long)lda, 0,
+                c2, 1, alpha, beta);
+    return;
+  }
+  GemmOperand a{A, 1 << 30, 0, ta ? 1 : lda, ta ? lda : 1, sA};
+  GemmOperand c{C, 1 << 30, 0, ldc, 1, sC};
+  add_general(stage, M, N, K, a, B, tb ? 1 : ldb, tb ? ldb : 1, sB, c, batch, alpha, beta);
+}
+
+void GemmBatch::add_general(int stage, int M, int N, int K, const GemmOperand& a, const double* B,
+                            long long bk, long long bj, long long sB, const GemmOperand& c,
+                            int batch, double alpha, double beta) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   T2S2_REQUIRE(K > 0, kErrShape, "GemmBatch: empty contraction");
   GemmProb g{};
-  g.A = A;
+  g.A = a.p;
+  g.ad = a.d;
+  g.ahi = a.hi;
+  g.alo = a.lo;
+  g.ak = a.k;
+  g.sA = a.batch;
   g.B = B;
-  g.C = C;
-  g.sA = sA;
+  g.bk = bk;
+  g.bj = bj;
   g.sB = sB;
-  g.sC = sC;
+  g.C = const_cast<double*>(c.p);
+  g.cd = c.d;
+  g.chi = c.hi;
+  g.clo = c.lo;
+  g.cj = c.k;
+  g.sC = c.batch;
   g.M = M;
   g.N = N;
   g.K = K;
-  g.lda = lda;
-  g.ldb = ldb;
-  g.ldc = ldc;
   g.batch = batch;
-  g.ta = ta;
-  g.tb = tb;
   g.alpha = alpha;
   g.beta = beta;
-  g.tiles = ceil_div(M, 32) * ceil_div(N, 32) * batch;
-  items_.push_back({stage, g});
+  // 64x64 tiles once a problem fills the GPU with them (more reuse per L2 byte)
+  g.big = M >= 64 && N >= 64 && K >= 64 &&
+          (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch >= 148;
+  g.tiles = g.big ? ceil_div(M, 64) * ceil_div(N, 64) * batch
+                  : ceil_div(M, 32) * ceil_div(N, 32) * batch;
   flops_ += 2.0 * M * N * (double)K * batch;
+  // split-K for long contractions with too few output tiles to fill the GPU:
+  // partial products at stage 2s, their deterministic sum at stage 2s+1
+  constexpr int kFill = 592;  // two waves of two CTAs per SM
+  if (batch == 1 && K >= 256 && g.tiles < kFill / 2) {
+    int S = K / 128;
+    const int want = ceil_div(kFill, g.tiles);
+    if (S > want) S = want;
+    if (S >= 2) {
+      const int chunk = ceil_div(K, S);
+      S = ceil_div(K, chunk);
+      double* P = temp({S, M, N});
+      for (int j = 0; j < S; ++j) {
+        const int k0 = j * chunk, kj = K - k0 < chunk ? K - k0 : chunk;
+        GemmProb h = g;
+        h.K = kj;
+        h.A = a.p + (long long)k0 * a.k;
+        h.B = B + (long long)k0 * bk;
+        h.C = P + (long long)j * M * N;
+        h.cd = 1 << 30;
+        h.chi = 0;
+        h.clo = N;
+        h.cj = 1;
+        h.alpha = 1.0;
+        h.beta = 0.0;
+        items_.push_back({2 * stage, h});
+      }
+      GemmProb r = g;
+      r.kind = 1;
+      r.A = P;
+      r.batch = S;
+      r.tiles = (int)(((long long)M * N + kReduceTile - 1) / kReduceTile);
+      items_.push_back({2 * stage + 1, r});
+      return;
+    }
+  }
+  items_.push_back({2 * stage, g});
 }
 
 void GemmBatch::run() {
@@ -378,6 +401,7 @@ void GemmBatch::run() {
   size_t i = 0;
   while (i < items_.size()) {
     GemmProgram prog{};
+    prog.guard = guard_;
     int last_stage = -1, max_tiles = 0, stage_tiles = 0;
     while (i < items_.size() && prog.nprob < kProgMaxProb) {
       const Item& it = items_[i];
@@ -400,7 +424,12 @@ void GemmBatch::run() {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    int grid = max_tiles < nsm ? max_tiles : nsm;
+    static int occ = 0;
+    if (occ == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_program_kernel, 256, 0);
+      if (occ < 1) occ = 1;
+    }
+    int grid = max_tiles < nsm * occ ? max_tiles : nsm * occ;
     if (sm_budget() > 0 && grid > sm_budget()) grid = sm_budget();
     if (grid < 1) grid = 1;
     {

@@ -19,21 +19,37 @@ void gemm_batched(bool ta, bool tb, int M, int N, int K, double alpha, const dou
 // A program of strided-batched GEMMs in stages: the problems of a stage are
 // independent, stage s+1 may read what stage s wrote.  One (cooperative)
 // launch per program with a grid barrier between stages.
-constexpr int kProgMaxProb = 24;
+constexpr int kProgMaxProb = 20;
 constexpr int kProgMaxStage = 24;
 struct GemmProb {
+  // A(i,k) = A[(i / ad) * ahi + (i % ad) * alo + k * ak]: a two-level row
+  // index folds a batch (or a split row index) into one large GEMM;
+  // B(k,j) = B[k * bk + j * bj]; C(i,j) = C[(i / cd) * chi + (i % cd) * clo + j * cj].
   const double* A;
   const double* B;
   double* C;
-  long long sA, sB, sC;
-  int M, N, K, lda, ldb, ldc, batch, tiles;
-  int ta, tb;
+  long long sA, sB, sC;  // strides of the explicit batch index
+  long long ahi, alo, ak, bk, bj, chi, clo, cj;
+  int ad, cd;
+  int M, N, K, batch, tiles;
+  int big;   // 64x64x16 tiles, else 32x32x32
+  int kind;  // 0 GEMM; 1 split-K reduction: C = alpha sum_j A[j] + beta C (A: batch x M x N)
   double alpha, beta;
 };
+
 struct GemmProgram {
+  const int* guard;  // device flag: the program does nothing while it reads 0 (null: run)
   int nprob, nstage;
   int stage_first[kProgMaxStage + 1];
   GemmProb p[kProgMaxProb];
+};
+
+// Operand with a two-level row index (see GemmProb): element (i, k) at
+// p + (i / d) * hi + (i % d) * lo + k * k_stride (+ batch stride).
+struct GemmOperand {
+  const double* p;
+  int d;
+  long long hi, lo, k, batch;
 };
 
 class GemmBatch {
@@ -43,9 +59,15 @@ class GemmBatch {
   void add(int stage, bool ta, bool tb, int M, int N, int K, const double* A, int lda, long long sA,
            const double* B, int ldb, long long sB, double* C, int ldc, long long sC, int batch = 1,
            double alpha = 1.0, double beta = 0.0);
+  // C = alpha op(A) B + beta C with general operand addressing
+  void add_general(int stage, int M, int N, int K, const GemmOperand& a, const double* B,
+                   long long bk, long long bj, long long sB, const GemmOperand& c, int batch = 1,
+                   double alpha = 1.0, double beta = 0.0);
   void run();
+  void set_guard(const int* g) { guard_ = g; }
 
  private:
+  const int* guard_ = nullptr;
   struct Item {
     int stage;
     GemmProb g;

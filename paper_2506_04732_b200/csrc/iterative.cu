@@ -5,6 +5,10 @@
 #include "blas.h"
 #include "iterative.h"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
 namespace t2s2 {
 namespace {
 
@@ -26,6 +30,7 @@ struct CgState {
   int active;
 };
 
+constexpr int kCgMaxCtas = 148;
 __device__ double cta_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -157,37 +162,79 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// scipy cg, top of iteration: convergence check, z = M r, rho, p update.
-__global__ void __launch_bounds__(kThreads)
-    cg_pre_kernel(CgState* st, const double* r, const double* diag, double* z, double* p, int n,
-                  double atol, int iteration) {
-  __shared__ double red[33];
-  if (!st->active) return;
-  const double rn = sqrt(cta_dot(r, r, n, red));
-  if (rn < atol) {
-    if (threadIdx.x == 0) st->active = 0;
-    return;
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) z[i] = r[i] / diag[i];
+// scipy cg (Jacobi-preconditioned), split around the matvec q = A p into two
+// cooperative kernels over G CTAs.  Reductions are deterministic: per-CTA
+// partials, one grid barrier, every CTA sums the G partials in order.
+__device__ __forceinline__ double block_reduce(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
-  const double rho = cta_dot(r, z, n, red);
-  const double beta = iteration > 0 ? rho / st->rho_prev : 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    p[i] = iteration > 0 ? fma(p[i], beta, z[i]) : z[i];
-  if (threadIdx.x == 0) st->rho_cur = rho;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;
 }
 
+// top of iteration: ||r|| < atol -> stop; rho = r.(r/diag); p = r/diag + beta p
 __global__ void __launch_bounds__(kThreads)
-    cg_post_kernel(CgState* st, const double* p, const double* q, double* x, double* r, int n) {
-  __shared__ double red[33];
+    cg_pre_kernel(CgState* st, const double* r, const double* diag, double* p, int n, double atol,
+                  int iteration, double* part) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
   if (!st->active) return;
-  const double pq = cta_dot(p, q, n, red);
-  const double alpha = st->rho_cur / pq;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  const int G = gridDim.x, gt = blockIdx.x * blockDim.x + threadIdx.x, gs = G * blockDim.x;
+  double rr = 0.0, rz = 0.0;
+  for (int i = gt; i < n; i += gs) {
+    const double ri = r[i];
+    rr = fma(ri, ri, rr);
+    rz = fma(ri, ri / diag[i], rz);
+  }
+  rr = block_reduce(rr, red);
+  rz = block_reduce(rz, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = rr;
+    part[G + blockIdx.x] = rz;
+  }
+  grid.sync();
+  double srr = 0.0, rho = 0.0;
+  for (int c = 0; c < G; ++c) {
+    srr += __ldcg(part + c);
+    rho += __ldcg(part + G + c);
+  }
+  if (sqrt(srr) < atol) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
+    return;
+  }
+  const double beta = iteration > 0 ? rho / st->rho_prev : 0.0;
+  for (int i = gt; i < n; i += gs) {
+    const double z = r[i] / diag[i];
+    p[i] = iteration > 0 ? fma(p[i], beta, z) : z;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_cur = rho;
+}
+
+// after q = A p: alpha = rho / p.q; x += alpha p; r -= alpha q
+__global__ void __launch_bounds__(kThreads)
+    cg_post_kernel(CgState* st, const double* p, const double* q, double* x, double* r, int n,
+                   double* part) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
+  if (!st->active) return;
+  const int G = gridDim.x, gt = blockIdx.x * blockDim.x + threadIdx.x, gs = G * blockDim.x;
+  double pq = 0.0;
+  for (int i = gt; i < n; i += gs) pq = fma(p[i], q[i], pq);
+  pq = block_reduce(pq, red);
+  if (threadIdx.x == 0) part[2 * G + blockIdx.x] = pq;
+  grid.sync();
+  double spq = 0.0;
+  for (int c = 0; c < G; ++c) spq += __ldcg(part + 2 * G + c);
+  const double alpha = st->rho_cur / spq;
+  for (int i = gt; i < n; i += gs) {
     x[i] = fma(alpha, p[i], x[i]);
     r[i] = fma(-alpha, q[i], r[i]);
   }
-  if (threadIdx.x == 0) st->rho_prev = st->rho_cur;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_prev = st->rho_cur;
 }
 
 template <class T>
@@ -216,7 +263,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   double* r = allocator().alloc(n);
   GmState* st = reinterpret_cast<GmState*>(allocator().alloc(sizeof(GmState) / sizeof(double) + 1));
   auto residual = [&]() {  // r = b - A x, returns ||r||
-    A(x, r);
+    A(x, r, nullptr);
     daxpby(1.0, b, -1.0, r, n);
     return dnrm2(r, n);
   };
@@ -238,7 +285,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
     T2S2_CHECK_LAUNCH();
     for (int col = 0; col < restart; ++col) {
       if (col > 0 && col % 8 == 0 && !read_flag(&st->active)) break;
-      A(V + (size_t)col * n, V + (size_t)(col + 1) * n);
+      A(V + (size_t)col * n, V + (size_t)(col + 1) * n, &st->active);  // skipped once converged
       {
         LaunchScope ls("gmres", 4.0*n*(col+2), 16.0*n*(col+2));
         gm_arnoldi_kernel<<<1, kThreads, 0, stream()>>>(st, V, n, col, restart);
@@ -277,33 +324,43 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
     return 0;
   }
   double* r = allocator().alloc(n);
-  double* z = allocator().alloc(n);
   double* p = allocator().alloc(n);
   double* q = allocator().alloc(n);
+  double* part = allocator().alloc(3 * kCgMaxCtas);
   CgState* st = reinterpret_cast<CgState*>(allocator().alloc(sizeof(CgState) / sizeof(double) + 1));
-  A(x, r);
+  A(x, r, nullptr);
   daxpby(1.0, b, -1.0, r, n);
   CgState init{0.0, 0.0, 1};
   T2S2_CUDA(cudaMemcpyAsync(st, &init, sizeof(CgState), cudaMemcpyHostToDevice, stream()));
+  int G = (n + 2047) / 2048;
+  if (G > kCgMaxCtas) G = kCgMaxCtas;
+  if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
+  if (G < 1) G = 1;
   int it = 0;
   for (; it < maxiter; ++it) {
     if (it > 0 && it % 10 == 0 && !read_flag(&st->active)) break;
     {
-      LaunchScope ls("cg", 6.0*n, 40.0*n);
-      cg_pre_kernel<<<1, kThreads, 0, stream()>>>(st, r, diag, z, p, n, atol, it);
+      LaunchScope ls("cg", 6.0 * n, 40.0 * n);
+      int itv = it;
+      double at = atol;
+      void* params[] = {&st, &r, &diag, &p, &n, &at, &itv, &part};
+      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_pre_kernel, dim3(G), dim3(kThreads), params,
+                                            0, stream()));
     }
-    A(p, q);
+    A(p, q, &st->active);  // skipped on the device once converged
     {
-      LaunchScope ls("cg", 6.0*n, 48.0*n);
-      cg_post_kernel<<<1, kThreads, 0, stream()>>>(st, p, q, x, r, n);
+      LaunchScope ls("cg", 6.0 * n, 48.0 * n);
+      void* params[] = {&st, &p, &q, &x, &r, &n, &part};
+      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_post_kernel, dim3(G), dim3(kThreads), params,
+                                            0, stream()));
     }
     T2S2_CHECK_LAUNCH();
   }
   T2S2_CUDA(cudaStreamSynchronize(stream()));  // init lives on the host stack
   allocator().release(r);
-  allocator().release(z);
   allocator().release(p);
   allocator().release(q);
+  allocator().release(part);
   allocator().release(reinterpret_cast<double*>(st));
   return it;
 }

@@ -15,7 +15,10 @@
 
 namespace t2s2 {
 
-using MatVec = std::function<void(const double* in, double* out)>;
+// out = A in.  guard (device int, may be null): when it reads 0 on the
+// device the application is skipped (a Krylov loop that converged between
+// two host polls does not pay for its trailing matvecs).
+using MatVec = std::function<void(const double* in, double* out, const int* guard)>;
 
 // x (device, length n) is the initial guess and receives the result.
 // rtol relative to ||b|| (scipy's atol = rtol * ||b||).  Returns inner
