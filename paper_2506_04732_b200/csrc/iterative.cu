@@ -214,10 +214,12 @@ __global__ void __launch_bounds__(kThreads)
   if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_cur = rho;
 }
 
-// after q = A p: alpha = rho / p.q; x += alpha p; r -= alpha q
+// After q = A p: alpha = rho / p.q, x += alpha p, r -= alpha q — fused
+// with the next iteration's top (||r|| < atol -> stop, rho, p update): one
+// launch per iteration besides the matvec.
 __global__ void __launch_bounds__(kThreads)
-    cg_post_kernel(CgState* st, const double* p, const double* q, double* x, double* r, int n,
-                   double* part) {
+    cg_step_kernel(CgState* st, const double* q, double* x, double* r, const double* diag,
+                   double* p, int n, double atol, int iteration, double* part) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
   if (!st->active) return;
@@ -229,12 +231,40 @@ __global__ void __launch_bounds__(kThreads)
   grid.sync();
   double spq = 0.0;
   for (int c = 0; c < G; ++c) spq += __ldcg(part + 2 * G + c);
-  const double alpha = st->rho_cur / spq;
+  const double rho_cur = st->rho_cur;
+  const double alpha = rho_cur / spq;
+  double rr = 0.0, rz = 0.0;
   for (int i = gt; i < n; i += gs) {
     x[i] = fma(alpha, p[i], x[i]);
-    r[i] = fma(-alpha, q[i], r[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    rr = fma(ri, ri, rr);
+    rz = fma(ri, ri / diag[i], rz);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_prev = st->rho_cur;
+  rr = block_reduce(rr, red);
+  rz = block_reduce(rz, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = rr;
+    part[G + blockIdx.x] = rz;
+  }
+  grid.sync();
+  // next iteration's top: convergence check, rho, p update
+  double srr = 0.0, rho = 0.0;
+  for (int c = 0; c < G; ++c) {
+    srr += __ldcg(part + c);
+    rho += __ldcg(part + G + c);
+  }
+  if (sqrt(srr) < atol) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
+    return;
+  }
+  const double beta = rho / rho_cur;  // rho_prev of the next iteration = this rho_cur
+  for (int i = gt; i < n; i += gs) p[i] = fma(p[i], beta, r[i] / diag[i]);
+  grid.sync();  // every CTA has read rho_cur
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rho_prev = rho_cur;
+    st->rho_cur = rho;
+  }
 }
 
 template <class T>
@@ -337,21 +367,23 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
   if (G < 1) G = 1;
   int it = 0;
+  double at = atol;
+  {
+    LaunchScope ls("cg", 6.0 * n, 40.0 * n);
+    int itv = 0;
+    void* params[] = {&st, &r, &diag, &p, &n, &at, &itv, &part};
+    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_pre_kernel, dim3(G), dim3(kThreads), params,
+                                          0, stream()));
+  }
   for (; it < maxiter; ++it) {
     if (it > 0 && it % 10 == 0 && !read_flag(&st->active)) break;
-    {
-      LaunchScope ls("cg", 6.0 * n, 40.0 * n);
-      int itv = it;
-      double at = atol;
-      void* params[] = {&st, &r, &diag, &p, &n, &at, &itv, &part};
-      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_pre_kernel, dim3(G), dim3(kThreads), params,
-                                            0, stream()));
-    }
     A(p, q, &st->active);  // skipped on the device once converged
     {
-      LaunchScope ls("cg", 6.0 * n, 48.0 * n);
-      void* params[] = {&st, &p, &q, &x, &r, &n, &part};
-      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_post_kernel, dim3(G), dim3(kThreads), params,
+      // this iteration's update and the next one's top (convergence, p)
+      LaunchScope ls("cg", 12.0 * n, 88.0 * n);
+      int itv = it;
+      void* params[] = {&st, &q, &x, &r, &diag, &p, &n, &at, &itv, &part};
+      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_step_kernel, dim3(G), dim3(kThreads), params,
                                             0, stream()));
     }
     T2S2_CHECK_LAUNCH();
