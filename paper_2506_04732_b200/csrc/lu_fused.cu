@@ -920,13 +920,10 @@ __device__ void np_trsm_rows(const NpArgs& a, int k0, int kb, int r, int m, doub
 #pragma unroll
     for (int jj = 0; jj < kNb; ++jj) {
       if (jj < kb) {
-        double v0 = R[jj * 65 + tid], v1 = 0.0;
+        double v[4] = {R[jj * 65 + tid], 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < jj; q += 2) {
-          v0 = fma(-l[q], U[jj * 33 + q], v0);
-          if (q + 1 < jj) v1 = fma(-l[q + 1], U[jj * 33 + q + 1], v1);
-        }
-        l[jj] = (v0 + v1) * rd[jj];
+        for (int q = 0; q < jj; ++q) v[q & 3] = fma(-l[q], U[jj * 33 + q], v[q & 3]);
+        l[jj] = ((v[0] + v[1]) + (v[2] + v[3])) * rd[jj];
         if (!(fabs(l[jj]) <= 1.0)) bad = true;
       }
     }
@@ -955,13 +952,10 @@ __device__ void np_trsm_cols(const NpArgs& a, int k0, int kb, int c, int n, doub
 #pragma unroll
     for (int i = 0; i < kNb; ++i) {
       if (i < kb) {
-        double v0 = u[i], v1 = 0.0;
+        double v[4] = {u[i], 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < i; q += 2) {
-          v0 = fma(-L[q * 33 + i], u[q], v0);
-          if (q + 1 < i) v1 = fma(-L[(q + 1) * 33 + i], u[q + 1], v1);
-        }
-        u[i] = v0 + v1;
+        for (int q = 0; q < i; ++q) v[q & 3] = fma(-L[q * 33 + i], u[q], v[q & 3]);
+        u[i] = (v[0] + v[1]) + (v[2] + v[3]);
       }
     }
 #pragma unroll

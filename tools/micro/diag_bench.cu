@@ -90,6 +90,51 @@ __global__ void diag_smem8(double* A, int reps, long long* cyc) {
   if (lane == 0) *cyc = (t1 - t0) / reps;
 }
 
+// V3: 256 threads, ping-pong buffers, one barrier per column (as np_diag)
+__global__ void __launch_bounds__(256, 1) diag_pp(double* A, int reps, long long* cyc) {
+  __shared__ double D0[33 * 32], D1[33 * 32], rinv[33];
+  const int tid = threadIdx.x;
+  long long t0 = clock64();
+  for (int rr = 0; rr < reps; ++rr) {
+    for (int e = tid; e < 1024; e += 256) {
+      const int c = e >> 5, i = e & 31;
+      D0[c * 33 + i] = A[c * 32 + i] + (i == c ? 40.0 : 0.0);
+    }
+    __syncthreads();
+    if (tid == 0) rinv[0] = 1.0 / D0[0];
+    __syncthreads();
+    const int j = tid & 31, i0 = tid >> 5;
+    double* Dc = D0;
+    double* Dn = D1;
+    for (int s = 0; s < 32; ++s) {
+      const double ri = rinv[s];
+      const double us = Dc[j * 33 + s];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + 8 * q;
+        const double x = Dc[j * 33 + i];
+        double v = x;
+        if (i > s) {
+          const double l = Dc[s * 33 + i] * ri;
+          if (j > s) v = fma(-l, us, x);
+          if (j == s) v = l;
+        }
+        Dn[j * 33 + i] = v;
+        if (i == s + 1 && j == s + 1) rinv[s + 1] = 1.0 / v;
+      }
+      __syncthreads();
+      double* t = Dc; Dc = Dn; Dn = t;
+    }
+    for (int e = tid; e < 1024; e += 256) {
+      const int c = e >> 5, i = e & 31;
+      A[c * 32 + i] = Dc[c * 33 + i] * 1e-3;
+    }
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (tid == 0) *cyc = (t1 - t0) / reps;
+}
+
 __global__ void div_lat(double* out, double x, int n, long long* cyc) {
   double v = x;
   long long t0 = clock64();
@@ -117,6 +162,7 @@ int main() {
   diag_kernel<2><<<1, 32>>>(A, 10, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("diag frcp  %lld cyc\n", h);
   diag_reg<<<1, 32>>>(A, 10, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("diag reg   %lld cyc\n", h);
   diag_smem8<<<1, 32>>>(A, 10, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("diag smem8 %lld cyc\n", h);
+  diag_pp<<<1, 256>>>(A, 10, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("diag pp256 %lld cyc\n", h);
   div_lat<<<1, 1>>>(o, 0.5, 1000, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("ddiv latency %lld cyc\n", h);
   fma_lat<<<1, 1>>>(o, 0.5, 1000, c); cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost); printf("dfma latency %lld cyc\n", h);
   return 0;
