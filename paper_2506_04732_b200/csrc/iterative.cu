@@ -23,6 +23,7 @@ struct GmState {
   int col_final;
   int active;
   int breakdown;
+  int restart;
 };
 
 struct CgState {
@@ -90,6 +91,8 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+__global__ void gm_set_restart(GmState* st, int restart) { st->restart = restart; }
+
 // Arnoldi step for column col (w = A v_col already in V[col+1]).
 __global__ void __launch_bounds__(kThreads)
     gm_arnoldi_kernel(GmState* st, double* V, int n, int col, int restart) {
@@ -137,6 +140,111 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Arnoldi step over G CTAs (cooperative): classical Gram-Schmidt applied
+// twice (CGS2, as orthogonal as scipy's modified Gram-Schmidt to working
+// precision) so the column costs three grid barriers instead of one CTA-wide
+// reduction per basis vector.  Dots: per-CTA partials (warp per basis
+// vector), every CTA sums them in the same order.
+__device__ void mc_dots(const double* V, const double* w, int n, int nk, int i0, int i1,
+                        double* part, int G) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < nk; k += nw) {
+    const double* v = k < nk - 1 ? V + (size_t)k * n : w;  // last: ||w||^2
+    double acc = 0.0;
+    for (int i = i0 + lane; i < i1; i += 32) acc = fma(v[i], w[i], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) part[(size_t)k * G + blockIdx.x] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    gm_arnoldi_mc_kernel(GmState* st, double* V, int n, int col, double* part) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double hs[kMaxRestart + 2], h2[kMaxRestart + 2];
+  if (!st->active) return;
+  const int G = gridDim.x;
+  const int chunk = (n + G - 1) / G, i0 = blockIdx.x * chunk;
+  const int i1 = i0 + chunk < n ? i0 + chunk : n;
+  double* w = V + (size_t)(col + 1) * n;
+  const int nk = col + 2;  // col+1 dots and ||w||^2
+  mc_dots(V, w, n, nk, i0, i1, part, G);
+  grid.sync();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < G; ++c) t += __ldcg(part + (size_t)k * G + c);
+    hs[k] = t;
+  }
+  __syncthreads();
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double x = w[i];
+    for (int k = 0; k <= col; ++k) x = fma(-hs[k], V[(size_t)k * n + i], x);
+    w[i] = x;
+  }
+  __syncthreads();
+  grid.sync();  // every CTA has read the first-pass partials
+  mc_dots(V, w, n, nk, i0, i1, part, G);
+  grid.sync();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < G; ++c) t += __ldcg(part + (size_t)k * G + c);
+    h2[k] = t;
+  }
+  __syncthreads();
+  double ww = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double x = w[i];
+    for (int k = 0; k <= col; ++k) x = fma(-h2[k], V[(size_t)k * n + i], x);
+    w[i] = x;
+    ww = fma(x, x, ww);
+  }
+  for (int o = 16; o > 0; o >>= 1) ww += __shfl_xor_sync(0xffffffffu, ww, o);
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = ww;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    part[(size_t)(kMaxRestart + 2) * G + blockIdx.x] = t;
+  }
+  grid.sync();
+  double sww = 0.0;
+  for (int c = 0; c < G; ++c) sww += __ldcg(part + (size_t)(kMaxRestart + 2) * G + c);
+  const double h0 = sqrt(hs[nk - 1]);
+  const double h1 = sqrt(sww);
+  const bool brk = h1 <= DBL_EPSILON * h0;
+  if (!brk) {
+    const double inv = 1.0 / h1;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) w[i] *= inv;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* hc = st->h[col];
+    for (int k = 0; k <= col; ++k) hc[k] = hs[k] + h2[k];
+    hc[col + 1] = brk ? 0.0 : h1;
+    if (brk) st->breakdown = 1;
+    for (int k = 0; k < col; ++k) {
+      const double c = st->gc[k], sn = st->gs[k];
+      const double n0 = hc[k], n1 = hc[k + 1];
+      hc[k] = c * n0 + sn * n1;
+      hc[k + 1] = -sn * n0 + c * n1;
+    }
+    double c, sn, mag;
+    lartg(hc[col], hc[col + 1], c, sn, mag);
+    st->gc[col] = c;
+    st->gs[col] = sn;
+    hc[col] = mag;
+    hc[col + 1] = 0.0;
+    const double t = -sn * st->S[col];
+    st->S[col] = c * st->S[col];
+    st->S[col + 1] = t;
+    st->presid = fabs(t);
+    if (st->presid <= st->ptol || brk || col == st->restart - 1) {
+      st->active = 0;
+      st->col_final = col;
+    }
+  }
+}
+
 // y = H^{-1} S (upper triangular, scipy's pseudo-solve), x += y V.
 __global__ void __launch_bounds__(kThreads)
     gm_update_kernel(GmState* st, const double* V, double* x, int n) {
@@ -155,7 +263,8 @@ __global__ void __launch_bounds__(kThreads)
     if (y[0] != 0.0) y[0] /= st->h[0][0];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // every CTA solved for y itself; the update is split over the grid
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double acc = x[i];
     for (int k = 0; k <= c; ++k) acc = fma(y[k], V[(size_t)k * n + i], acc);
     x[i] = acc;
@@ -292,6 +401,12 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   double* V = allocator().alloc((size_t)(restart + 1) * n);
   double* r = allocator().alloc(n);
   GmState* st = reinterpret_cast<GmState*>(allocator().alloc(sizeof(GmState) / sizeof(double) + 1));
+  // multi-CTA Arnoldi once each CTA gets >= 512 entries
+  int G = n / 512;
+  if (G > kCgMaxCtas) G = kCgMaxCtas;
+  if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
+  if (G < 1) G = 1;
+  double* part = allocator().alloc((size_t)(kMaxRestart + 3) * kCgMaxCtas);
   auto residual = [&]() {  // r = b - A x, returns ||r||
     A(x, r, nullptr);
     daxpby(1.0, b, -1.0, r, n);
@@ -302,6 +417,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   if (rnorm < atol) {
     allocator().release(V);
     allocator().release(r);
+    allocator().release(part);
     allocator().release(reinterpret_cast<double*>(st));
     return 0;
   }
@@ -311,20 +427,29 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
     {
       LaunchScope ls("gmres", 3.0*n, 24.0*n);
       gm_cycle_kernel<<<1, kThreads, 0, stream()>>>(st, r, V, n, ptol);
+      gm_set_restart<<<1, 1, 0, stream()>>>(st, restart);
     }
     T2S2_CHECK_LAUNCH();
     for (int col = 0; col < restart; ++col) {
       if (col > 0 && col % 8 == 0 && !read_flag(&st->active)) break;
       A(V + (size_t)col * n, V + (size_t)(col + 1) * n, &st->active);  // skipped once converged
       {
-        LaunchScope ls("gmres", 4.0*n*(col+2), 16.0*n*(col+2));
-        gm_arnoldi_kernel<<<1, kThreads, 0, stream()>>>(st, V, n, col, restart);
+        LaunchScope ls("gmres", 8.0 * n * (col + 2), 32.0 * n * (col + 2));
+        if (G > 1) {
+          int c = col;
+          int nn = n;
+          void* params[] = {&st, &V, &nn, &c, &part};
+          T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gm_arnoldi_mc_kernel, dim3(G),
+                                                dim3(kThreads), params, 0, stream()));
+        } else {
+          gm_arnoldi_kernel<<<1, kThreads, 0, stream()>>>(st, V, n, col, restart);
+        }
       }
       T2S2_CHECK_LAUNCH();
     }
     {
       LaunchScope ls("gmres", 2.0*n*restart, 8.0*n*restart);
-      gm_update_kernel<<<1, kThreads, 0, stream()>>>(st, V, x, n);
+      gm_update_kernel<<<G, kThreads, 0, stream()>>>(st, V, x, n);
     }
     T2S2_CHECK_LAUNCH();
     GmState h = read_state<GmState>(st);
@@ -341,6 +466,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   }
   allocator().release(V);
   allocator().release(r);
+  allocator().release(part);
   allocator().release(reinterpret_cast<double*>(st));
   return inner;
 }
