@@ -229,6 +229,52 @@ def test_dense_local_solve_without_interchanges(pk, n):
     assert np.linalg.norm(a @ x - b) <= 1e-13 * np.linalg.norm(a) * np.linalg.norm(x)
 
 
+def test_dense_local_solve_late_interchange(pk):
+    """Diagonally dominant except one column deep in the matrix: the no-pivot
+    kernel runs through several panels, meets a multiplier > 1, declines
+    (info -1) and the pivoting kernel solves the original matrix."""
+    from paper_2506_04732_b200 import _native
+
+    rng = np.random.default_rng(5)
+    n = 300
+    a = rng.standard_normal((n, n))
+    a += np.diag(np.abs(a).sum(0))
+    a[200, 200] *= 1e-6  # column 200 needs a row interchange
+    b = rng.standard_normal(n)
+    _native.stats_reset()
+    x = _native.dense_solve(a, b)
+    st = _native.stats_read()
+    assert st["lu_nopivot"]["launches"] == 1 and st["lu_fused"]["launches"] == 1
+    want = np.linalg.solve(a, b)
+    assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k", [
+    (0, 0, 37, 29, 13), (1, 0, 64, 65, 70), (0, 1, 130, 64, 132), (1, 1, 33, 40, 9),
+    (0, 0, 2112, 64, 1024),  # split-K with a reduce stage
+    (0, 1, 200, 48, 600),    # split-K, transposed B
+    (0, 0, 1024, 2112, 64),  # 64x64 tiles
+])
+def test_gemm_program_against_torch(pk, ta, tb, m, n, k):
+    """The GEMM-program kernel behind every contraction (DMMA tiles, operand
+    layouts, split-K) against a plain PyTorch fp64 matmul (cuBLAS)."""
+    import torch
+
+    from paper_2506_04732_b200 import _native
+
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
+    a = torch.randn((k, m) if ta else (m, k), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn((n, k) if tb else (k, n), dtype=torch.float64, device="cuda", generator=g)
+    c = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    _native.gemm_device(ta, tb, m, n, k, a.data_ptr(), a.shape[1], b.data_ptr(), b.shape[1],
+                        c.data_ptr(), n)
+    _native.synchronize()
+    want = (a.T if ta else a) @ (b.T if tb else b)
+    # fp64 rounding of a length-k dot product: well inside 1e-13 relative
+    assert torch.isfinite(c).all()
+    assert ((c - want).norm() / want.norm()).item() <= 1e-13
+
+
 def test_dense_local_solve_singular(pk):
     from paper_2506_04732_b200 import _native
 
