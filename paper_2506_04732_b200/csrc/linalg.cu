@@ -14,6 +14,13 @@ namespace t2s2 {
 namespace {
 
 constexpr int kQrThreads = 512;
+
+// Threads for a one-CTA factorisation whose column step keeps at most
+// `busy` warps working: fewer warps make each CTA barrier cheaper.
+inline int threads_for(int busy) {
+  int w = busy < 2 ? 2 : (busy > kQrThreads / 32 ? kQrThreads / 32 : busy);
+  return 32 * w;
+}
 constexpr size_t kSmemCap = 200 * 1024;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -335,7 +342,7 @@ void qr_r(int m, int n, const double* A, DTensor& R) {
   DTensor stacked({blocks * n, n});
   {
     LaunchScope ls("qr", 2.0 * m * (double)n * n, 8.0 * m * (double)n);
-    qr_r_kernel<<<blocks, kQrThreads, (size_t)chunk * n * sizeof(double), stream()>>>(
+    qr_r_kernel<<<blocks, threads_for(n), (size_t)chunk * n * sizeof(double), stream()>>>(
         m, n, chunk, A, stacked.p);
   }
   T2S2_CHECK_LAUNCH();
@@ -366,7 +373,7 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
                                        (int)kSmemCap));
         attr = true;
       }
-      qr_kernel<true><<<1, kQrThreads, need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+      qr_kernel<true><<<1, threads_for(n), need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
     } else {
       qr_kernel<false><<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
     }
@@ -396,7 +403,8 @@ void jacobi_svd(int p, int q, double* G, DTensor& U, DTensor& s, DTensor& Vt) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
         attr = true;
       }
-      jacobi_kernel<true><<<1, kQrThreads, need, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
+      jacobi_kernel<true><<<1, threads_for((q + 1) / 2), need, stream()>>>(p, q, G, V, perm, U.p,
+                                                                           s.p, Vt.p);
     } else {
       jacobi_kernel<false><<<1, kQrThreads, 0, stream()>>>(p, q, G, V, perm, U.p, s.p, Vt.p);
     }
