@@ -47,8 +47,8 @@ __device__ __forceinline__ long long row_off(int i, int d, long long hi, long lo
 template <int TM, int TN, int TK>
 __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz) {
   constexpr int PA = TM * TK / 256, PB = TK * TN / 256;
-  __shared__ double As[TK][TM + 1];
-  __shared__ double Bs[TK][TN + 1];
+  __shared__ double As[TK][TM + 4];  // +4: conflict-free DMMA fragment loads
+  __shared__ double Bs[TK][TN + 4];
   const double* A = g.A + bz * g.sA;
   const double* B = g.B + bz * g.sB;
   double* C = g.C + bz * g.sC;
@@ -359,10 +359,16 @@ void GemmBatch::add_general(int stage, int M, int N, int K, const GemmOperand& a
   // partial products at stage 2s, their deterministic sum at stage 2s+1
   constexpr int kFill = 592;  // two waves of two CTAs per SM
   if (batch == 1 && K >= 256 && g.tiles < kFill / 2) {
+    // chunks of >= 128; 64x64 tiles when the output allows (twice the
+    // operand reuse of 32x32)
+    const bool big = M >= 64 && N >= 64;
+    const int tiles = big ? ceil_div(M, 64) * ceil_div(N, 64) : g.tiles;
     int S = K / 128;
-    const int want = ceil_div(kFill, g.tiles);
+    const int want = ceil_div(kFill, tiles);
     if (S > want) S = want;
     if (S >= 2) {
+      g.big = big;
+      g.tiles = tiles;
       const int chunk = ceil_div(K, S);
       S = ceil_div(K, chunk);
       double* P = temp({S, M, N});
