@@ -44,26 +44,13 @@ __device__ __forceinline__ double warp_dot(const double* x, const double* y, int
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
-// A row-major (m x n) -> Q row-major (m x k), R row-major (k x n).
-// W: column-major m x n scratch, Qc: column-major m x k scratch, tau: k.
-// SM = true: the working copies live in dynamic shared memory (the caller
-// checked the size), so every column step is LDS/STS instead of L2 trips.
-template <bool SM>
-__global__ void __launch_bounds__(kQrThreads)
-    qr_kernel(int m, int n, const double* __restrict__ A, double* Wg, double* Qg, double* tg,
-              double* Q, double* R) {
-  extern __shared__ double qsm[];
+// Householder QR of the column-major m x n matrix W in place (LAPACK
+// dgeqrf conventions: R on and above the diagonal, reflectors below, tau).
+// One warp per column update, three CTA barriers per column.
+__device__ void qr_factor(int m, int n, double* W, double* tau) {
   const int k = m < n ? m : n;
-  double* W = SM ? qsm : Wg;
-  double* tau = SM ? qsm + (size_t)m * n : tg;
-  (void)Qg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ double sh_tau, sh_scal, sh_beta;
-  for (int e = tid; e < (int)m * n; e += blockDim.x) {
-    int i = (int)(e / n), j = (int)(e % n);
-    W[(long long)j * m + i] = A[e];
-  }
-  __syncthreads();
   for (int j = 0; j < k; ++j) {
     double* v = W + (long long)j * m;
     if (warp == 0) {
@@ -102,14 +89,12 @@ __global__ void __launch_bounds__(kQrThreads)
     }
     __syncthreads();
   }
-  // R
-  for (int e = tid; e < (int)k * n; e += blockDim.x) {
-    int r = (int)(e / n), c = (int)(e % n);
-    R[e] = c >= r ? W[(long long)c * m + r] : 0.0;
-  }
-  // Q = H_0 ... H_{k-1} [I_k; 0] formed in place over the reflectors
-  // (LAPACK dorg2r order): column j becomes e_j - tau_j v_j after H_j has
-  // been applied to the already-formed columns right of it.
+}
+
+// Q = H_0 ... H_{k-1} [I_k; 0] formed in place over the reflectors in the
+// first k columns of W (LAPACK dorg2r order).  R must be read before.
+__device__ void qr_form_q(int m, int k, double* W, const double* tau) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __syncthreads();
   for (int j = k - 1; j >= 0; --j) {
     const double t = tau[j];
@@ -126,6 +111,33 @@ __global__ void __launch_bounds__(kQrThreads)
     for (int i = tid; i < m; i += blockDim.x) v[i] = i < j ? 0.0 : (i == j ? 1.0 - t : -t * v[i]);
     __syncthreads();
   }
+}
+
+// A row-major (m x n) -> Q row-major (m x k), R row-major (k x n).
+// W: column-major m x n scratch, tau: k.  SM = true: the working copies live
+// in dynamic shared memory (the caller checked the size), so every column
+// step is LDS/STS instead of L2 trips.
+template <bool SM>
+__global__ void __launch_bounds__(kQrThreads)
+    qr_kernel(int m, int n, const double* __restrict__ A, double* Wg, double* Qg, double* tg,
+              double* Q, double* R) {
+  extern __shared__ double qsm[];
+  const int k = m < n ? m : n;
+  double* W = SM ? qsm : Wg;
+  double* tau = SM ? qsm + (size_t)m * n : tg;
+  (void)Qg;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < (int)m * n; e += blockDim.x) {
+    int i = (int)(e / n), j = (int)(e % n);
+    W[(long long)j * m + i] = A[e];
+  }
+  __syncthreads();
+  qr_factor(m, n, W, tau);
+  for (int e = tid; e < (int)k * n; e += blockDim.x) {
+    int r = (int)(e / n), c = (int)(e % n);
+    R[e] = c >= r ? W[(long long)c * m + r] : 0.0;
+  }
+  qr_form_q(m, k, W, tau);
   for (int e = tid; e < (int)m * k; e += blockDim.x) {
     int i = (int)(e / k), c = (int)(e % k);
     Q[e] = W[(long long)c * m + i];
@@ -190,21 +202,9 @@ __global__ void __launch_bounds__(kQrThreads)
 }
 
 // One-sided (Hestenes) Jacobi on the columns of G (column-major p x q,
-// p >= q).  Circle-method ordering: each round rotates q/2 disjoint column
-// pairs, one warp per pair.  Outputs U (row-major p x q), s (q), Vt
-// (row-major q x q), singular values sorted descending.
-template <bool SM>
-__global__ void __launch_bounds__(kQrThreads)
-    jacobi_kernel(int p, int q, double* Gg, double* Vg, int* perm, double* U, double* s,
-                  double* Vt) {
-  extern __shared__ double jsm[];
-  double* G = Gg;
-  double* V = SM ? jsm + (size_t)p * q : Vg;
-  if (SM) {
-    for (int e = threadIdx.x; e < p * q; e += blockDim.x) jsm[e] = Gg[e];
-    G = jsm;
-    __syncthreads();
-  }
+// p >= q), V (q x q) accumulating the rotations.  Circle-method ordering:
+// each round rotates q/2 disjoint column pairs, one warp per pair.
+__device__ void jacobi_sweeps(int p, int q, double* G, double* V) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   __shared__ int sh_rot;
   for (int e = tid; e < (int)q * q; e += blockDim.x) {
@@ -284,7 +284,12 @@ __global__ void __launch_bounds__(kQrThreads)
     if (!sh_rot) break;
     __syncthreads();
   }
-  // column norms -> s (unsorted, staged in s), then a stable descending order
+}
+
+// Column norms of the rotated G -> s sorted descending (stable), perm[j] =
+// source column of the j-th singular value.  sv: q doubles of scratch.
+__device__ void jacobi_sort(int p, int q, const double* G, int* perm, double* s, double* sv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   for (int c = warp; c < q; c += nwarps) {
     const double* g = G + (long long)c * p;
     double acc = 0.0;
@@ -303,11 +308,30 @@ __global__ void __launch_bounds__(kQrThreads)
     perm[rank] = c;
   }
   __syncthreads();
-  double* sv = V + (long long)q * q;  // q extra doubles of scratch after V
   for (int j = tid; j < q; j += blockDim.x) sv[j] = s[perm[j]];
   __syncthreads();
   for (int j = tid; j < q; j += blockDim.x) s[j] = sv[j];
   __syncthreads();
+}
+
+// Outputs U (row-major p x q), s (q), Vt (row-major q x q), singular values
+// sorted descending.
+template <bool SM>
+__global__ void __launch_bounds__(kQrThreads)
+    jacobi_kernel(int p, int q, double* Gg, double* Vg, int* perm, double* U, double* s,
+                  double* Vt) {
+  extern __shared__ double jsm[];
+  double* G = Gg;
+  double* V = SM ? jsm + (size_t)p * q : Vg;
+  if (SM) {
+    for (int e = threadIdx.x; e < p * q; e += blockDim.x) jsm[e] = Gg[e];
+    G = jsm;
+    __syncthreads();
+  }
+  const int tid = threadIdx.x;
+  jacobi_sweeps(p, q, G, V);
+  double* sv = V + (long long)q * q;  // q extra doubles of scratch after V
+  jacobi_sort(p, q, G, perm, s, sv);
   for (int e = tid; e < (int)p * q; e += blockDim.x) {
     int i = (int)(e / q), j = (int)(e % q);
     double sj = s[j];
@@ -316,6 +340,74 @@ __global__ void __launch_bounds__(kQrThreads)
   for (int e = tid; e < (int)q * q; e += blockDim.x) {
     int j = (int)(e / q), i = (int)(e % q);
     Vt[e] = V[(long long)perm[j] * q + i];
+  }
+}
+
+// Whole thin SVD of a small row-major m x n matrix in one CTA, everything in
+// shared memory: A' = A (m >= n) or A^T (m < n) is factored QR (Householder),
+// R by one-sided Jacobi, U' = Q Ur; for the transposed case the roles of the
+// factors swap on output.  Replaces QR, transpose, Jacobi and GEMM launches.
+__global__ void __launch_bounds__(kQrThreads)
+    svd_small_kernel(int m, int n, const double* __restrict__ A, double* U, double* s, double* Vt) {
+  extern __shared__ double ssm[];
+  const bool tr = m < n;
+  const int mp = tr ? n : m, np = tr ? m : n;  // A' is mp x np, mp >= np
+  double* W = ssm;                       // mp x np column-major
+  double* tau = W + (size_t)mp * np;     // np
+  double* G = tau + np;                  // np x np column-major (R, then rotated)
+  double* V = G + (size_t)np * np;       // np x np
+  double* sv = V + (size_t)np * np;      // np
+  double* ss = sv + np;                  // np
+  double* Ur = ss + np;                  // np x np: Ur[k*np + j]
+  int* perm = reinterpret_cast<int*>(Ur + (size_t)np * np);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < m * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;  // A(i, j)
+    if (tr)
+      W[(size_t)i * mp + j] = A[e];  // A'(j, i) = A(i, j), column i of A'
+    else
+      W[(size_t)j * mp + i] = A[e];
+  }
+  __syncthreads();
+  qr_factor(mp, np, W, tau);
+  for (int e = tid; e < np * np; e += blockDim.x) {
+    const int c = e / np, i = e - c * np;
+    G[e] = i <= c ? W[(size_t)c * mp + i] : 0.0;
+  }
+  __syncthreads();
+  jacobi_sweeps(np, np, G, V);
+  jacobi_sort(np, np, G, perm, ss, sv);
+  for (int e = tid; e < np * np; e += blockDim.x) {
+    const int k = e / np, j = e - k * np;
+    const double sj = ss[j];
+    Ur[e] = sj > 0.0 ? G[(size_t)perm[j] * np + k] / sj : 0.0;
+  }
+  for (int j = tid; j < np; j += blockDim.x) s[j] = ss[j];
+  qr_form_q(mp, np, W, tau);  // begins with a barrier
+  // U' = Q Ur (mp x np), V' = V[:, perm]
+  if (!tr) {
+    for (int e = tid; e < m * n; e += blockDim.x) {
+      const int i = e / n, j = e - (e / n) * n;
+      double acc = 0.0;
+      for (int k = 0; k < np; ++k) acc = fma(W[(size_t)k * mp + i], Ur[k * np + j], acc);
+      U[e] = acc;
+    }
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int j = e / n, i = e - j * n;
+      Vt[e] = V[(size_t)perm[j] * n + i];
+    }
+  } else {
+    // A = V' S U'^T: U (m x m) = V'[:, perm] rows, Vt (m x n) = U'^T
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = e / m, j = e - i * m;
+      U[e] = V[(size_t)perm[j] * m + i];
+    }
+    for (int e = tid; e < m * n; e += blockDim.x) {
+      const int j = e / n, c = e - j * n;
+      double acc = 0.0;
+      for (int k = 0; k < np; ++k) acc = fma(W[(size_t)k * mp + c], Ur[k * np + j], acc);
+      Vt[e] = acc;
+    }
   }
 }
 
@@ -431,6 +523,27 @@ void svd_tall(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
 
 void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
+  {
+    const int mp = m >= n ? m : n, np = m >= n ? n : m;
+    const size_t need = ((size_t)mp * np + 3 * (size_t)np * np + 4 * (size_t)np) * sizeof(double);
+    if (need <= kSmemCap && np <= 64) {
+      static bool attr = false;
+      if (!attr) {
+        T2S2_CUDA(cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemCap));
+        attr = true;
+      }
+      U = m >= n ? DTensor({m, n}) : DTensor({m, m});
+      s = DTensor({np});
+      Vt = m >= n ? DTensor({n, n}) : DTensor({m, n});
+      {
+        LaunchScope ls("svd_jacobi", 4.0 * mp * (double)np * np, 8.0 * m * (double)n);
+        svd_small_kernel<<<1, threads_for(np), need, stream()>>>(m, n, A, U.p, s.p, Vt.p);
+      }
+      T2S2_CHECK_LAUNCH();
+      return;
+    }
+  }
   if (m >= n) {
     svd_tall(m, n, A, U, s, Vt);
     return;

@@ -1054,7 +1054,9 @@ bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   static const bool off = getenv("T2S2_LU_PIVOT_ONLY") != nullptr;
-  const int grid = sm_budget() > 0 && sm_budget() < g_num_sms ? sm_budget() : g_num_sms;
+  static const int grid_env = getenv("T2S2_NP_GRID") ? atoi(getenv("T2S2_NP_GRID")) : 0;
+  int grid = sm_budget() > 0 && sm_budget() < g_num_sms ? sm_budget() : g_num_sms;
+  if (grid_env > 1 && grid_env < grid) grid = grid_env;
   if (off || N > 8192 || grid < 2) return false;
   size_t need = 2 * (size_t)kTm * kTs;
   if (need < (size_t)N) need = N;
