@@ -117,10 +117,12 @@ __device__ void qr_form_q(int m, int k, double* W, const double* tau) {
 // W: column-major m x n scratch, tau: k.  SM = true: the working copies live
 // in dynamic shared memory (the caller checked the size), so every column
 // step is LDS/STS instead of L2 trips.
+// cm != 0: A and Q are column-major (A m x n, Q m x k) — the unfolding of a
+// core read transposed, as the right-orthogonalisation needs it.
 template <bool SM>
 __global__ void __launch_bounds__(kQrThreads)
     qr_kernel(int m, int n, const double* __restrict__ A, double* Wg, double* Qg, double* tg,
-              double* Q, double* R) {
+              double* Q, double* R, int cm) {
   extern __shared__ double qsm[];
   const int k = m < n ? m : n;
   double* W = SM ? qsm : Wg;
@@ -128,8 +130,12 @@ __global__ void __launch_bounds__(kQrThreads)
   (void)Qg;
   const int tid = threadIdx.x;
   for (int e = tid; e < (int)m * n; e += blockDim.x) {
-    int i = (int)(e / n), j = (int)(e % n);
-    W[(long long)j * m + i] = A[e];
+    if (cm) {
+      W[e] = A[e];
+    } else {
+      int i = (int)(e / n), j = (int)(e % n);
+      W[(long long)j * m + i] = A[e];
+    }
   }
   __syncthreads();
   qr_factor(m, n, W, tau);
@@ -139,8 +145,12 @@ __global__ void __launch_bounds__(kQrThreads)
   }
   qr_form_q(m, k, W, tau);
   for (int e = tid; e < (int)m * k; e += blockDim.x) {
-    int i = (int)(e / k), c = (int)(e % k);
-    Q[e] = W[(long long)c * m + i];
+    if (cm) {
+      Q[e] = W[e];
+    } else {
+      int i = (int)(e / k), c = (int)(e % k);
+      Q[e] = W[(long long)c * m + i];
+    }
   }
 }
 
@@ -149,7 +159,7 @@ __global__ void __launch_bounds__(kQrThreads)
 // Householder in shared memory and writes its upper-trapezoidal R (zero
 // padded to n rows) at rows [c*n, (c+1)*n) of Rout.
 __global__ void __launch_bounds__(kQrThreads)
-    qr_r_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Rout) {
+    qr_r_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Rout, int cm) {
   extern __shared__ double W[];
   const int r0 = blockIdx.x * chunk;
   const int mr = m - r0 < chunk ? m - r0 : chunk;
@@ -158,7 +168,7 @@ __global__ void __launch_bounds__(kQrThreads)
   __shared__ double sh_tau, sh_scal, sh_beta;
   for (int e = tid; e < mr * n; e += blockDim.x) {
     const int i = e / n, j = e % n;
-    W[j * mr + i] = A[(long long)(r0 + i) * n + j];
+    W[j * mr + i] = cm ? A[(long long)j * m + r0 + i] : A[(long long)(r0 + i) * n + j];
   }
   __syncthreads();
   for (int j = 0; j < k; ++j) {
@@ -413,7 +423,7 @@ __global__ void __launch_bounds__(kQrThreads)
 
 }  // namespace
 
-void qr_r(int m, int n, const double* A, DTensor& R) {
+void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_r: empty matrix");
   // rows per CTA so that the CTA's block fits the shared-memory budget
   int chunk = (int)(kSmemCap / (sizeof(double) * (size_t)n));
@@ -421,7 +431,7 @@ void qr_r(int m, int n, const double* A, DTensor& R) {
   if (chunk < m && chunk < 2 * n) {
     // a TSQR leaf would not shrink the row count: one global-memory QR
     DTensor Q;
-    qr_thin(m, n, A, Q, R);
+    qr_thin(m, n, A, Q, R, cm);
     return;
   }
   const int blocks = ceil_div(m, chunk);
@@ -435,7 +445,7 @@ void qr_r(int m, int n, const double* A, DTensor& R) {
   {
     LaunchScope ls("qr", 2.0 * m * (double)n * n, 8.0 * m * (double)n);
     qr_r_kernel<<<blocks, threads_for(n), (size_t)chunk * n * sizeof(double), stream()>>>(
-        m, n, chunk, A, stacked.p);
+        m, n, chunk, A, stacked.p, cm ? 1 : 0);
   }
   T2S2_CHECK_LAUNCH();
   if (blocks == 1) {
@@ -447,7 +457,7 @@ void qr_r(int m, int n, const double* A, DTensor& R) {
   qr_r(blocks * n, n, stacked.p, R);  // TSQR: reduce the stacked leaf factors
 }
 
-void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
+void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_thin: empty matrix");
   const int k = m < n ? m : n;
   Q = DTensor({m, k});
@@ -465,9 +475,10 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R) {
                                        (int)kSmemCap));
         attr = true;
       }
-      qr_kernel<true><<<1, threads_for(n), need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+      qr_kernel<true><<<1, threads_for(n), need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p,
+                                                              cm ? 1 : 0);
     } else {
-      qr_kernel<false><<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p);
+      qr_kernel<false><<<1, kQrThreads, 0, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p, cm ? 1 : 0);
     }
   }
   T2S2_CHECK_LAUNCH();

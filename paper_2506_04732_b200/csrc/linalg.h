@@ -10,11 +10,12 @@ namespace t2s2 {
 // Thin QR of a row-major m x n matrix: Q (m x k, orthonormal columns) and
 // R (k x n, upper trapezoidal), k = min(m, n).  Householder reflectors in
 // the LAPACK dgeqrf/dorgqr convention.
-void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R);
+// cm: A (m x n) and Q (m x k) column-major instead.
+void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm = false);
 
 // R factor only (k x n, k = min(m, n)) of a row-major m x n matrix; tall
 // inputs are reduced by a TSQR tree of shared-memory Householder leaves.
-void qr_r(int m, int n, const double* A, DTensor& R);
+void qr_r(int m, int n, const double* A, DTensor& R, bool cm = false);
 
 // Thin SVD A = U diag(s) Vt of a row-major m x n matrix, k = min(m, n),
 // singular values descending.  Tall case: QR, then one-sided Jacobi on R.

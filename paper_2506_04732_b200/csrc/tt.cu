@@ -103,13 +103,13 @@ void right_orthonormalize(std::vector<DTensor>& cores) {
     const int r0 = c.dim(0), r1 = c.dim(-1);
     const long long mid = mid_size(c);
     const int rows = (int)(mid * r1);
-    DTensor Mt({rows, r0});
-    transpose(c.p, Mt.p, r0, rows);
+    // the row-major r0 x rows unfolding is the column-major rows x r0 matrix
+    // whose QR we need; Q comes back column-major = the new core row-major
     DTensor Q, R;
-    qr_thin(rows, r0, Mt.p, Q, R);  // Q rows x k, R k x r0
+    qr_thin(rows, r0, c.p, Q, R, true);  // Q rows x k (column-major), R k x r0
     const int k = rows < r0 ? rows : r0;
     DTensor nc(with_bonds(c, k, r1));
-    transpose(Q.p, nc.p, rows, k);
+    dcopy(nc.p, Q.p, (size_t)rows * k);
     DTensor& p = cores[l - 1];
     const int pr = (int)((long long)p.size() / r0);
     DTensor np(with_bonds(p, p.dim(0), k));
@@ -136,9 +136,7 @@ double tt_norm(const Train& t) {
     else
       gemm(false, true, r0 * mid, k, r1, 1.0, c.p, r1, Rp.p, r1, 0.0, Y.p, k);
     if (l == 0) return dnrm2(Y.p, Y.size());
-    DTensor Yt({mid * k, r0});
-    transpose(Y.p, Yt.p, r0, mid * k);
-    qr_r(mid * k, r0, Yt.p, Rp);
+    qr_r(mid * k, r0, Y.p, Rp, true);  // Y row-major r0 x (mid k) = column-major (mid k) x r0
   }
   return 0.0;
 }
