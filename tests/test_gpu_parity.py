@@ -365,3 +365,74 @@ def test_config4_sweep_concurrent_contexts(golden, pk):
     # deterministic engine: solve 0 is bit-identical with and without threads
     for c1, c2 in zip(res[0]["x"], serial[0]["x"]):
         np.testing.assert_array_equal(c1, c2)
+
+
+def test_config3_full_size_steps_match_oracle(pk):
+    """Config 3 at full size (d=6, n=65, eps=1e-12, dt=5e-4): the first two
+    implicit steps through the device march against the CPU oracle (the
+    numpy restatement of time_integration._march / tt_solver.solve) on the
+    same operators and forcing.  Ranks identical, states within the
+    protocol's tolerance (solve residuals plus the step re-truncation)."""
+    from oracle import als_solver as als
+    from oracle import march as om
+    from paper_2506_04732_b200 import workloads as wl
+    from paper_2506_04732_b200.march import march_device
+
+    _, tt, solver, _ = pk
+    recipe = wl.config(3)
+    left, right, state0, forcing, exact, _ = wl.march_problem(recipe)
+    steps = 2
+    fs = [forcing(k) for k in range(1, steps + 1)]
+    hl, hr, hs = tt.to_device(left), tt.to_device(right), tt.to_device(state0)
+    bcs = [tt.to_device(b) for b, _ in fs]
+    srcs = [tt.to_device(s) for _, s in fs]
+    cfg = solver.SolverConfig(**recipe.solver)
+    stored, rows = march_device(hl, hr, hs, steps, bcs, srcs, recipe.step_tol, cfg, store_stride=1)
+    state = state0.cores
+    for k in range(1, steps + 1):
+        state, rep, _ = om.step(left.cores, right.cores, state, fs[k - 1][0].cores,
+                                fs[k - 1][1].cores, recipe.step_tol, als.Config(**recipe.solver))
+        got = tt.from_device(stored[k]).cores
+        ok, det = ranks_agree(got, state)
+        assert ok, (k, det)
+        tol = value_tol(rows[k - 1][3], rep.residual_history[-1]) + 2 * recipe.step_tol
+        assert rel_diff(got, state) <= k * tol, k
+    for h in [hl, hr, hs] + bcs + srcs + list(stored.values()):
+        h.free()
+
+
+@pytest.mark.parametrize("index", [0, 7])
+def test_config4_full_size_sweeps_within_oracle_spread(pk, index):
+    """Config 4 at full size (d=6, n=33): two alternating sweeps of one of
+    the 64 seeded boundary-layer solves (index 7: eps = 2.9e-12, the steep
+    end of the draw) from the default initial guess.  Far from convergence
+    the reference algorithm itself is not reproducible: with the same
+    inputs, the oracle's residual after one sweep moves by ~2% between BLAS
+    thread counts (0.885 with 1 thread, 0.865 with 8, 0.878 default for
+    index 0: tools/c4_check.py), because near-equal candidate scores
+    (tt_solver.py:383-387) and enrichment directions depend on the summation
+    order.  The device run must reproduce the ranks exactly and its residual
+    history must lie within the envelope of five oracle executions (1, 2, 4,
+    8 BLAS threads and the default) widened by their own spread."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import als_solver as als
+    from paper_2506_04732_b200 import workloads as wl
+
+    _, tt, solver, _ = pk
+    r = wl.sweep_recipes()[index]
+    a, b, exact, _ = wl.steady_problem(r)
+    kw = dict(r.solver)
+    kw["max_sweeps"] = 2
+    x, rep = solver.solve(a, b, cfg=solver.SolverConfig(**kw))
+    runs = []
+    for limit in (1, 2, 4, 8, None):
+        with threadpool_limits(limits=limit):
+            xo, repo = als.solve(a.cores, b.cores, cfg=als.Config(**kw))
+        runs.append((xo, np.array(repo.residual_history)))
+        assert ot.ranks_of(x.cores) == ot.ranks_of(xo)
+    hist = np.array([h for _, h in runs])
+    lo, hi = hist.min(axis=0), hist.max(axis=0)
+    spread = np.maximum(hi - lo, 1e-8 * hi)
+    got = np.array(rep.residual_history)
+    assert np.all(got >= lo - 3 * spread) and np.all(got <= hi + 3 * spread), (got, lo, hi)
