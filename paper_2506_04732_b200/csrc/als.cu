@@ -545,33 +545,88 @@ int count_significant(const std::vector<double>& zs) {
   return nz;
 }
 
+// Truncation rank of a split on the device (tt_solver.py:249-258, 268-270):
+// delta = rounding_tol * ||s|| / sqrt(max(d-1, 1)), keep = first k with
+// ||s[k:]|| <= delta (at least 1), capped at max_rank; mask[j] = j < keep.
+// Products and sums are rounded separately, in the reference's order.  One
+// thread: s has at most a few dozen entries.
+__global__ void split_keep_kernel(const double* s, int n, double tol, double rootd, int max_rank,
+                                  double* keep_out, double* mask) {
+  if (threadIdx.x != 0) return;
+  double nrm = 0.0;
+  for (int k = 0; k < n; ++k) nrm = __dadd_rn(nrm, __dmul_rn(s[k], s[k]));
+  const double delta = tol * sqrt(nrm) / rootd;
+  int r = n;
+  double acc = 0.0;
+  // tails from the back; keep the FIRST k with tail <= delta
+  for (int k = n - 1; k >= 0; --k) {
+    acc = __dadd_rn(acc, __dmul_rn(s[k], s[k]));
+    if (sqrt(acc) <= delta) r = k;
+  }
+  if (n == 0) r = 1;
+  if (r < 1) r = 1;
+  if (r > max_rank) r = max_rank;
+  keep_out[0] = (double)r;
+  for (int j = 0; j < n; ++j) mask[j] = j < r ? 1.0 : 0.0;
+}
+
+// Split of a solved core with enrichment from the residual gradient
+// (tt_solver.py:261-302).  The truncation rank is decided on the device and
+// the projection of the gradient is masked with it, so the core's singular
+// values, the gradient's singular values and the rank travel to the host in
+// ONE read-back (was two synchronising reads).
+struct SplitSync {
+  DTensor keep_mask;  // [0] = keep, [1..kk] = mask
+  int kk;
+  SplitSync(const DTensor& s, const SolverConfig& cfg, int d) : keep_mask({1 + s.dim(0)}), kk(s.dim(0)) {
+    LaunchScope ls("reduce", 0, 0);
+    split_keep_kernel<<<1, 32, 0, stream()>>>(s.p, kk, cfg.rounding_tol,
+                                              std::sqrt((double)(d - 1 > 1 ? d - 1 : 1)),
+                                              cfg.max_rank, keep_mask.p, keep_mask.p + 1);
+    T2S2_CHECK_LAUNCH();
+  }
+  const double* mask() const { return keep_mask.p + 1; }
+  // read keep, s and (optionally) zs together
+  int read(const DTensor& s, const DTensor* zs, std::vector<double>& hz) {
+    const int zk = zs ? zs->dim(0) : 0;
+    DTensor buf({1 + kk + zk});
+    dcopy(buf.p, keep_mask.p, 1);
+    dcopy(buf.p + 1, s.p, kk);
+    if (zk) dcopy(buf.p + 1 + kk, zs->p, zk);
+    std::vector<double> h(1 + kk + zk);
+    to_host(h.data(), buf.p, h.size());
+    hz.assign(h.begin() + 1 + kk, h.end());
+    return (int)h[0];
+  }
+};
+
 Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& cfg, int d) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
   DTensor U, s, Vt;
   svd_thin(m, r1, u.p, U, s, Vt);
   const int kk = s.dim(0);
-  std::vector<double> hs = host_vec(s);
-  const double delta = cfg.rounding_tol * vec_norm(hs) / std::sqrt((double)(d - 1 > 1 ? d - 1 : 1));
-  int keep = tail_keep(hs, delta);
-  if (keep > cfg.max_rank) keep = cfg.max_rank;
+  SplitSync sync(s, cfg, d);
+  const bool enrich = cfg.enrichment_rank > 0 && grad;
+  DTensor zu, zs, zvt;
+  int zk = 0;
+  if (enrich) {
+    // z = g - U_keep U_keep^T g, with U_keep = U diag(mask)
+    const int gc = (int)(grad->size() / m);
+    DTensor z = grad->clone();
+    DTensor tmp({kk, gc});
+    gemm(true, false, kk, gc, m, 1.0, U.p, kk, z.p, gc, 0.0, tmp.p, gc);
+    scale_rows(tmp.p, kk, gc, gc, sync.mask());
+    gemm(false, false, m, gc, kk, -1.0, U.p, kk, tmp.p, gc, 1.0, z.p, gc);
+    svd_thin(m, gc, z.p, zu, zs, zvt);
+    zk = zs.dim(0);
+  }
+  std::vector<double> hz;
+  const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({keep, r1});
   dcopy(out.carry.p, Vt.p, (size_t)keep * r1);
   scale_rows(out.carry.p, keep, r1, r1, s.p);
-  DTensor zu;
-  int zk = 0;
-  if (cfg.enrichment_rank > 0 && keep < cfg.max_rank && grad) {
-    DTensor basis({m, keep});
-    copy2d(basis.p, keep, U.p, kk, m, keep);
-    const int gc = (int)(grad->size() / m);
-    DTensor z = grad->clone();
-    DTensor tmp({keep, gc});
-    gemm(true, false, keep, gc, m, 1.0, basis.p, keep, z.p, gc, 0.0, tmp.p, gc);
-    gemm(false, false, m, gc, keep, -1.0, basis.p, keep, tmp.p, gc, 1.0, z.p, gc);
-    DTensor zs, zvt;
-    svd_thin(m, gc, z.p, zu, zs, zvt);
-    zk = zs.dim(0);
-    std::vector<double> hz = host_vec(zs);
+  if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
     if (cfg.max_rank - keep < extra) extra = cfg.max_rank - keep;
@@ -589,24 +644,26 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
   DTensor U, s, Vt;
   svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
   const int kk = s.dim(0);
-  std::vector<double> hs = host_vec(s);
-  const double delta = cfg.rounding_tol * vec_norm(hs) / std::sqrt((double)(d - 1 > 1 ? d - 1 : 1));
-  int keep = tail_keep(hs, delta);
-  if (keep > cfg.max_rank) keep = cfg.max_rank;
+  SplitSync sync(s, cfg, d);
+  const bool enrich = cfg.enrichment_rank > 0 && grad;
+  DTensor zu, zs, zvt;
+  if (enrich) {
+    // z = g - g Vt_keep^T Vt_keep, with Vt_keep = diag(mask) Vt
+    const int gr = (int)(grad->size() / cols);
+    DTensor z = grad->clone();
+    DTensor tmp({gr, kk});
+    gemm(false, true, gr, kk, cols, 1.0, z.p, cols, Vt.p, cols, 0.0, tmp.p, kk);
+    scale_cols(tmp.p, gr, kk, kk, sync.mask());
+    gemm(false, false, gr, cols, kk, -1.0, tmp.p, kk, Vt.p, cols, 1.0, z.p, cols);
+    svd_thin(gr, cols, z.p, zu, zs, zvt);
+  }
+  std::vector<double> hz;
+  const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({r0, keep});
   copy2d(out.carry.p, keep, U.p, kk, r0, keep);
   scale_cols(out.carry.p, r0, keep, keep, s.p);
-  DTensor zvt;
-  if (cfg.enrichment_rank > 0 && keep < cfg.max_rank && grad) {
-    const int gr = (int)(grad->size() / cols);
-    DTensor z = grad->clone();
-    DTensor tmp({gr, keep});
-    gemm(false, true, gr, keep, cols, 1.0, z.p, cols, Vt.p, cols, 0.0, tmp.p, keep);
-    gemm(false, false, gr, cols, keep, -1.0, tmp.p, keep, Vt.p, cols, 1.0, z.p, cols);
-    DTensor zu, zs;
-    svd_thin(gr, cols, z.p, zu, zs, zvt);
-    std::vector<double> hz = host_vec(zs);
+  if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
     if (cfg.max_rank - keep < extra) extra = cfg.max_rank - keep;

@@ -1,5 +1,6 @@
 // Device GMRES(restart) and Jacobi-PCG (see iterative.h).
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "blas.h"
@@ -414,6 +415,9 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   };
   double rnorm = residual();
   int inner = 0;
+  // host polls of the device convergence flag (each one drains the stream);
+  // iterations past convergence are no-ops on the device (guarded)
+  static const int poll = getenv("T2S2_KRYLOV_POLL") ? atoi(getenv("T2S2_KRYLOV_POLL")) : 16;
   if (rnorm < atol) {
     allocator().release(V);
     allocator().release(r);
@@ -431,7 +435,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
     }
     T2S2_CHECK_LAUNCH();
     for (int col = 0; col < restart; ++col) {
-      if (col > 0 && col % 8 == 0 && !read_flag(&st->active)) break;
+      if (col > 0 && col % poll == 0 && !read_flag(&st->active)) break;
       A(V + (size_t)col * n, V + (size_t)(col + 1) * n, &st->active);  // skipped once converged
       {
         LaunchScope ls("gmres", 8.0 * n * (col + 2), 32.0 * n * (col + 2));
@@ -494,6 +498,7 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   if (G < 1) G = 1;
   int it = 0;
   double at = atol;
+  static const int poll = getenv("T2S2_KRYLOV_POLL") ? atoi(getenv("T2S2_KRYLOV_POLL")) : 20;
   {
     LaunchScope ls("cg", 6.0 * n, 40.0 * n);
     int itv = 0;
@@ -502,7 +507,7 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
                                           0, stream()));
   }
   for (; it < maxiter; ++it) {
-    if (it > 0 && it % 10 == 0 && !read_flag(&st->active)) break;
+    if (it > 0 && it % poll == 0 && !read_flag(&st->active)) break;
     A(p, q, &st->active);  // skipped on the device once converged
     {
       // this iteration's update and the next one's top (convergence, p)
