@@ -1,0 +1,614 @@
+// Verified no-pivot dense solve of a local system by blocked Gauss-Jordan
+// elimination in ONE cooperative launch, one grid barrier per 32-column
+// panel and no back-substitution chain.
+//
+// The local systems of an implicit step (I + dt L projected on orthonormal
+// interface bases, tt_solver.py:350-362 solves them with numpy.linalg.solve)
+// are well conditioned and almost never need a row interchange.  Gaussian
+// elimination with partial pivoting makes no interchange exactly when every
+// multiplier satisfies |l| <= 1; we check every multiplier and decline
+// (*info = -1, the caller runs the pivoting kernel) otherwise.
+//
+// Panel p (rows/columns [k0, k1), k1 = k0 + 32), normalised block
+// Gauss-Jordan:
+//   CTA 0 (previous phase) factored the diagonal block D_p = L U (one
+//   32-step loop: U, L^{-1} and U^{-1} together, multipliers checked) and
+//   published D^{-1} = U^{-1} L^{-1} and U^{-1} (32 x 32 each).
+//   Every other row block I (above AND below the panel) is a tile task
+//   together with a column block J of [k1, N] (column N = right-hand side):
+//       W_J = D^{-1} A[p, J]            (the panel rows, normalised)
+//       A[I, J] -= A[I, p] W_J          (FP64 tensor core, DMMA m8n8k4)
+//   and, once per row block below the panel, the multipliers
+//   A[I, p] U^{-1} are formed and checked (|l| <= 1).  A CTA walks a
+//   contiguous J-major chunk of tasks, so W_J is formed once per CTA and
+//   column block, and the next task's global loads are in flight (in
+//   registers) while the current one computes.  The tile of row block 0
+//   stores W_J to a double-buffered 32 x (N+1) row panel, which the next
+//   phase reads as those rows' current values.
+//   CTA 0 takes the tile holding the next diagonal block and factors it
+//   while the other CTAs work (lookahead), so a panel costs ONE grid
+//   barrier.
+// After the last panel every diagonal block is the identity: b holds x.
+//
+// Algorithmic cost N^3 (vs 2/3 N^3 + back substitution for LU): on this
+// latency-bound size range (N <= 2000, <= 63 panels) the extra tiles fill
+// otherwise idle SMs and the sequential back-substitution disappears.
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "linalg.h"
+
+namespace cg = cooperative_groups;
+
+namespace t2s2 {
+namespace {
+
+constexpr int kThr = 256;      // 8 warps
+constexpr int kP = 32;         // panel width
+constexpr int kT = 64;         // tile rows / columns
+constexpr int kLdT = kT + 4;   // smem stride of 64-long columns
+constexpr int kLdP = kP + 4;   // smem stride of 32-long columns
+constexpr int kInv = 2 * kP * kP;  // per panel: L^{-1} then U^{-1}, column-major
+
+struct GjArgs {
+  int N;
+  double* A;      // column-major N x N (clobbered)
+  double* b;      // right-hand side (column N), overwritten with x
+  double* inv;    // npan * kInv
+  double* wbuf;   // 2 x (kP x (N+1)), column-major ld kP
+  int* info;      // 0, or -1: a multiplier exceeded 1 / zero pivot
+  unsigned long long* prof;
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void gj_fail(const GjArgs& a) { atomicExch(a.info, -1); }
+
+// Geometry of one phase.
+struct Phase {
+  int N, p, k0, kb, k1;  // panel rows/cols [k0, k1)
+  int kb2;            // width of the next diagonal block (0 on the last panel)
+  int nbelow, nabove, nrb;  // row blocks: [next diag (kb2 rows)], 64-row blocks below, 64-row blocks above
+  int ncb;            // column blocks of [k1, N]: [next diag (kb2)], 64-wide blocks
+  int kprev;          // first row of the previous panel (rows read from wbuf), -1 if p == 0
+  __device__ Phase(int N_, int p_) : N(N_), p(p_) {
+    k0 = p * kP;
+    kb = N - k0 < kP ? N - k0 : kP;
+    k1 = k0 + kb;
+    kb2 = N - k1 < kP ? N - k1 : kP;
+    const int rest = N - k1 - kb2;  // rows below the next diagonal block
+    nbelow = (kb2 > 0 ? 1 : 0) + (rest + kT - 1) / kT;
+    nabove = (k0 + kT - 1) / kT;
+    nrb = nbelow + nabove;
+    const int crest = N + 1 - k1 - kb2;  // columns after the next diagonal block (incl. rhs)
+    ncb = (kb2 > 0 ? 1 : 0) + (crest + kT - 1) / kT;
+    kprev = p > 0 ? k0 - kP : -1;
+  }
+  __device__ void rows(int I, int& r, int& m) const {
+    if (I < nbelow) {
+      if (kb2 > 0 && I == 0) {
+        r = k1;
+        m = kb2;
+        return;
+      }
+      r = k1 + kb2 + (kb2 > 0 ? I - 1 : I) * kT;
+      m = N - r < kT ? N - r : kT;
+    } else {
+      r = (I - nbelow) * kT;
+      m = k0 - r < kT ? k0 - r : kT;
+    }
+  }
+  __device__ void cols(int J, int N, int& c, int& n) const {
+    if (kb2 > 0 && J == 0) {
+      c = k1;
+      n = kb2;
+      return;
+    }
+    const int j = kb2 > 0 ? J - 1 : J;
+    c = k1 + kb2 + j * kT;
+    n = N + 1 - c < kT ? N + 1 - c : kT;
+  }
+};
+
+// Current value of the augmented matrix entry (r, c), c <= N: rows of the
+// previous panel live in the row-panel buffer of the previous phase.
+__device__ __forceinline__ const double* src_ptr(const GjArgs& a, const Phase& ph, int r, int c) {
+  if (ph.kprev >= 0 && r >= ph.kprev && r < ph.k0)
+    return a.wbuf + (size_t)((ph.p - 1) & 1) * kP * (a.N + 1) + (size_t)c * kP + (r - ph.kprev);
+  return c < a.N ? a.A + (size_t)c * a.N + r : a.b + r;
+}
+__device__ __forceinline__ double* dst_ptr(const GjArgs& a, int r, int c) {
+  return c < a.N ? a.A + (size_t)c * a.N + r : a.b + r;
+}
+
+struct Smem {
+  double di[kP * kLdP];   // D^{-1}: A operand, [k*kLdP + m]
+  double ui[kP * kLdP];   // U^{-1}: B operand, [n*kLdP + k]
+  double ab[kP * kLdT];   // A[I, p] (m x kb): A operand [k*kLdT + m]
+  double pb[kT * kLdP];   // A[p, J] (kb x n): B operand [n*kLdP + k]
+  double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
+  double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
+  double za[kP * kLdP], xb[kP * kLdP];  // U^{-1}, L^{-1} as DMMA operands (gj_diag)
+  double rowd[2][kP], rowx[2][kP], cold[2][kP], colz[2][kP], rinv[kP];  // gj_diag broadcasts
+};
+
+// Load D^{-1}, U^{-1} of panel p into shared memory.
+__device__ void load_inv(const GjArgs& a, int p, Smem& s) {
+  const double* g = a.inv + (size_t)p * kInv;
+  for (int e = threadIdx.x; e < kP * kP; e += kThr) {
+    const int c = e >> 5, r = e & 31;
+    s.di[c * kLdP + r] = __ldcg(g + e);            // Dinv[r][c] -> A op [k=c][m=r]
+    s.ui[c * kLdP + r] = __ldcg(g + kP * kP + e);  // Uinv[r][c] -> B op [n=c][k=r]
+  }
+}
+
+// One tile task of a phase: rows [r, r+m) x columns [c, c+n) of the
+// augmented matrix (column N = right-hand side).
+struct Task {
+  int I, J, r, m, c, n;
+};
+__device__ __forceinline__ Task task_of(const Phase& ph, int t) {
+  Task k;
+  k.J = t / ph.nrb;
+  k.I = t - k.J * ph.nrb;
+  ph.rows(k.I, k.r, k.m);
+  ph.cols(k.J, ph.N, k.c, k.n);
+  return k;
+}
+
+// The global loads of one task, held in registers while the previous task
+// computes: A[I, p] (8 per thread), A[p, J] (8 per thread, only for a new
+// column block) and this lane's C fragments (warp tile 32 x 16).
+struct TileRegs {
+  double ab[8], pb[8], cv[4][2][2];
+};
+
+__device__ __forceinline__ void tile_load(const GjArgs& a, const Phase& ph, const Task& k, bool want_p,
+                                          TileRegs& R) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = wm0 + i * 8 + (lane >> 2), cc = wn0 + j * 8 + (lane & 3) * 2 + h;
+        R.cv[i][j][h] = (rr < k.m && cc < k.n) ? __ldcg(src_ptr(a, ph, k.r + rr, k.c + cc)) : 0.0;
+      }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int e = tid + q * kThr, kk = e >> 6, i = e & 63;
+    R.ab[q] = (i < k.m && kk < ph.kb) ? __ldcg(src_ptr(a, ph, k.r + i, ph.k0 + kk)) : 0.0;
+  }
+  if (want_p) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + q * kThr, j = e >> 5, kk = e & 31;
+      R.pb[q] = (kk < ph.kb && j < k.n) ? __ldcg(dst_ptr(a, ph.k0 + kk, k.c + j)) : 0.0;
+    }
+  }
+}
+
+__device__ __forceinline__ void tile_stage(const TileRegs& R, bool want_p, Smem& s) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int e = tid + q * kThr;
+    s.ab[(e >> 6) * kLdT + (e & 63)] = R.ab[q];
+  }
+  if (want_p) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + q * kThr;
+      s.pb[(e >> 5) * kLdP + (e & 31)] = R.pb[q];
+    }
+  }
+}
+
+// Compute one staged task (operands in s.ab / s.pb, C fragments in cv):
+//   want_w : W = D^{-1} A[p, J] for a new column block (store_w: publish it
+//            as the panel rows' new values),
+//   check  : the multipliers A[I, p] U^{-1} of rows below the panel,
+//   C -= A[I, p] W  -> global memory, or s.dg for the next diagonal block.
+__device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, const double (&cv)[4][2][2],
+                             bool want_w, bool store_w, bool check, bool to_diag, Smem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (want_w) {
+    const int wr0 = (warp >> 2) * 16, wc0 = (warp & 3) * 16;
+    double acc[2][2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[2], bf[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = s.di[kr * kLdP + wr0 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = s.pb[(wc0 + j * 8 + (lane >> 2)) * kLdP + kr];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    double* wdst = a.wbuf + (size_t)(ph.p & 1) * kP * (a.N + 1);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kr = wr0 + i * 8 + (lane >> 2), cc = wc0 + j * 8 + (lane & 3) * 2 + h;
+          s.ws[cc * kLdP + kr] = acc[i][j][h];
+          if (store_w && kr < ph.kb && cc < k.n) wdst[(size_t)(k.c + cc) * kP + kr] = acc[i][j][h];
+        }
+  }
+  if (check) {
+    const int mm0 = (warp >> 1) * 16, mn0 = (warp & 1) * 16;
+    double acc[2][2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[2], bf[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = s.ab[kr * kLdT + mm0 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = s.ui[(mn0 + j * 8 + (lane >> 2)) * kLdP + kr];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (mm0 + i * 8 + (lane >> 2) < k.m && !(fabs(acc[i][j][h]) <= 1.0)) bad = true;
+    if (bad) gj_fail(a);
+  }
+  __syncthreads();  // W visible
+  const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
+  if (wm0 < k.m && wn0 < k.n) {
+    double acc[4][2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = s.ab[kr * kLdT + wm0 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = s.ws[(wn0 + j * 8 + (lane >> 2)) * kLdP + kr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = wm0 + i * 8 + (lane >> 2), cc = wn0 + j * 8 + (lane & 3) * 2 + h;
+          if (rr < k.m && cc < k.n) {
+            const double v = cv[i][j][h] - acc[i][j][h];
+            if (to_diag)
+              s.dg[cc * 33 + rr] = v;
+            else
+              *dst_ptr(a, k.r + rr, k.c + cc) = v;
+          }
+        }
+  }
+  __syncthreads();  // s.ab / s.pb / s.ws free
+}
+
+// Factor the kb x kb block in s.dg (no interchanges, multipliers checked)
+// and publish L^{-1}, U^{-1} (zero padded to 32 x 32) for panel p.
+//
+// One right-looking loop of 32 steps, one CTA barrier each.  Thread
+// (row i = lane, column group g = warp) keeps four columns of three
+// matrices in registers:
+//   D  the block being eliminated (U in the upper triangle at the end),
+//   X  L^{-1}: forward elimination of [L | I] rides along (row st of X is
+//      final when st becomes the pivot row),
+//   Z  U^{-1} column by column: Y[:, st] = Z[:, st] / u_stst as soon as
+//      row st of U is final, then Z[:, j>st] -= Y[:, st] U[st, j].
+// Step st needs row st of D and X and column st of D and Z, which their
+// owners publish (double buffered) before the barrier that ends step
+// st - 1; the owner of u_{st+1,st+1} also publishes its reciprocal.
+// Rolled over the steps: this runs once per panel between tile phases,
+// so it must stay small in the instruction cache.
+#ifdef GJ_MICRO
+__device__ long long g_diag_t[8];
+#define GJ_T(k) if (threadIdx.x == 0) g_diag_t[k] = clock64();
+#define GJ_TS(k) if (threadIdx.x == 75 && st == 10) g_diag_t[k] = clock64();
+#else
+#define GJ_T(k)
+#define GJ_TS(k)
+#endif
+__device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
+  const int tid = threadIdx.x, i = tid & 31, g = tid >> 5;
+  __syncthreads();
+  GJ_T(0)
+  double dv[4], xv[4], zv[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = 4 * g + q;
+    dv[q] = (i < kb && j < kb) ? s.dg[j * 33 + i] : (i == j ? 1.0 : 0.0);
+    xv[q] = i == j ? 1.0 : 0.0;
+    zv[q] = xv[q];
+  }
+  bool bad = false;
+  // publish step 0's row, column and reciprocal pivot
+  if (i == 0)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s.rowd[0][4 * g + q] = dv[q];
+      s.rowx[0][4 * g + q] = xv[q];
+    }
+  if (g == 0) {
+    s.cold[0][i] = dv[0];
+    s.colz[0][i] = zv[0];
+    if (i == 0) {
+      s.rinv[0] = 1.0 / dv[0];
+      if (!(fabs(dv[0]) > 0.0) || !isfinite(dv[0])) bad = true;
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int st = 0; st < kP; ++st) {
+    GJ_TS(3)
+    const int par = st & 1;
+    const double rinv = s.rinv[st];
+    const double l = i > st ? s.cold[par][i] * rinv : 0.0;  // multiplier l_{i,st}
+    const double y = i <= st ? s.colz[par][i] * rinv : 0.0; // (U^{-1})_{i,st}
+    if (g == 0 && !(fabs(l) <= 1.0)) bad = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = 4 * g + q;
+      const double ur = s.rowd[par][j], xr = s.rowx[par][j];
+      if (j > st) {
+        dv[q] = fma(-l, ur, dv[q]);
+        zv[q] = fma(-y, ur, zv[q]);
+      } else {
+        xv[q] = fma(-l, xr, xv[q]);
+        if (j == st && i <= st) zv[q] = y;
+      }
+    }
+    GJ_TS(4)
+    const int nx = st + 1;
+    if (nx < kP) {
+      if (i == nx)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s.rowd[par ^ 1][4 * g + q] = dv[q];
+          s.rowx[par ^ 1][4 * g + q] = xv[q];
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * g + q == nx) {
+          s.cold[par ^ 1][i] = dv[q];
+          s.colz[par ^ 1][i] = zv[q];
+          if (i == nx) {
+            s.rinv[nx] = 1.0 / dv[q];
+            if (!(fabs(dv[q]) > 0.0) || !isfinite(dv[q])) bad = true;
+          }
+        }
+    }
+    GJ_TS(5)
+    __syncthreads();
+    GJ_TS(6)
+  }
+  GJ_T(1)
+  if (bad) gj_fail(a);
+  // D^{-1} = U^{-1} L^{-1} (DMMA, 32 x 32 x 32); publish D^{-1} and U^{-1}
+  // zero padded outside kb x kb
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    s.za[(4 * g + q) * kLdP + i] = zv[q];  // A operand [k][m] = Z[m][k]
+    s.xb[(4 * g + q) * kLdP + i] = xv[q];  // B operand [n][k] = X[k][n]
+  }
+  __syncthreads();
+  double* gl = a.inv + (size_t)p * kInv;
+  {
+    const int lane = i, warp = g, m0 = (warp >> 1) * 8, n0 = (warp & 1) * 16;
+    double acc[2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      const double af = s.za[kr * kLdP + m0 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        dmma(acc[j][0], acc[j][1], af, s.xb[(n0 + j * 8 + (lane >> 2)) * kLdP + kr]);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
+        gl[cc * kP + rr] = (rr < kb && cc < kb) ? acc[j][h] : 0.0;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = 4 * g + q;
+    gl[kP * kP + j * kP + i] = (i < kb && j < kb) ? zv[q] : 0.0;
+  }
+  GJ_T(2)
+  __syncthreads();  // (the grid barrier that follows publishes the stores)
+}
+
+__global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& s = *reinterpret_cast<Smem*>(smraw);
+  const int N = a.N, G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int npan = (N + kP - 1) / kP;
+  const bool pr = a.prof && cta < 2 && tid == 0;
+  unsigned long long tp = pr ? gtimer() : 0;
+#define GJ_PHASE(slot)                         \
+  if (pr) {                                    \
+    const unsigned long long tq = gtimer();    \
+    a.prof[cta * 4 + (slot)] += tq - tp;       \
+    tp = tq;                                   \
+  }
+  if (cta == 0) {
+    const int kb = N < kP ? N : kP;
+    for (int e = tid; e < kP * kP; e += kThr) {
+      const int c = e >> 5, r = e & 31;
+      if (r < kb && c < kb) s.dg[c * 33 + r] = __ldcg(a.A + (size_t)c * N + r);
+    }
+    gj_diag(a, 0, kb, s);
+  }
+  grid.sync();
+  TileRegs R;
+  for (int p = 0; p < npan; ++p) {
+    if (__ldcg(a.info) != 0) break;  // declined: stop early (uniform after the barrier)
+    GJ_PHASE(3)
+    const Phase ph(N, p);
+    const bool has_diag = ph.kb2 > 0;
+    const int ntile = ph.nrb * ph.ncb - (has_diag ? 1 : 0);
+    if (has_diag && cta == 0) {
+      // the next diagonal block: W of its columns, multipliers checked,
+      // updated block kept in shared memory, then factored
+      const Task k = task_of(ph, 0);
+      tile_load(a, ph, k, true, R);
+      load_inv(a, p, s);
+      tile_stage(R, true, s);
+      __syncthreads();
+      tile_compute(a, ph, k, R.cv, true, true, true, true, s);
+      unsigned long long td = pr ? gtimer() : 0;
+      gj_diag(a, p + 1, ph.kb2, s);
+      if (pr) a.prof[9] += gtimer() - td;
+    } else {
+      // a contiguous chunk of the J-major task list (consecutive tasks share
+      // W); the next task's loads are in flight while one computes
+      const int G1 = has_diag ? G - 1 : G, me = has_diag ? cta - 1 : cta, off = has_diag ? 1 : 0;
+      const int t0 = (int)((long long)ntile * me / G1), t1 = (int)((long long)ntile * (me + 1) / G1);
+      if (t0 < t1) {
+        Task k = task_of(ph, t0 + off);
+        tile_load(a, ph, k, true, R);
+        load_inv(a, p, s);
+        int lastJ = -1;
+        for (int tt = t0; tt < t1; ++tt) {
+          const bool neww = k.J != lastJ;
+          tile_stage(R, neww, s);
+          double cv[4][2][2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) cv[i][j][h] = R.cv[i][j][h];
+          __syncthreads();
+          Task kn = k;
+          if (tt + 1 < t1) {
+            kn = task_of(ph, tt + 1 + off);
+            tile_load(a, ph, kn, kn.J != k.J, R);
+          }
+          // multipliers of rows below the panel are checked once per row
+          // block, in its first column block
+          tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s);
+          lastJ = k.J;
+          k = kn;
+        }
+      }
+    }
+    GJ_PHASE(0)
+    grid.sync();
+    GJ_PHASE(1)
+  }
+  // the system is now the identity on every panel: b holds x except the
+  // last panel's rows, which are in its row-panel buffer (a single panel
+  // never ran a tile phase: x = D^{-1} b)
+  if (__ldcg(a.info) == 0 && cta == 0) {
+    const int p = npan - 1, k0 = p * kP, kb = N - k0;
+    if (npan > 1) {
+      if (tid < kb) a.b[k0 + tid] = __ldcg(a.wbuf + (size_t)(p & 1) * kP * (N + 1) + (size_t)N * kP + tid);
+    } else {
+      double* sy = s.dg;
+      if (tid < kP) sy[tid] = tid < kb ? __ldcg(a.b + tid) : 0.0;
+      __syncthreads();
+      if (tid < kb) {
+        double v = 0.0;
+        for (int k = 0; k < kb; ++k) v = fma(__ldcg(a.inv + k * kP + tid), sy[k], v);
+        a.b[tid] = v;
+      }
+    }
+  }
+  GJ_PHASE(2)
+#undef GJ_PHASE
+}
+
+int g_sms = 0;
+
+}  // namespace
+
+#ifndef GJ_MICRO
+
+bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const int grid_env = getenv("T2S2_NP_GRID") ? atoi(getenv("T2S2_NP_GRID")) : 0;
+  int grid = sm_budget() > 0 && sm_budget() < g_sms ? sm_budget() : g_sms;
+  if (grid_env > 1 && grid_env < grid) grid = grid_env;
+  if (N < 1 || N > 8192 || grid < 2) return false;
+  const size_t smem = sizeof(Smem);
+  static bool attr = false;
+  if (!attr) {
+    T2S2_CUDA(cudaFuncSetAttribute(gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int npan = (N + kP - 1) / kP;
+  double* inv = allocator().alloc((size_t)npan * kInv);
+  double* wbuf = allocator().alloc((size_t)2 * kP * (N + 1));
+  T2S2_CUDA(cudaMemsetAsync(info_dev, 0, sizeof(int), stream()));
+  static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
+  unsigned long long* pbuf = nullptr;
+  if (prof) {
+    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
+    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
+  }
+  GjArgs a{N, A, b, inv, wbuf, info_dev, pbuf};
+  void* params[] = {&a};
+  {
+    // algorithmic: N^3 (Gauss-Jordan) + 2 N^2; bytes: one read and write of the matrix
+    LaunchScope ls("gj_nopivot", (double)N * N * N + 2.0 * (double)N * N, 16.0 * (double)N * N);
+    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gj_kernel, dim3(grid), dim3(kThr), params, smem,
+                                          stream()));
+  }
+  allocator().release(inv);
+  allocator().release(wbuf);
+  if (prof) {
+    unsigned long long h[16];
+    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
+    T2S2_CUDA(cudaStreamSynchronize(stream()));
+    fprintf(stderr, "gj N=%d cta0: work %.1f sync %.1f final %.1f top %.1f (diag %.1f) | cta1: work %.1f sync %.1f final %.1f top %.1f us\n",
+            N, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[9] / 1e3, h[4] / 1e3, h[5] / 1e3,
+            h[6] / 1e3, h[7] / 1e3);
+    allocator().release(reinterpret_cast<double*>(pbuf));
+  }
+  return true;
+}
+
+#endif  // GJ_MICRO
+
+}  // namespace t2s2

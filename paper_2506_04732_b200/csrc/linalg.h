@@ -35,5 +35,9 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev);
 // sets *info_dev = -1 and leaves A, b clobbered: rebuild and use the
 // pivoting kernel.  Returns false when not applicable (nothing launched).
 bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev);
+// The same contract by blocked Gauss-Jordan (gj_solve.cu): one grid barrier
+// per 32-column panel, no back-substitution chain.  lu_solve_nopivot
+// dispatches to it (T2S2_NP_OLD=1 keeps the LU kernel for comparison).
+bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev);
 
 }  // namespace t2s2

@@ -1048,6 +1048,8 @@ int g_num_sms = 0;
 }  // namespace
 
 bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev) {
+  static const bool old = getenv("T2S2_NP_OLD") != nullptr;
+  if (!old && !getenv("T2S2_LU_PIVOT_ONLY") && gj_solve_nopivot(N, A, b, info_dev)) return true;
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

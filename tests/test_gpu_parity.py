@@ -222,7 +222,7 @@ def test_dense_local_solve_without_interchanges(pk, n):
     _native.stats_reset()
     x = _native.dense_solve(a, b)
     st = _native.stats_read()
-    assert st["lu_nopivot"]["launches"] == 1
+    assert st["gj_nopivot"]["launches"] == 1
     assert st.get("lu_fused", {}).get("launches", 0) == 0
     want = np.linalg.solve(a, b)
     assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
@@ -244,7 +244,7 @@ def test_dense_local_solve_late_interchange(pk):
     _native.stats_reset()
     x = _native.dense_solve(a, b)
     st = _native.stats_read()
-    assert st["lu_nopivot"]["launches"] == 1 and st["lu_fused"]["launches"] == 1
+    assert st["gj_nopivot"]["launches"] == 1 and st["lu_fused"]["launches"] == 1
     want = np.linalg.solve(a, b)
     assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
 

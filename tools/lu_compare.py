@@ -26,8 +26,9 @@ for n in sizes:
     for _ in range(reps):
         x = _native.dense_solve(a, b)
     st = _native.stats_read()
-    fam = "lu_nopivot" if st.get("lu_nopivot", {}).get("launches", 0) and not st.get("lu_fused", {}).get("launches", 0) else "lu_fused"
-    lu_ms = sum(v["device_ms"] for k, v in st.items() if k.startswith("lu_")) / reps
+    fams = [k for k in ("gj_nopivot", "lu_nopivot", "lu_fused") if st.get(k, {}).get("launches", 0)]
+    fam = "+".join(fams)
+    lu_ms = sum(st[k]["device_ms"] for k in fams) / reps
     err = np.linalg.norm(a @ x - b) / np.linalg.norm(b)
     line = f"N={n:5d} {fam} {lu_ms * 1e3:8.1f} us  resid {err:.1e}"
     try:
