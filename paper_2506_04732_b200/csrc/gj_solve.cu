@@ -142,7 +142,9 @@ struct Smem {
   double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
   double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
   double za[kP * kLdP], xb[kP * kLdP];  // U^{-1}, L^{-1} as DMMA operands (gj_diag)
-  double rowd[2][kP], rowx[2][kP], cold[2][kP], colz[2][kP], rinv[kP];  // gj_diag broadcasts
+  alignas(32) double rowd[2][kP];  // gj_diag broadcasts (double buffered)
+  alignas(32) double rowx[2][kP];
+  double cold[2][kP], colz[2][kP], rinv[kP];
 };
 
 // Load D^{-1}, U^{-1} of panel p into shared memory.
@@ -318,7 +320,7 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 }
 
 // Factor the kb x kb block in s.dg (no interchanges, multipliers checked)
-// and publish L^{-1}, U^{-1} (zero padded to 32 x 32) for panel p.
+// and publish D^{-1} and U^{-1} (zero padded to 32 x 32) for panel p.
 //
 // One right-looking loop of 32 steps, one CTA barrier each.  Thread
 // (row i = lane, column group g = warp) keeps four columns of three
@@ -330,101 +332,107 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 //      row st of U is final, then Z[:, j>st] -= Y[:, st] U[st, j].
 // Step st needs row st of D and X and column st of D and Z, which their
 // owners publish (double buffered) before the barrier that ends step
-// st - 1; the owner of u_{st+1,st+1} also publishes its reciprocal.
-// Rolled over the steps: this runs once per panel between tile phases,
-// so it must stay small in the instruction cache.
+// st - 1; the owner of u_{st+1,st+1} also publishes its reciprocal.  Each
+// step issues all its shared-memory loads first, updates branch-free and
+// stores last.  Rolled over the steps: this runs once per panel between
+// tile phases, so it must stay small in the instruction cache.  Then
+// D^{-1} = U^{-1} L^{-1} by DMMA.
+//
+// Measured (tools/micro/gj_bench.cu): ~750 cycles per step, ~25k cycles per
+// block.  A shared-memory round trip through a CTA barrier costs ~200
+// cycles on B200 and the reciprocal ~80 more; a blocked variant (8 x 8
+// register leaves, panel and trailing updates between barriers) and
+// single-warp variants (shared-memory rows, shuffled register rows) were
+// all measured slower or no faster.
 #ifdef GJ_MICRO
 __device__ long long g_diag_t[8];
 #define GJ_T(k) if (threadIdx.x == 0) g_diag_t[k] = clock64();
-#define GJ_TS(k) if (threadIdx.x == 75 && st == 10) g_diag_t[k] = clock64();
 #else
 #define GJ_T(k)
-#define GJ_TS(k)
 #endif
+
 __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
-  const int tid = threadIdx.x, i = tid & 31, g = tid >> 5;
+  const int tid = threadIdx.x, i = tid & 31, g = tid >> 5, j0 = 4 * g;
   __syncthreads();
   GJ_T(0)
   double dv[4], xv[4], zv[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int j = 4 * g + q;
+    const int j = j0 + q;
     dv[q] = (i < kb && j < kb) ? s.dg[j * 33 + i] : (i == j ? 1.0 : 0.0);
     xv[q] = i == j ? 1.0 : 0.0;
     zv[q] = xv[q];
   }
-  bool bad = false;
+  bool ok = true;
   // publish step 0's row, column and reciprocal pivot
-  if (i == 0)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      s.rowd[0][4 * g + q] = dv[q];
-      s.rowx[0][4 * g + q] = xv[q];
-    }
+  if (i == 0) {
+    *reinterpret_cast<double4*>(&s.rowd[0][j0]) = make_double4(dv[0], dv[1], dv[2], dv[3]);
+    *reinterpret_cast<double4*>(&s.rowx[0][j0]) = make_double4(xv[0], xv[1], xv[2], xv[3]);
+  }
   if (g == 0) {
     s.cold[0][i] = dv[0];
     s.colz[0][i] = zv[0];
     if (i == 0) {
       s.rinv[0] = 1.0 / dv[0];
-      if (!(fabs(dv[0]) > 0.0) || !isfinite(dv[0])) bad = true;
+      ok = fabs(dv[0]) > 0.0 && isfinite(dv[0]);
     }
   }
   __syncthreads();
 #pragma unroll 1
   for (int st = 0; st < kP; ++st) {
-    GJ_TS(3)
-    const int par = st & 1;
-    const double rinv = s.rinv[st];
-    const double l = i > st ? s.cold[par][i] * rinv : 0.0;  // multiplier l_{i,st}
-    const double y = i <= st ? s.colz[par][i] * rinv : 0.0; // (U^{-1})_{i,st}
-    if (g == 0 && !(fabs(l) <= 1.0)) bad = true;
+    const int par = st & 1, nx = st + 1;
+    // loads
+    const double rinv = s.rinv[st], cd = s.cold[par][i], cz = s.colz[par][i];
+    const double4 u4 = *reinterpret_cast<const double4*>(&s.rowd[par][j0]);
+    const double4 x4 = *reinterpret_cast<const double4*>(&s.rowx[par][j0]);
+    const double ur[4] = {u4.x, u4.y, u4.z, u4.w}, xr[4] = {x4.x, x4.y, x4.z, x4.w};
+    // multiplier l_{i,st} and (U^{-1})_{i,st}
+    const double l = i > st ? cd * rinv : 0.0;
+    const double y = i <= st ? cz * rinv : 0.0;
+    ok = ok && fabs(l) <= 1.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int j = 4 * g + q;
-      const double ur = s.rowd[par][j], xr = s.rowx[par][j];
-      if (j > st) {
-        dv[q] = fma(-l, ur, dv[q]);
-        zv[q] = fma(-y, ur, zv[q]);
-      } else {
-        xv[q] = fma(-l, xr, xv[q]);
-        if (j == st && i <= st) zv[q] = y;
+      const int j = j0 + q;
+      const bool ahead = j > st;
+      dv[q] = fma(ahead ? -l : 0.0, ur[q], dv[q]);
+      zv[q] = fma(ahead ? -y : 0.0, ur[q], zv[q]);
+      xv[q] = fma(ahead ? 0.0 : -l, xr[q], xv[q]);
+      zv[q] = (j == st && i <= st) ? y : zv[q];
+    }
+    // stores for step nx
+    if (nx < kP) {
+      const int qn = nx - j0;  // in [0, 4) for the owner warp
+      if (qn >= 0 && qn < 4) {
+        const double dc = qn == 0 ? dv[0] : qn == 1 ? dv[1] : qn == 2 ? dv[2] : dv[3];
+        const double zc = qn == 0 ? zv[0] : qn == 1 ? zv[1] : qn == 2 ? zv[2] : zv[3];
+        if (i == nx) {
+          s.rinv[nx] = 1.0 / dc;
+          ok = ok && fabs(dc) > 0.0 && isfinite(dc);
+        }
+        s.cold[par ^ 1][i] = dc;
+        s.colz[par ^ 1][i] = zc;
+      }
+      if (i == nx) {
+        *reinterpret_cast<double4*>(&s.rowd[par ^ 1][j0]) = make_double4(dv[0], dv[1], dv[2], dv[3]);
+        *reinterpret_cast<double4*>(&s.rowx[par ^ 1][j0]) = make_double4(xv[0], xv[1], xv[2], xv[3]);
       }
     }
-    GJ_TS(4)
-    const int nx = st + 1;
-    if (nx < kP) {
-      if (i == nx)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          s.rowd[par ^ 1][4 * g + q] = dv[q];
-          s.rowx[par ^ 1][4 * g + q] = xv[q];
-        }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (4 * g + q == nx) {
-          s.cold[par ^ 1][i] = dv[q];
-          s.colz[par ^ 1][i] = zv[q];
-          if (i == nx) {
-            s.rinv[nx] = 1.0 / dv[q];
-            if (!(fabs(dv[q]) > 0.0) || !isfinite(dv[q])) bad = true;
-          }
-        }
-    }
-    GJ_TS(5)
     __syncthreads();
-    GJ_TS(6)
   }
   GJ_T(1)
-  if (bad) gj_fail(a);
+  if (!ok) gj_fail(a);
   // D^{-1} = U^{-1} L^{-1} (DMMA, 32 x 32 x 32); publish D^{-1} and U^{-1}
   // zero padded outside kb x kb
+  double* gl = a.inv + (size_t)p * kInv;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    s.za[(4 * g + q) * kLdP + i] = zv[q];  // A operand [k][m] = Z[m][k]
-    s.xb[(4 * g + q) * kLdP + i] = xv[q];  // B operand [n][k] = X[k][n]
+    const int j = j0 + q;
+    s.za[j * kLdP + i] = zv[q];  // A operand [k][m] = Z[m][k]
+    s.xb[j * kLdP + i] = xv[q];  // B operand [n][k] = X[k][n]
+    gl[kP * kP + j * kP + i] = (i < kb && j < kb) ? zv[q] : 0.0;
   }
   __syncthreads();
-  double* gl = a.inv + (size_t)p * kInv;
+  GJ_T(2)
   {
     const int lane = i, warp = g, m0 = (warp >> 1) * 8, n0 = (warp & 1) * 16;
     double acc[2][2] = {};
@@ -444,12 +452,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
         gl[cc * kP + rr] = (rr < kb && cc < kb) ? acc[j][h] : 0.0;
       }
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = 4 * g + q;
-    gl[kP * kP + j * kP + i] = (i < kb && j < kb) ? zv[q] : 0.0;
-  }
-  GJ_T(2)
+  GJ_T(3)
   __syncthreads();  // (the grid barrier that follows publishes the stores)
 }
 
@@ -483,7 +486,8 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     const Phase ph(N, p);
     const bool has_diag = ph.kb2 > 0;
     const int ntile = ph.nrb * ph.ncb - (has_diag ? 1 : 0);
-    if (has_diag && cta == 0) {
+    const bool special = has_diag && cta == 0;
+    if (special) {
       // the next diagonal block: W of its columns, multipliers checked,
       // updated block kept in shared memory, then factored
       const Task k = task_of(ph, 0);
@@ -495,10 +499,13 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       unsigned long long td = pr ? gtimer() : 0;
       gj_diag(a, p + 1, ph.kb2, s);
       if (pr) a.prof[9] += gtimer() - td;
-    } else {
+    }
+    if (!special || G == 1) {
       // a contiguous chunk of the J-major task list (consecutive tasks share
-      // W); the next task's loads are in flight while one computes
-      const int G1 = has_diag ? G - 1 : G, me = has_diag ? cta - 1 : cta, off = has_diag ? 1 : 0;
+      // W); the next task's loads are in flight while one computes.  A
+      // one-CTA launch (small N) does all of it after the diagonal block.
+      const bool sep = has_diag && G > 1;
+      const int G1 = sep ? G - 1 : G, me = sep ? cta - 1 : cta, off = has_diag ? 1 : 0;
       const int t0 = (int)((long long)ntile * me / G1), t1 = (int)((long long)ntile * (me + 1) / G1);
       if (t0 < t1) {
         Task k = task_of(ph, t0 + off);
@@ -569,8 +576,19 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   }
   static const int grid_env = getenv("T2S2_NP_GRID") ? atoi(getenv("T2S2_NP_GRID")) : 0;
   int grid = sm_budget() > 0 && sm_budget() < g_sms ? sm_budget() : g_sms;
-  if (grid_env > 1 && grid_env < grid) grid = grid_env;
-  if (N < 1 || N > 8192 || grid < 2) return false;
+  if (grid_env > 0 && grid_env < grid) grid = grid_env;
+  if (N < 1 || N > 8192) return false;
+  // no more CTAs than the first (largest) phase has tile tasks: a smaller
+  // grid makes every grid barrier cheaper; tiny systems run on one CTA
+  {
+    const int kb2 = N - kP < kP ? N - kP : kP, rest = N - kP - kb2;
+    const int nrb = (kb2 > 0 ? 1 : 0) + (rest > 0 ? (rest + kT - 1) / kT : 0);
+    const int crest = N + 1 - kP - kb2;
+    const int ncb = (kb2 > 0 ? 1 : 0) + (crest + kT - 1) / kT;
+    const int tasks = nrb * ncb;  // including the diagonal block's
+    const int want = tasks <= 3 ? 1 : tasks;
+    if (want < grid) grid = want;
+  }
   const size_t smem = sizeof(Smem);
   static bool attr = false;
   if (!attr) {

@@ -101,7 +101,7 @@ int main() {
     printf("diag_parts: gj_diag %lld cycles, 32 bare barriers %lld\n", hh[0], hh[1]);
     long long dt[8];
     cudaMemcpyFromSymbol(dt, g_diag_t, sizeof(dt));
-    printf("   loop %lld, dinv+store %lld | step10 owner: compute %lld publish %lld barrier %lld\n", dt[1] - dt[0], dt[2] - dt[1], dt[4]-dt[3], dt[5]-dt[4], dt[6]-dt[5]);
+    printf("   lu %lld inverses %lld dinv+store %lld\n", dt[1]-dt[0], dt[2]-dt[1], dt[3]-dt[2]);
   }
   for (int it = 0; it < 2; ++it) {
     diag_loop<<<1, kThr, smem>>>(a, 100, cyc);
