@@ -6,6 +6,7 @@
 // Householder step needs two CTA barriers and a Jacobi round one.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "blas.h"
 #include "linalg.h"
@@ -14,6 +15,13 @@ namespace t2s2 {
 namespace {
 
 constexpr int kQrThreads = 512;
+#ifdef SVD_MICRO
+__device__ long long g_svd_t[8];
+__device__ int g_svd_sweeps;
+#define SVD_T(k) if (threadIdx.x == 0) g_svd_t[k] = clock64();
+#else
+#define SVD_T(k)
+#endif
 
 // Threads for a one-CTA factorisation whose column step keeps at most
 // `busy` warps working: fewer warps make each CTA barrier cheaper.
@@ -291,6 +299,9 @@ __device__ void jacobi_sweeps(int p, int q, double* G, double* V) {
       __syncthreads();
     }
     __syncthreads();
+#ifdef SVD_MICRO
+    if (threadIdx.x == 0) g_svd_sweeps = sweep + 1;
+#endif
     if (!sh_rot) break;
     __syncthreads();
   }
@@ -379,13 +390,16 @@ __global__ void __launch_bounds__(kQrThreads)
       W[(size_t)j * mp + i] = A[e];
   }
   __syncthreads();
+  SVD_T(0)
   qr_factor(mp, np, W, tau);
   for (int e = tid; e < np * np; e += blockDim.x) {
     const int c = e / np, i = e - c * np;
     G[e] = i <= c ? W[(size_t)c * mp + i] : 0.0;
   }
   __syncthreads();
+  SVD_T(1)
   jacobi_sweeps(np, np, G, V);
+  SVD_T(2)
   jacobi_sort(np, np, G, perm, ss, sv);
   for (int e = tid; e < np * np; e += blockDim.x) {
     const int k = e / np, j = e - k * np;
@@ -393,7 +407,9 @@ __global__ void __launch_bounds__(kQrThreads)
     Ur[e] = sj > 0.0 ? G[(size_t)perm[j] * np + k] / sj : 0.0;
   }
   for (int j = tid; j < np; j += blockDim.x) s[j] = ss[j];
+  SVD_T(3)
   qr_form_q(mp, np, W, tau);  // begins with a barrier
+  SVD_T(4)
   // U' = Q Ur (mp x np), V' = V[:, perm]
   if (!tr) {
     for (int e = tid; e < m * n; e += blockDim.x) {
@@ -419,6 +435,257 @@ __global__ void __launch_bounds__(kQrThreads)
       Vt[e] = acc;
     }
   }
+}
+
+// Thin SVD of a small row-major m x n matrix, np = min(m, n) <= 16 columns of
+// A' (A, or A^T when m < n) and mp = max(m, n) <= 32 * RPL rows: the same
+// algorithm as svd_small_kernel (Householder QR A' = Q R, one-sided Jacobi
+// on R with circle ordering, U' = Q G/s, V' = accumulated rotations), with
+// warp-level parallelism instead of CTA barriers per step:
+//   QR     warp c holds column c of A' in registers (RPL rows per lane); the
+//          owner of column j forms its reflector (LAPACK dgeqrf
+//          conventions) and publishes it in shared memory, ONE CTA barrier,
+//          every later column's warp applies it (warp reduction + axpy);
+//   Jacobi in ONE warp, lane c holding column c of R and of V: a round's
+//          disjoint pairs (partner lane (2 rnd - c) mod (qe - 1)) exchange
+//          columns by shuffles and both lanes of a pair form the same
+//          rotation locally — no reductions, no barriers; a sweep ends with
+//          a warp vote;
+//   Q      each warp applies H_c ... H_0 to its own unit column (no
+//          barriers); U' = Q Ur through shared memory.
+template <int RPL, int NPX>
+__global__ void __launch_bounds__(512)
+    svd_warp_kernel(int m, int n, const double* __restrict__ A, double* U, double* s, double* Vt) {
+  extern __shared__ double wsm[];
+  const bool tr = m < n;
+  const int mp = tr ? n : m, np = tr ? m : n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* vb = wsm;                      // reflectors, column j at vb[j*mp], v_j = 1 implicit
+  double* Rs = vb + (size_t)mp * np;     // R column-major np x np
+  double* tau = Rs + np * np;            // np
+  double* Ur = tau + np;                 // np x np: Ur[k*np + j] = G[k][perm j] / s_j
+  double* Vs = Ur + np * np;             // V' sorted: Vs[j*np + i] = V[i][perm j]
+  double* ssv = Vs + np * np;            // np singular values (sorted)
+  double* Qs = ssv + np;                 // Q column-major mp x np
+  SVD_T(0)
+  double a[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    a[r] = 0.0;
+    if (warp < np && i < mp) a[r] = tr ? A[(size_t)warp * n + i] : A[(size_t)i * n + warp];
+  }
+  // --- Householder QR, one barrier per column
+  for (int j = 0; j < np; ++j) {
+    if (warp == j) {
+      double ss = 0.0, alpha = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > j && i < mp) ss = fma(a[r], a[r], ss);
+        if (i == j) alpha = a[r];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      alpha = __shfl_sync(0xffffffffu, alpha, j & 31);
+      double t, sc, beta;
+      if (ss == 0.0) {
+        t = 0.0;
+        sc = 1.0;
+        beta = alpha;
+      } else {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i < mp) {
+          if (i < j) Rs[j * np + i] = a[r];
+          if (i == j) Rs[j * np + i] = beta;
+          vb[(size_t)j * mp + i] = i > j ? a[r] * sc : (i == j ? 1.0 : 0.0);
+        }
+      }
+      if (lane == 0) tau[j] = t;
+    }
+    __syncthreads();
+    if (warp > j && warp < np) {
+      const double t = tau[j];
+      if (t != 0.0) {
+        const double* v = vb + (size_t)j * mp;
+        double w = 0.0, vv[RPL];
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          vv[r] = (i >= j && i < mp) ? v[i] : 0.0;
+          w = fma(vv[r], a[r], w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        const double tw = t * w;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) a[r] = fma(-tw, vv[r], a[r]);
+      }
+    }
+  }
+  SVD_T(1)
+  // --- one-sided Jacobi on R in warp 0: lane c = column c of R and of V
+  if (warp == 0) {
+    const int c = lane;
+    double g[NPX], v[NPX];
+#pragma unroll
+    for (int i = 0; i < NPX; ++i) {
+      g[i] = (c < np && i < np && i <= c) ? Rs[c * np + i] : 0.0;
+      v[i] = (i == c && c < np) ? 1.0 : 0.0;
+    }
+    const double tol = DBL_EPSILON * sqrt((double)np), tol2 = tol * tol;
+    const int qe = np + (np & 1);
+    for (int sweep = 0; sweep < 60 && np > 1; ++sweep) {
+      bool rot = false;
+      for (int rnd = 0; rnd < qe - 1; ++rnd) {
+        int pt;
+        if (c == qe - 1)
+          pt = rnd;
+        else if (c == rnd)
+          pt = qe - 1;
+        else {
+          pt = 2 * rnd - c;
+          if (pt < 0) pt += qe - 1;
+          if (pt >= qe - 1) pt -= qe - 1;
+        }
+        if (c >= qe) pt = c;
+        double pg[NPX];
+#pragma unroll
+        for (int i = 0; i < NPX; ++i) pg[i] = __shfl_sync(0xffffffffu, g[i], pt);
+        const bool isa = c < pt;
+        bool doit = false;
+        double cs = 1.0, ssn = 0.0;  // own' = cs own + ssn partner
+        if (c < np && pt < np && pt != c) {
+          double o2 = 0.0, p2 = 0.0, op = 0.0;
+#pragma unroll
+          for (int i = 0; i < NPX; ++i) {
+            o2 = fma(g[i], g[i], o2);
+            p2 = fma(pg[i], pg[i], p2);
+            op = fma(g[i], pg[i], op);
+          }
+          const double al = isa ? o2 : p2, be = isa ? p2 : o2, gab = op;
+          if (!(gab == 0.0 || al == 0.0 || be == 0.0) && !(gab * gab <= tol2 * al * be)) {
+            // the rotation of svd_small_kernel (column a: c x - s y, column b:
+            // s x + c y) with t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+            // zeta = (be - al) / (2 gab), rewritten without forming zeta:
+            // t = sign(e) d / (|e| + sqrt(e^2 + d^2)), e = be - al, d = 2 gab
+            const double e = be - al, d = 2.0 * gab;
+            const double t = (e >= 0.0 ? d : -d) / (fabs(e) + sqrt(fma(e, e, d * d)));
+            cs = rsqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+            ssn = isa ? -sn : sn;
+            doit = true;
+            rot = true;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NPX; ++i) {
+          const double pvi = __shfl_sync(0xffffffffu, v[i], pt);
+          g[i] = doit ? fma(ssn, pg[i], cs * g[i]) : g[i];
+          v[i] = doit ? fma(ssn, pvi, cs * v[i]) : v[i];
+        }
+      }
+#ifdef SVD_MICRO
+      if (lane == 0) g_svd_sweeps = sweep + 1;
+#endif
+      if (!__any_sync(0xffffffffu, rot)) break;
+    }
+    // singular values sorted descending (stable), Ur = G[:, perm] / s, V' = V[:, perm]
+    double nrm = 0.0;
+#pragma unroll
+    for (int i = 0; i < NPX; ++i) nrm = fma(g[i], g[i], nrm);
+    nrm = sqrt(nrm);
+    int rank = 0;
+    for (int o = 0; o < np; ++o) {
+      const double so = __shfl_sync(0xffffffffu, nrm, o);
+      rank += (so > nrm) || (so == nrm && o < c);
+    }
+    if (c < np) {
+      ssv[rank] = nrm;
+#pragma unroll
+      for (int i = 0; i < NPX; ++i)
+        if (i < np) {
+          Ur[i * np + rank] = nrm > 0.0 ? g[i] / nrm : 0.0;
+          Vs[rank * np + i] = v[i];
+        }
+    }
+  }
+  SVD_T(2)
+  // --- Q = H_0 ... H_{k-1} [I; 0], warp c forms column c on its own
+  if (warp < np) {
+    double q[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) q[r] = (lane + 32 * r == warp) ? 1.0 : 0.0;
+    for (int j = warp; j >= 0; --j) {  // H_j leaves e_c unchanged for j > c
+      const double t = tau[j];
+      if (t == 0.0) continue;
+      const double* v = vb + (size_t)j * mp;
+      double w = 0.0, vv[RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        vv[r] = (i >= j && i < mp) ? v[i] : 0.0;
+        w = fma(vv[r], q[r], w);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      const double tw = t * w;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) q[r] = fma(-tw, vv[r], q[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < mp) Qs[(size_t)warp * mp + i] = q[r];
+    }
+  }
+  __syncthreads();
+  SVD_T(3)
+  for (int j = tid; j < np; j += blockDim.x) s[j] = ssv[j];
+  // U' = Q Ur (mp x np); V' = V[:, perm]
+  if (!tr) {
+    for (int e = tid; e < m * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      double acc = 0.0;
+      for (int k = 0; k < np; ++k) acc = fma(Qs[(size_t)k * mp + i], Ur[k * np + j], acc);
+      U[e] = acc;
+    }
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int j = e / n, i = e - j * n;
+      Vt[e] = Vs[j * np + i];
+    }
+  } else {
+    // A = V' S U'^T: U (m x m) = V'[:, perm], Vt (m x n) = U'^T
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = e / m, j = e - i * m;
+      U[e] = Vs[j * np + i];
+    }
+    for (int e = tid; e < m * n; e += blockDim.x) {
+      const int j = e / n, cc = e - j * n;
+      double acc = 0.0;
+      for (int k = 0; k < np; ++k) acc = fma(Qs[(size_t)k * mp + cc], Ur[k * np + j], acc);
+      Vt[e] = acc;
+    }
+  }
+}
+
+template <int RPL, int NPX>
+void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double* Vt, size_t smem,
+                     int thr) {
+  static bool attr = false;  // one flag per instantiation
+  if (!attr) {
+    T2S2_CUDA(cudaFuncSetAttribute(svd_warp_kernel<RPL, NPX>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+    attr = true;
+  }
+  svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt);
 }
 
 }  // namespace
@@ -536,6 +803,32 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
   {
     const int mp = m >= n ? m : n, np = m >= n ? n : m;
+    static const bool old_svd = getenv("T2S2_SVD_OLD") != nullptr;
+    // warp-level kernel: np <= 16 columns, mp <= 384 rows
+    const size_t wneed = (2 * (size_t)mp * np + 3 * (size_t)np * np + 2 * (size_t)np) * sizeof(double);
+    if (!old_svd && np <= 16 && mp <= 384 && wneed <= kSmemCap) {
+      U = m >= n ? DTensor({m, n}) : DTensor({m, m});
+      s = DTensor({np});
+      Vt = m >= n ? DTensor({n, n}) : DTensor({m, n});
+      {
+        LaunchScope ls("svd_jacobi", 4.0 * mp * (double)np * np, 8.0 * m * (double)n);
+        const int thr = 32 * (np < 2 ? 2 : np);
+        const int rpl = (mp + 31) / 32;
+#define T2S2_SVDW(NPX)                                                            \
+  do {                                                                            \
+    if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);   \
+    else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr); \
+    else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);           \
+  } while (0)
+        if (np <= 4) T2S2_SVDW(4);
+        else if (np <= 8) T2S2_SVDW(8);
+        else if (np <= 12) T2S2_SVDW(12);
+        else T2S2_SVDW(16);
+#undef T2S2_SVDW
+      }
+      T2S2_CHECK_LAUNCH();
+      return;
+    }
     const size_t need = ((size_t)mp * np + 3 * (size_t)np * np + 4 * (size_t)np) * sizeof(double);
     if (need <= kSmemCap && np <= 64) {
       static bool attr = false;

@@ -29,6 +29,9 @@ __global__ void k(double* dout, long long* cyc, int nthr) {
     else if (M == 6) { __syncthreads(); }
     else if (M == 7) dmma(d, e, d, f);
     else if (M == 8) { dmma(d, e, f, f); }
+    else if (M == 9) d = sqrt(d) + 1.0;
+    else if (M == 10) d = rsqrt(d) + 1.0;
+    else if (M == 11) { int x = (int)d; d = (double)((x * 7 + 3) % 13) + 1.0; }
   }
   }
   long long t1 = clock64();
@@ -57,5 +60,8 @@ int main() {
   run<8>("dmma acc chain (8 warps)", 256, 256);
   run<8>("dmma acc chain (16 warps)", 512, 512);
   run<0>("dfma dep (32 warps)", 1024, 1024);
+  run<9>("sqrt dependent", 32, 32);
+  run<10>("rsqrt dependent", 32, 32);
+  run<11>("int mod + cvt dependent", 32, 32);
   return 0;
 }
