@@ -688,10 +688,242 @@ void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double
   svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt);
 }
 
+// Householder QR of a tall block (m rows <= 32 * RPL, n <= 32 * CPW columns,
+// m >= n) with warp-level parallelism: warp w holds columns w, w + nw, ...
+// (CPW of them) in registers, RPL rows per lane.  Column j's owner forms
+// its reflector (LAPACK dgeqrf conventions), publishes it in shared memory,
+// ONE CTA barrier, and every owner of later columns applies it (warp
+// reduction + axpy).  Mode Q: thin Q (each warp forms its own columns of
+// H_0 ... H_{n-1} [I; 0], no barriers) and R; mode R (TSQR leaf): CTA b
+// factors rows [b*chunk, b*chunk + rows) and writes its n x n R at rows
+// [b*n, (b+1)*n) of the output.  A, Q column-major when cm, else row-major.
+template <int RPL, int CPW, bool WANTQ>
+__global__ void __launch_bounds__(512)
+    wqr_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Q, double* R, int cm) {
+  extern __shared__ double qsm2[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int r0 = blockIdx.x * chunk;
+  const int mr = m - r0 < chunk ? m - r0 : chunk;  // rows of this block (>= n, or the whole matrix)
+  const int k = mr < n ? mr : n;
+  double* vb = qsm2;                  // reflectors, column j at vb[j*mr]
+  double* Rs = vb + (size_t)mr * n;   // R column-major n x n
+  double* tau = Rs + (size_t)n * n;   // n
+  double a[CPW][RPL];
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int c = warp + q * nw;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      a[q][r] = (c < n && i < mr) ? (cm ? A[(size_t)c * m + r0 + i] : A[(size_t)(r0 + i) * n + c]) : 0.0;
+    }
+  }
+  for (int j = 0; j < k; ++j) {
+    const int ow = j % nw, oq = j / nw;
+    if (warp == ow) {
+      double ss = 0.0, alpha = 0.0;
+#pragma unroll
+      for (int q = 0; q < CPW; ++q)
+        if (q == oq)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i > j && i < mr) ss = fma(a[q][r], a[q][r], ss);
+            if (i == j) alpha = a[q][r];
+          }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      alpha = __shfl_sync(0xffffffffu, alpha, j & 31);
+      double t, sc, beta;
+      if (ss == 0.0) {
+        t = 0.0;
+        sc = 1.0;
+        beta = alpha;
+      } else {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+#pragma unroll
+      for (int q = 0; q < CPW; ++q)
+        if (q == oq)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i < mr) {
+              if (i < j) Rs[(size_t)j * n + i] = a[q][r];
+              if (i == j) Rs[(size_t)j * n + i] = beta;
+              vb[(size_t)j * mr + i] = i > j ? a[q][r] * sc : (i == j ? 1.0 : 0.0);
+            }
+          }
+      if (lane == 0) tau[j] = t;
+    }
+    __syncthreads();
+    const double t = tau[j];
+    if (t != 0.0) {
+      const double* v = vb + (size_t)j * mr;
+      double vv[RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        vv[r] = (i >= j && i < mr) ? v[i] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) {
+        const int c = warp + q * nw;
+        if (c > j && c < n) {
+          double w = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) w = fma(vv[r], a[q][r], w);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+          const double tw = t * w;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) a[q][r] = fma(-tw, vv[r], a[q][r]);
+        }
+      }
+    }
+  }
+  // columns j >= k (wide leaf, mr < n): their R rows < k are the updated values
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int c = warp + q * nw;
+    if (c >= k && c < n)
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i < k) Rs[(size_t)c * n + i] = a[q][r];
+      }
+  }
+  __syncthreads();
+  if (!WANTQ) {
+    double* Rb = R + (size_t)blockIdx.x * n * n;  // n x n row-major, zero padded
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int rr = e / n, cc = e - rr * n;
+      Rb[e] = (rr < k && cc >= rr) ? Rs[(size_t)cc * n + rr] : 0.0;
+    }
+    return;
+  }
+  for (int e = tid; e < k * n; e += blockDim.x) {
+    const int rr = e / n, cc = e - rr * n;
+    R[e] = cc >= rr ? Rs[(size_t)cc * n + rr] : 0.0;
+  }
+  // thin Q: warp forms its own columns c < k
+#pragma unroll
+  for (int q = 0; q < CPW; ++q) {
+    const int c = warp + q * nw;
+    if (c >= k) continue;
+    double x[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) x[r] = (lane + 32 * r == c) ? 1.0 : 0.0;
+    for (int j = c; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double* v = vb + (size_t)j * mr;
+      double w = 0.0, vv[RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        vv[r] = (i >= j && i < mr) ? v[i] : 0.0;
+        w = fma(vv[r], x[r], w);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      const double tw = tj * w;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) x[r] = fma(-tw, vv[r], x[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < mr) {
+        if (cm)
+          Q[(size_t)c * m + i] = x[r];
+        else
+          Q[(size_t)i * k + c] = x[r];
+      }
+    }
+  }
+}
+
+template <int RPL, int CPW, bool WANTQ>
+void launch_wqr(int blocks, int thr, size_t smem, int m, int n, int chunk, const double* A, double* Q,
+                double* R, int cm) {
+  static bool attr = false;  // one flag per instantiation
+  if (!attr) {
+    T2S2_CUDA(cudaFuncSetAttribute(wqr_kernel<RPL, CPW, WANTQ>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
+    attr = true;
+  }
+  wqr_kernel<RPL, CPW, WANTQ><<<blocks, thr, smem, stream()>>>(m, n, chunk, A, Q, R, cm);
+}
+
+// Dispatch: at most 16 warps, CPW = ceil(n / 16) columns each (1, 2 or 4);
+// rows per block <= 384 (<= 256 with four columns per warp, registers);
+// false if not applicable.
+template <bool WANTQ>
+bool wqr(int blocks, int m, int n, int chunk, const double* A, double* Q, double* R, int cm) {
+  const int rows = chunk < m ? chunk : m;
+  const int cpw = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
+  if (n < 1 || n > 64 || rows > (cpw == 4 ? 256 : 384)) return false;
+  const int rpl = (rows + 31) / 32;
+  const int nw = (n + cpw - 1) / cpw;
+  const int thr = 32 * (nw < 2 ? 2 : nw);
+  const size_t smem = ((size_t)rows * n + (size_t)n * n + n) * sizeof(double);
+  if (smem > kSmemCap) return false;
+#define T2S2_WQR(R_, C_) launch_wqr<R_, C_, WANTQ>(blocks, thr, smem, m, n, chunk, A, Q, R, cm)
+  if (cpw == 1) {
+    if (rpl <= 4) T2S2_WQR(4, 1);
+    else if (rpl <= 8) T2S2_WQR(8, 1);
+    else T2S2_WQR(12, 1);
+  } else if (cpw == 2) {
+    if (rpl <= 4) T2S2_WQR(4, 2);
+    else if (rpl <= 8) T2S2_WQR(8, 2);
+    else T2S2_WQR(12, 2);
+  } else {
+    if (rpl <= 4) T2S2_WQR(4, 4);
+    else T2S2_WQR(8, 4);
+  }
+#undef T2S2_WQR
+  return true;
+}
+
 }  // namespace
 
 void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_r: empty matrix");
+  static const bool old_qr = getenv("T2S2_QR_OLD") != nullptr;
+  if (!old_qr && n <= 64 && m >= n) {
+    // warp-level TSQR: leaves of <= 384 rows (and >= 2n so the stack shrinks)
+    const int k = m < n ? m : n;
+    const int cap = n > 32 ? 256 : 384;  // rows per leaf (see wqr)
+    int chunk = m;
+    if (m > cap) {
+      const int leaves = (m + cap - 1) / cap;
+      chunk = (m + leaves - 1) / leaves;
+      if (chunk < 2 * n) chunk = 2 * n;
+    }
+    const int blocks = ceil_div(m, chunk);
+    if (chunk <= cap && (blocks == 1 || chunk >= 2 * n)) {
+      DTensor stacked({blocks * n, n});
+      bool ok;
+      {
+        LaunchScope ls("qr", 2.0 * m * (double)n * n, 8.0 * m * (double)n);
+        ok = wqr<false>(blocks, m, n, chunk, A, nullptr, stacked.p, cm ? 1 : 0);
+      }
+      if (ok) {
+        T2S2_CHECK_LAUNCH();
+        if (blocks == 1) {
+          R = DTensor({k, n});
+          dcopy(R.p, stacked.p, (size_t)k * n);
+          return;
+        }
+        qr_r(blocks * n, n, stacked.p, R);
+        return;
+      }
+    }
+  }
   // rows per CTA so that the CTA's block fits the shared-memory budget
   int chunk = (int)(kSmemCap / (sizeof(double) * (size_t)n));
   if (chunk > m) chunk = m;
@@ -729,6 +961,18 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
   const int k = m < n ? m : n;
   Q = DTensor({m, k});
   R = DTensor({k, n});
+  static const bool old_qr = getenv("T2S2_QR_OLD") != nullptr;
+  if (!old_qr && m >= n && m <= (n > 32 ? 256 : 384) && n <= 64) {
+    bool ok;
+    {
+      LaunchScope ls("qr", 4.0 * m * (double)n * k, 16.0 * m * (double)n);
+      ok = wqr<true>(1, m, n, m, A, Q.p, R.p, cm ? 1 : 0);
+    }
+    if (ok) {
+      T2S2_CHECK_LAUNCH();
+      return;
+    }
+  }
   double* W = allocator().alloc((size_t)m * n);
   double* Qc = allocator().alloc((size_t)m * k);
   double* tau = allocator().alloc(k);
