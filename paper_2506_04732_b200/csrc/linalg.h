@@ -31,7 +31,8 @@ void lu_solve(int N, const double* LU, const int* ipiv, double* b);
 bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev);
 // Verified no-pivot LU solve (one cooperative launch): when partial pivoting
 // would make no interchange — every multiplier |l| <= 1 — it computes the
-// same factors without a pivot search.  Otherwise (or on a zero pivot) it
+// same factors without a pivot search.  (Dispatches to the block
+// Gauss-Jordan kernel, gj_solve.cu.)  Otherwise (or on a zero pivot) it
 // sets *info_dev = -1 and leaves A, b clobbered: rebuild and use the
 // pivoting kernel.  Returns false when not applicable (nothing launched).
 bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev);
