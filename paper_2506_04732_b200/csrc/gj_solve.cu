@@ -150,9 +150,7 @@ struct Smem {
   double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
   double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
   double za[kP * kLdP], xb[kP * kLdP];  // U^{-1}, L^{-1} as DMMA operands (gj_diag)
-  alignas(32) double rowd[2][kP];  // gj_diag broadcasts (double buffered)
-  alignas(32) double rowx[2][kP];
-  double cold[2][kP], colz[2][kP], rinv[kP];
+  double cold[2][kP], colz[2][kP], rinv[kP];  // gj_diag broadcasts (double buffered)
 };
 
 // Load D^{-1}, U^{-1} of panel p into shared memory.
@@ -327,6 +325,80 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
   __syncthreads();  // s.ab / s.pb / s.ws free
 }
 
+// The next diagonal block (rows and columns [k1, k1 + kb2), kb2 <= 32) on
+// CTA 0 — the head of every panel's critical path — as 32 x 32 products on
+// all eight warps (warp tile 8 x 16) instead of a 64 x 64 tile task:
+//   W = D^{-1} A[p, J0] (published to the row panel), the multipliers
+//   A[I0, p] U^{-1} checked, and A[I0, J0] - A[I0, p] W left in s.dg.
+__device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = ph.k1, m = ph.kb2, k0 = ph.k0, kb = ph.kb;
+  const int m0 = (warp >> 1) * 8, n0 = (warp & 1) * 16;
+  double cv[2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
+      cv[j][h] = (rr < m && cc < m) ? __ldcg(src_ptr(a, ph, r + rr, r + cc)) : 0.0;
+    }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + q * kThr, kk = e >> 5, i = e & 31;  // A[I0, p]: (i, kk)
+    s.ab[kk * kLdT + i] = (i < m && kk < kb) ? __ldcg(src_ptr(a, ph, r + i, k0 + kk)) : 0.0;
+    const int j = e >> 5, k = e & 31;  // A[p, J0]: (k, j)
+    s.pb[j * kLdP + k] = (k < kb && j < m) ? __ldcg(dst_ptr(a, k0 + k, r + j)) : 0.0;
+  }
+  load_inv(a, ph.p, s);
+  __syncthreads();
+  {
+    double aw[2][2] = {}, am[2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      const double fw = s.di[kr * kLdP + m0 + (lane >> 2)];  // D^{-1}[row][kr]
+      const double fm = s.ab[kr * kLdT + m0 + (lane >> 2)];  // A[I0, p][row][kr]
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = n0 + j * 8 + (lane >> 2);
+        dmma(aw[j][0], aw[j][1], fw, s.pb[col * kLdP + kr]);
+        dmma(am[j][0], am[j][1], fm, s.ui[col * kLdP + kr]);
+      }
+    }
+    double* wdst = a.wbuf + (size_t)(ph.p & 1) * kP * (a.N + 1);
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
+        s.ws[cc * kLdP + rr] = aw[j][h];
+        if (rr < kb && cc < m) wdst[(size_t)(r + cc) * kP + rr] = aw[j][h];
+        if (rr < m && !(fabs(am[j][h]) <= kPivThresh)) bad = true;
+      }
+    if (bad) gj_fail(a);
+  }
+  __syncthreads();
+  {
+    double acc[2][2] = {};
+#pragma unroll
+    for (int kk = 0; kk < kP; kk += 4) {
+      const int kr = kk + (lane & 3);
+      const double f = s.ab[kr * kLdT + m0 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        dmma(acc[j][0], acc[j][1], f, s.ws[(n0 + j * 8 + (lane >> 2)) * kLdP + kr]);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
+        if (rr < m && cc < m) s.dg[cc * 33 + rr] = cv[j][h] - acc[j][h];
+      }
+  }
+}
+
 // Factor the kb x kb block in s.dg (no interchanges, multipliers checked)
 // and publish D^{-1} and U^{-1} (zero padded to 32 x 32) for panel p.
 //
@@ -338,11 +410,11 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 //      final when st becomes the pivot row),
 //   Z  U^{-1} column by column: Y[:, st] = Z[:, st] / u_stst as soon as
 //      row st of U is final, then Z[:, j>st] -= Y[:, st] U[st, j].
-// Step st needs row st of D and X and column st of D and Z, which their
-// owners publish (double buffered) before the barrier that ends step
-// st - 1; the owner of u_{st+1,st+1} also publishes its reciprocal.  Each
-// step issues all its shared-memory loads first, updates branch-free and
-// stores last.  Rolled over the steps: this runs once per panel between
+// Step st needs row st of D and X — lane st of every warp holds it for the
+// warp's own columns, so it travels by shuffles — and column st of D and Z,
+// which its owner warp publishes (double buffered) in shared memory before
+// the barrier that ends step st - 1, with the pivot's reciprocal.  Each
+// step loads first, updates branch-free and stores last.  Rolled over the steps: this runs once per panel between
 // tile phases, so it must stay small in the instruction cache.  Then
 // D^{-1} = U^{-1} L^{-1} by DMMA.
 //
@@ -372,11 +444,9 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
     zv[q] = xv[q];
   }
   bool ok = true;
-  // publish step 0's row, column and reciprocal pivot
-  if (i == 0) {
-    *reinterpret_cast<double4*>(&s.rowd[0][j0]) = make_double4(dv[0], dv[1], dv[2], dv[3]);
-    *reinterpret_cast<double4*>(&s.rowx[0][j0]) = make_double4(xv[0], xv[1], xv[2], xv[3]);
-  }
+  // publish step 0's column and reciprocal pivot (pivot rows travel by
+  // shuffles inside each warp: lane st of every warp holds row st of its
+  // four columns)
   if (g == 0) {
     s.cold[0][i] = dv[0];
     s.colz[0][i] = zv[0];
@@ -389,11 +459,15 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
 #pragma unroll 1
   for (int st = 0; st < kP; ++st) {
     const int par = st & 1, nx = st + 1;
-    // loads
+    // loads: the pivot reciprocal and this row's column-st entries from
+    // shared memory, the pivot row from lane st of this warp
     const double rinv = s.rinv[st], cd = s.cold[par][i], cz = s.colz[par][i];
-    const double4 u4 = *reinterpret_cast<const double4*>(&s.rowd[par][j0]);
-    const double4 x4 = *reinterpret_cast<const double4*>(&s.rowx[par][j0]);
-    const double ur[4] = {u4.x, u4.y, u4.z, u4.w}, xr[4] = {x4.x, x4.y, x4.z, x4.w};
+    double ur[4], xr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ur[q] = __shfl_sync(0xffffffffu, dv[q], st);
+      xr[q] = __shfl_sync(0xffffffffu, xv[q], st);
+    }
     // multiplier l_{i,st} and (U^{-1})_{i,st}
     const double l = i > st ? cd * rinv : 0.0;
     const double y = i <= st ? cz * rinv : 0.0;
@@ -407,7 +481,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
       xv[q] = fma(ahead ? 0.0 : -l, xr[q], xv[q]);
       zv[q] = (j == st && i <= st) ? y : zv[q];
     }
-    // stores for step nx
+    // column nx for step nx (its owner warp)
     if (nx < kP) {
       const int qn = nx - j0;  // in [0, 4) for the owner warp
       if (qn >= 0 && qn < 4) {
@@ -419,10 +493,6 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
         }
         s.cold[par ^ 1][i] = dc;
         s.colz[par ^ 1][i] = zc;
-      }
-      if (i == nx) {
-        *reinterpret_cast<double4*>(&s.rowd[par ^ 1][j0]) = make_double4(dv[0], dv[1], dv[2], dv[3]);
-        *reinterpret_cast<double4*>(&s.rowx[par ^ 1][j0]) = make_double4(xv[0], xv[1], xv[2], xv[3]);
       }
     }
     __syncthreads();
@@ -498,12 +568,7 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     if (special) {
       // the next diagonal block: W of its columns, multipliers checked,
       // updated block kept in shared memory, then factored
-      const Task k = task_of(ph, 0);
-      tile_load(a, ph, k, true, R);
-      load_inv(a, p, s);
-      tile_stage(R, true, s);
-      __syncthreads();
-      tile_compute(a, ph, k, R.cv, true, true, true, true, s);
+      special_tile(a, ph, s);
       unsigned long long td = pr ? gtimer() : 0;
       gj_diag(a, p + 1, ph.kb2, s);
       if (pr) a.prof[9] += gtimer() - td;

@@ -47,6 +47,31 @@ __global__ void tile_loop(GjArgs a, int reps, int want_w, long long* cyc) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / reps;
 }
 
+// the special tile (next diagonal block, 32 x 32) followed by its factorisation
+__global__ void special_loop(GjArgs a, int reps, long long* cyc) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem& s = *reinterpret_cast<Smem*>(smraw);
+  const Phase ph(a.N, 1);
+  long long tt = 0, td = 0;
+  for (int r = 0; r < reps; ++r) {
+    long long t0 = clock64();
+    special_tile(a, ph, s);
+    __syncthreads();
+    long long t1 = clock64();
+    for (int e = threadIdx.x; e < kP * 33; e += kThr) s.dg[e] += (e % 34 == 0) ? 40.0 : 0.0;
+    __syncthreads();
+    long long t2 = clock64();
+    gj_diag(a, 2, kP, s);
+    long long t3 = clock64();
+    tt += t1 - t0;
+    td += t3 - t2;
+  }
+  if (threadIdx.x == 0) {
+    cyc[0] = tt / reps;
+    cyc[1] = td / reps;
+  }
+}
+
 __global__ void sync_loop(int reps, long long* cyc) {
   cg::grid_group grid = cg::this_grid();
   long long t0 = clock64();
@@ -101,7 +126,14 @@ int main() {
     printf("diag_parts: gj_diag %lld cycles, 32 bare barriers %lld\n", hh[0], hh[1]);
     long long dt[8];
     cudaMemcpyFromSymbol(dt, g_diag_t, sizeof(dt));
-    printf("   lu %lld inverses %lld dinv+store %lld\n", dt[1]-dt[0], dt[2]-dt[1], dt[3]-dt[2]);
+    printf("   lu %lld inverses %lld dinv+store %lld | b0: leaf %lld panel %lld\n", dt[1]-dt[0], dt[2]-dt[1], dt[3]-dt[2], dt[4]-dt[6], dt[5]-dt[4]);
+  }
+  cudaFuncSetAttribute(special_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int it = 0; it < 2; ++it) {
+    special_loop<<<1, kThr, smem>>>(a, 50, cyc);
+    long long hh[2];
+    cudaMemcpy(hh, cyc, 16, cudaMemcpyDeviceToHost);
+    printf("special tile %lld cycles, then gj_diag %lld cycles (steady state)\n", hh[0], hh[1]);
   }
   for (int it = 0; it < 2; ++it) {
     diag_loop<<<1, kThr, smem>>>(a, 100, cyc);
