@@ -150,7 +150,7 @@ struct Smem {
   double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
   double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
   double za[kP * kLdP], xb[kP * kLdP];  // U^{-1}, L^{-1} as DMMA operands (gj_diag)
-  double cold[2][kP], colz[2][kP], rinv[kP];  // gj_diag broadcasts (double buffered)
+  double gl[2][4][kP], gy[2][4][kP];  // gj_diag: a group's l and y columns (double buffered)
 };
 
 // Load D^{-1}, U^{-1} of panel p into shared memory.
@@ -402,28 +402,24 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
 // Factor the kb x kb block in s.dg (no interchanges, multipliers checked)
 // and publish D^{-1} and U^{-1} (zero padded to 32 x 32) for panel p.
 //
-// One right-looking loop of 32 steps, one CTA barrier each.  Thread
-// (row i = lane, column group g = warp) keeps four columns of three
-// matrices in registers:
+// Right-looking elimination in groups of four steps.  Thread (row i = lane,
+// column group g = warp) keeps four columns of three matrices in registers:
 //   D  the block being eliminated (U in the upper triangle at the end),
 //   X  L^{-1}: forward elimination of [L | I] rides along (row st of X is
 //      final when st becomes the pivot row),
 //   Z  U^{-1} column by column: Y[:, st] = Z[:, st] / u_stst as soon as
 //      row st of U is final, then Z[:, j>st] -= Y[:, st] U[st, j].
-// Step st needs row st of D and X — lane st of every warp holds it for the
-// warp's own columns, so it travels by shuffles — and column st of D and Z,
-// which its owner warp publishes (double buffered) in shared memory before
-// the barrier that ends step st - 1, with the pivot's reciprocal.  Each
-// step loads first, updates branch-free and stores last.  Rolled over the steps: this runs once per panel between
-// tile phases, so it must stay small in the instruction cache.  Then
-// D^{-1} = U^{-1} L^{-1} by DMMA.
-//
-// Measured (tools/micro/gj_bench.cu): ~750 cycles per step, ~25k cycles per
-// block.  A shared-memory round trip through a CTA barrier costs ~200
-// cycles on B200 and the reciprocal ~80 more; a blocked variant (8 x 8
-// register leaves, panel and trailing updates between barriers) and
-// single-warp variants (shared-memory rows, shuffled register rows) were
-// all measured slower or no faster.
+// Group g (steps 4g..4g+3) is warp g's own columns: that warp factors it
+// alone — pivot rows and the pivot by shuffles, registers only — and
+// publishes the group's four multiplier columns and four Y columns; after
+// ONE CTA barrier every other warp applies the group to its columns as four
+// shuffle mini-steps (the pivot rows are in lane st of the same warp).
+// Eight barriers per block instead of 32: a shared-memory round trip
+// through a CTA barrier costs ~200 cycles on B200 and dominated the
+// step-per-barrier version (24.6k -> 14.1k cycles, tools/micro/gj_bench.cu).
+// Rolled over the groups: this runs once per panel between tile phases and
+// must stay small in the instruction cache.  Then D^{-1} = U^{-1} L^{-1} by
+// DMMA.
 #ifdef GJ_MICRO
 __device__ long long g_diag_t[8];
 #define GJ_T(k) if (threadIdx.x == 0) g_diag_t[k] = clock64();
@@ -444,58 +440,63 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
     zv[q] = xv[q];
   }
   bool ok = true;
-  // publish step 0's column and reciprocal pivot (pivot rows travel by
-  // shuffles inside each warp: lane st of every warp holds row st of its
-  // four columns)
-  if (g == 0) {
-    s.cold[0][i] = dv[0];
-    s.colz[0][i] = zv[0];
-    if (i == 0) {
-      s.rinv[0] = 1.0 / dv[0];
-      ok = fabs(dv[0]) > 0.0 && isfinite(dv[0]);
-    }
-  }
-  __syncthreads();
+  // Four steps per group, group g = steps 4g..4g+3 = the columns of warp g.
+  // The owner warp factors its group alone (pivot row and column by
+  // shuffles, registers only) and publishes the four multiplier columns
+  // l and the four U^{-1} columns y; after ONE barrier every other warp
+  // applies the group to its own columns as four shuffle mini-steps
+  // (pivot rows from lane st of the same warp).
 #pragma unroll 1
-  for (int st = 0; st < kP; ++st) {
-    const int par = st & 1, nx = st + 1;
-    // loads: the pivot reciprocal and this row's column-st entries from
-    // shared memory, the pivot row from lane st of this warp
-    const double rinv = s.rinv[st], cd = s.cold[par][i], cz = s.colz[par][i];
-    double ur[4], xr[4];
+  for (int grp = 0; grp < kP / 4; ++grp) {
+    const int st0 = 4 * grp, par = grp & 1;
+    if (g == grp) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ur[q] = __shfl_sync(0xffffffffu, dv[q], st);
-      xr[q] = __shfl_sync(0xffffffffu, xv[q], st);
-    }
-    // multiplier l_{i,st} and (U^{-1})_{i,st}
-    const double l = i > st ? cd * rinv : 0.0;
-    const double y = i <= st ? cz * rinv : 0.0;
-    ok = ok && fabs(l) <= kPivThresh;
+      for (int sidx = 0; sidx < 4; ++sidx) {
+        const int st = st0 + sidx;
+        const double piv = __shfl_sync(0xffffffffu, dv[sidx], st);
+        const double rinv = 1.0 / piv;
+        ok = ok && fabs(piv) > 0.0 && isfinite(piv);
+        const double l = i > st ? dv[sidx] * rinv : 0.0;   // multiplier l_{i,st}
+        const double y = i <= st ? zv[sidx] * rinv : 0.0;  // (U^{-1})_{i,st}
+        ok = ok && fabs(l) <= kPivThresh;
+        s.gl[par][sidx][i] = l;
+        s.gy[par][sidx][i] = y;
+        if (i <= st) zv[sidx] = y;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + q;
-      const bool ahead = j > st;
-      dv[q] = fma(ahead ? -l : 0.0, ur[q], dv[q]);
-      zv[q] = fma(ahead ? -y : 0.0, ur[q], zv[q]);
-      xv[q] = fma(ahead ? 0.0 : -l, xr[q], xv[q]);
-      zv[q] = (j == st && i <= st) ? y : zv[q];
-    }
-    // column nx for step nx (its owner warp)
-    if (nx < kP) {
-      const int qn = nx - j0;  // in [0, 4) for the owner warp
-      if (qn >= 0 && qn < 4) {
-        const double dc = qn == 0 ? dv[0] : qn == 1 ? dv[1] : qn == 2 ? dv[2] : dv[3];
-        const double zc = qn == 0 ? zv[0] : qn == 1 ? zv[1] : qn == 2 ? zv[2] : zv[3];
-        if (i == nx) {
-          s.rinv[nx] = 1.0 / dc;
-          ok = ok && fabs(dc) > 0.0 && isfinite(dc);
+        for (int q = 0; q < 4; ++q) {
+          if (q > sidx) {  // columns ahead inside the group: D and Z
+            const double u = __shfl_sync(0xffffffffu, dv[q], st);
+            dv[q] = fma(-l, u, dv[q]);
+            zv[q] = fma(-y, u, zv[q]);
+          } else {  // columns j <= st: X
+            const double xr = __shfl_sync(0xffffffffu, xv[q], st);
+            xv[q] = fma(-l, xr, xv[q]);
+          }
         }
-        s.cold[par ^ 1][i] = dc;
-        s.colz[par ^ 1][i] = zc;
       }
     }
     __syncthreads();
+    if (g != grp) {
+#pragma unroll
+      for (int sidx = 0; sidx < 4; ++sidx) {
+        const int st = st0 + sidx;
+        const double l = s.gl[par][sidx][i], y = s.gy[par][sidx][i];
+        if (g > grp) {  // columns ahead: D and Z
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double u = __shfl_sync(0xffffffffu, dv[q], st);
+            dv[q] = fma(-l, u, dv[q]);
+            zv[q] = fma(-y, u, zv[q]);
+          }
+        } else {  // columns behind: X
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double xr = __shfl_sync(0xffffffffu, xv[q], st);
+            xv[q] = fma(-l, xr, xv[q]);
+          }
+        }
+      }
+    }
   }
   GJ_T(1)
   if (!ok) gj_fail(a);
