@@ -145,7 +145,7 @@ __device__ __forceinline__ double* dst_ptr(const GjArgs& a, int r, int c) {
 struct Smem {
   double di[kP * kLdP];   // D^{-1}: A operand, [k*kLdP + m]
   double ui[kP * kLdP];   // U^{-1}: B operand, [n*kLdP + k]
-  double ab[kP * kLdT];   // A[I, p] (m x kb): A operand [k*kLdT + m]
+  double ab2[2][kP * kLdT];  // A[I, p] (m x kb): A operand [k*kLdT + m], double buffered
   double pb[kT * kLdP];   // A[p, J] (kb x n): B operand [n*kLdP + k]
   double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
   double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
@@ -184,39 +184,68 @@ struct TileRegs {
   double ab[8], pb[8], cv[4][2][2];
 };
 
+// Source of row r of the augmented matrix: element (r, c) at
+// base + c * stride, except column N of a matrix row, which is b[r].  The
+// previous panel's rows live in its row-panel buffer (stride kP).
+struct RowSrc {
+  const double* base;
+  int stride;
+  bool buf;
+};
+__device__ __forceinline__ RowSrc row_src(const GjArgs& a, const Phase& ph, int r) {
+  if (ph.kprev >= 0 && r >= ph.kprev && r < ph.k0)
+    return {a.wbuf + (size_t)((ph.p - 1) & 1) * kP * (a.N + 1) + (r - ph.kprev), kP, true};
+  return {a.A + r, a.N, false};
+}
+__device__ __forceinline__ const double* elem(const GjArgs& a, const RowSrc& rs, int r, int c) {
+  return (c == a.N && !rs.buf) ? a.b + r : rs.base + (size_t)c * rs.stride;
+}
+
 __device__ __forceinline__ void tile_load(const GjArgs& a, const Phase& ph, const Task& k, bool want_p,
                                           TileRegs& R) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int rr = wm0 + i * 8 + (lane >> 2);
+    const RowSrc rs = row_src(a, ph, k.r + rr);
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int rr = wm0 + i * 8 + (lane >> 2), cc = wn0 + j * 8 + (lane & 3) * 2 + h;
-        R.cv[i][j][h] = (rr < k.m && cc < k.n) ? __ldcg(src_ptr(a, ph, k.r + rr, k.c + cc)) : 0.0;
+        const int cc = wn0 + j * 8 + (lane & 3) * 2 + h;
+        R.cv[i][j][h] = (rr < k.m && cc < k.n) ? __ldcg(elem(a, rs, k.r + rr, k.c + cc)) : 0.0;
       }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int e = tid + q * kThr, kk = e >> 6, i = e & 63;
-    R.ab[q] = (i < k.m && kk < ph.kb) ? __ldcg(src_ptr(a, ph, k.r + i, ph.k0 + kk)) : 0.0;
   }
-  if (want_p) {
+  {
+    const int i = tid & 63, kk0 = tid >> 6;  // row i, columns k0 + kk0 + 4q
+    const RowSrc rs = row_src(a, ph, k.r + i);
+    const bool rowok = i < k.m;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * kThr, j = e >> 5, kk = e & 31;
-      R.pb[q] = (kk < ph.kb && j < k.n) ? __ldcg(dst_ptr(a, ph.k0 + kk, k.c + j)) : 0.0;
+      const int kk = kk0 + 4 * q;
+      R.ab[q] = (rowok && kk < ph.kb) ? __ldcg(rs.base + (size_t)(ph.k0 + kk) * rs.stride) : 0.0;
+    }
+  }
+  if (want_p) {
+    const int kk = tid & 31, j0 = tid >> 5;  // panel row k0 + kk, columns c + j0 + 8q
+    const bool rowok = kk < ph.kb;
+    const double* rowp = a.A + ph.k0 + kk;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + 8 * q, c = k.c + j;
+      R.pb[q] = (rowok && j < k.n) ? __ldcg(c == a.N ? a.b + ph.k0 + kk : rowp + (size_t)c * a.N) : 0.0;
     }
   }
 }
 
-__device__ __forceinline__ void tile_stage(const TileRegs& R, bool want_p, Smem& s) {
+__device__ __forceinline__ void tile_stage(const TileRegs& R, bool want_p, Smem& s, int buf) {
   const int tid = threadIdx.x;
+  double* ab = s.ab2[buf];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int e = tid + q * kThr;
-    s.ab[(e >> 6) * kLdT + (e & 63)] = R.ab[q];
+    ab[(e >> 6) * kLdT + (e & 63)] = R.ab[q];
   }
   if (want_p) {
 #pragma unroll
@@ -233,8 +262,9 @@ __device__ __forceinline__ void tile_stage(const TileRegs& R, bool want_p, Smem&
 //   check  : the multipliers A[I, p] U^{-1} of rows below the panel,
 //   C -= A[I, p] W  -> global memory, or s.dg for the next diagonal block.
 __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, const double (&cv)[4][2][2],
-                             bool want_w, bool store_w, bool check, bool to_diag, Smem& s) {
+                             bool want_w, bool store_w, bool check, bool to_diag, Smem& s, int buf) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* ab = s.ab2[buf];
   if (want_w) {
     const int wr0 = (warp >> 2) * 16, wc0 = (warp & 3) * 16;
     double acc[2][2][2] = {};
@@ -271,7 +301,7 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
       const int kr = kk + (lane & 3);
       double af[2], bf[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = s.ab[kr * kLdT + mm0 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < 2; ++i) af[i] = ab[kr * kLdT + mm0 + i * 8 + (lane >> 2)];
 #pragma unroll
       for (int j = 0; j < 2; ++j) bf[j] = s.ui[(mn0 + j * 8 + (lane >> 2)) * kLdP + kr];
 #pragma unroll
@@ -289,7 +319,7 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
           if (mm0 + i * 8 + (lane >> 2) < k.m && !(fabs(acc[i][j][h]) <= kPivThresh)) bad = true;
     if (bad) gj_fail(a);
   }
-  __syncthreads();  // W visible
+  if (want_w || check) __syncthreads();  // W visible, s.pb free
   const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
   if (wm0 < k.m && wn0 < k.n) {
     double acc[4][2][2] = {};
@@ -298,7 +328,7 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
       const int kr = kk + (lane & 3);
       double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = s.ab[kr * kLdT + wm0 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < 4; ++i) af[i] = ab[kr * kLdT + wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
       for (int j = 0; j < 2; ++j) bf[j] = s.ws[(wn0 + j * 8 + (lane >> 2)) * kLdP + kr];
 #pragma unroll
@@ -322,7 +352,9 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
           }
         }
   }
-  __syncthreads();  // s.ab / s.pb / s.ws free
+  // no closing barrier: the next task stages into the other s.ab2 buffer,
+  // and s.pb / s.ws are rewritten only after the next staging barrier, which
+  // every warp reaches after its C stage here
 }
 
 // The next diagonal block (rows and columns [k1, k1 + kb2), kb2 <= 32) on
@@ -345,7 +377,7 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int e = tid + q * kThr, kk = e >> 5, i = e & 31;  // A[I0, p]: (i, kk)
-    s.ab[kk * kLdT + i] = (i < m && kk < kb) ? __ldcg(src_ptr(a, ph, r + i, k0 + kk)) : 0.0;
+    s.ab2[0][kk * kLdT + i] = (i < m && kk < kb) ? __ldcg(src_ptr(a, ph, r + i, k0 + kk)) : 0.0;
     const int j = e >> 5, k = e & 31;  // A[p, J0]: (k, j)
     s.pb[j * kLdP + k] = (k < kb && j < m) ? __ldcg(dst_ptr(a, k0 + k, r + j)) : 0.0;
   }
@@ -357,7 +389,7 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
     for (int kk = 0; kk < kP; kk += 4) {
       const int kr = kk + (lane & 3);
       const double fw = s.di[kr * kLdP + m0 + (lane >> 2)];  // D^{-1}[row][kr]
-      const double fm = s.ab[kr * kLdT + m0 + (lane >> 2)];  // A[I0, p][row][kr]
+      const double fm = s.ab2[0][kr * kLdT + m0 + (lane >> 2)];  // A[I0, p][row][kr]
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int col = n0 + j * 8 + (lane >> 2);
@@ -384,7 +416,7 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
 #pragma unroll
     for (int kk = 0; kk < kP; kk += 4) {
       const int kr = kk + (lane & 3);
-      const double f = s.ab[kr * kLdT + m0 + (lane >> 2)];
+      const double f = s.ab2[0][kr * kLdT + m0 + (lane >> 2)];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         dmma(acc[j][0], acc[j][1], f, s.ws[(n0 + j * 8 + (lane >> 2)) * kLdP + kr]);
@@ -588,7 +620,8 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
         int lastJ = -1;
         for (int tt = t0; tt < t1; ++tt) {
           const bool neww = k.J != lastJ;
-          tile_stage(R, neww, s);
+          const int buf = (tt - t0) & 1;
+          tile_stage(R, neww, s, buf);
           double cv[4][2][2];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -604,7 +637,7 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
           }
           // multipliers of rows below the panel are checked once per row
           // block, in its first column block
-          tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s);
+          tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s, buf);
           lastJ = k.J;
           k = kn;
         }

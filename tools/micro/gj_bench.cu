@@ -34,14 +34,14 @@ __global__ void tile_loop(GjArgs a, int reps, int want_w, long long* cyc) {
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     const bool w = want_w || r == 0;
-    tile_stage(R, w, s);
+    tile_stage(R, w, s, r & 1);
     double cv[4][2][2];
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 2; ++j)
         for (int h = 0; h < 2; ++h) cv[i][j][h] = R.cv[i][j][h];
     __syncthreads();
     tile_load(a, ph, k, want_w, R);
-    tile_compute(a, ph, k, cv, w, false, false, false, s);
+    tile_compute(a, ph, k, cv, w, false, false, false, s, r & 1);
   }
   long long t1 = clock64();
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / reps;
