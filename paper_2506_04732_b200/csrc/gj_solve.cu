@@ -582,6 +582,10 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     tp = tq;                                   \
   }
   if (cta == 0) {
+    // *info = 0 before the first grid barrier; every check that can set it
+    // runs after that barrier
+    if (tid == 0) *a.info = 0;
+    __syncthreads();
     const int kb = N < kP ? N : kP;
     for (int e = tid; e < kP * kP; e += kThr) {
       const int c = e >> 5, r = e & 31;
@@ -705,14 +709,13 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   const int npan = (N + kP - 1) / kP;
   double* inv = allocator().alloc((size_t)npan * kInv);
   double* wbuf = allocator().alloc((size_t)2 * kP * (N + 1));
-  T2S2_CUDA(cudaMemsetAsync(info_dev, 0, sizeof(int), stream()));
   static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
   unsigned long long* pbuf = nullptr;
   if (prof) {
     pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
     T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
   }
-  GjArgs a{N, A, b, inv, wbuf, info_dev, pbuf};
+  GjArgs a{N, A, b, inv, wbuf, info_dev, pbuf};  // *info zeroed by the kernel
   void* params[] = {&a};
   {
     // algorithmic: N^3 (Gauss-Jordan) + 2 N^2; bytes: one read and write of the matrix
