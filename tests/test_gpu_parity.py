@@ -441,3 +441,37 @@ def test_config4_full_size_sweeps_within_oracle_spread(pk, index):
     spread = np.maximum(hi - lo, 1e-8 * hi)
     got = np.array(rep.residual_history)
     assert np.all(got >= lo - 3 * spread) and np.all(got <= hi + 3 * spread), (got, lo, hi)
+
+
+@pytest.mark.parametrize("rank", [8, 24, 40, 64])
+def test_norm_and_round_wide_cores(pk, rank):
+    """TT norm and rounding at the ranks of the residual difference train and
+    of config 4 (unfoldings up to 33*64 x 64): the warp-level QR/TSQR leaves
+    (one to four columns per warp, multi-leaf trees) and the thin SVD against
+    the oracle (numpy Householder QR / LAPACK SVD)."""
+    from oracle import tt_ops as ot
+
+    _, tt, _, _ = pk
+    rng = np.random.default_rng(rank)
+    d, n = 4, 33
+    ranks = [1] + [rank] * (d - 1) + [1]
+    # graded cores: singular values spread over many orders, a sum of two
+    # trains so the unfoldings are rank deficient after the sum
+    cores = []
+    for l in range(d):
+        c = rng.standard_normal((ranks[l], n, ranks[l + 1]))
+        c *= np.logspace(0, -12, ranks[l + 1])[None, None, :]
+        cores.append(c)
+    x = tt.TTVector(cores)
+    want = ot.tt_norm(cores)
+    got = tt.tt_norm(x)
+    assert abs(got - want) <= 1e-13 * want
+    s = ot.tt_add(cores, ot.tt_scale(cores, -0.5))  # ranks double, half of them dependent
+    got_s = tt.tt_norm(tt.TTVector(s))
+    assert abs(got_s - 0.5 * want) <= 1e-12 * want
+    r = tt.tt_round(tt.TTVector(s), 1e-10)
+    ro = ot.tt_round(s, 1e-10)
+    assert r.ranks == list(ot.ranks_of(ro)) or ranks_agree(r.cores, ro)[0]
+    full_ok = float(np.prod([float(c.shape[1]) for c in s])) <= 2e6
+    if full_ok:
+        assert np.linalg.norm(ot.tt_full(r.cores) - ot.tt_full(ro)) <= 1e-9 * np.linalg.norm(ot.tt_full(ro))
