@@ -805,11 +805,15 @@ __global__ void __launch_bounds__(512)
     }
     return;
   }
-  for (int e = tid; e < k * n; e += blockDim.x) {
-    const int rr = e / n, cc = e - rr * n;
-    R[e] = cc >= rr ? Rs[(size_t)cc * n + rr] : 0.0;
+  {
+    // k x n (one block), or n x n per block (TSQR leaves, rows >= n)
+    double* Rb = R + (size_t)blockIdx.x * n * n;
+    for (int e = tid; e < k * n; e += blockDim.x) {
+      const int rr = e / n, cc = e - rr * n;
+      Rb[e] = cc >= rr ? Rs[(size_t)cc * n + rr] : 0.0;
+    }
   }
-  // thin Q: warp forms its own columns c < k
+  // thin Q: warp forms its own columns c < k (rows of this block)
 #pragma unroll
   for (int q = 0; q < CPW; ++q) {
     const int c = warp + q * nw;
@@ -839,9 +843,9 @@ __global__ void __launch_bounds__(512)
       const int i = lane + 32 * r;
       if (i < mr) {
         if (cm)
-          Q[(size_t)c * m + i] = x[r];
+          Q[(size_t)c * m + r0 + i] = x[r];
         else
-          Q[(size_t)i * k + c] = x[r];
+          Q[(size_t)(r0 + i) * k + c] = x[r];
       }
     }
   }
@@ -971,6 +975,40 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
     if (ok) {
       T2S2_CHECK_LAUNCH();
       return;
+    }
+  }
+  // tall blocks that do not fit the one-CTA shared-memory kernel (config-4
+  // cores, 33*64 x 64): TSQR with Q — warp-level leaves, the stacked leaf
+  // R factors factored recursively (Q2, R), Q = diag(Q_leaf) Q2 as one
+  // small GEMM per leaf
+  if (!old_qr && m > n && n <= 64 && ((size_t)m * n + k) * sizeof(double) > kSmemCap) {
+    const int cap = n > 32 ? 256 : 384;
+    const int leaves = (m + cap - 1) / cap;
+    const int chunk = (m + leaves - 1) / leaves;
+    const int blocks = ceil_div(m, chunk);
+    const int last = m - (blocks - 1) * chunk;
+    if (chunk <= cap && last >= n) {
+      DTensor Ql({m, n}), S({blocks * n, n});
+      bool ok;
+      {
+        LaunchScope ls("qr", 4.0 * m * (double)n * n, 16.0 * m * (double)n);
+        ok = wqr<true>(blocks, m, n, chunk, A, Ql.p, S.p, cm ? 1 : 0);
+      }
+      if (ok) {
+        T2S2_CHECK_LAUNCH();
+        DTensor Q2;
+        qr_thin(blocks * n, n, S.p, Q2, R, false);  // Q2 row-major (blocks n) x n, R n x n
+        for (int b = 0; b < blocks; ++b) {
+          const int r0 = b * chunk, mr = b + 1 < blocks ? chunk : last;
+          if (cm)  // Q^T (n x m, ld m) block = Q2_b^T Q_b^T
+            gemm(true, false, n, mr, n, 1.0, Q2.p + (size_t)b * n * n, n, Ql.p + r0, m, 0.0,
+                 Q.p + r0, m);
+          else  // Q rows of the leaf = Q_b Q2_b
+            gemm(false, false, mr, n, n, 1.0, Ql.p + (size_t)r0 * n, n, Q2.p + (size_t)b * n * n, n,
+                 0.0, Q.p + (size_t)r0 * n, n);
+        }
+        return;
+      }
     }
   }
   double* W = allocator().alloc((size_t)m * n);
