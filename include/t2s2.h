@@ -144,10 +144,12 @@ int t2s2_full(t2s2_context* ctx, const t2s2_train* v, double* host_dense, size_t
 int t2s2_solve(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* rhs,
                const t2s2_train* x0, const t2s2_solver_config* cfg, t2s2_train** x,
                t2s2_solve_report* report);
-/* Dense solve of one local system (column-major n x n, partial pivoting) —
- * the kernel behind the direct local solves (tt_solver.py:357-366, 392-397),
- * exposed for testing; returns T2S2_ERR_VALUE on an exactly singular matrix
- * (numpy.linalg.solve's LinAlgError). */
+/* Dense solve of one local system (column-major n x n) — the kernels behind
+ * the direct local solves (tt_solver.py:357-366, 392-397), exposed for
+ * testing: the verified no-pivot block Gauss-Jordan kernel (GEPP's factors
+ * whenever partial pivoting would make no interchange), else the
+ * partial-pivoting kernel; returns T2S2_ERR_VALUE on an exactly singular
+ * matrix (numpy.linalg.solve's LinAlgError). */
 int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const double* b,
                      double* x);
 /* Row-major fp64 GEMM on device pointers, C = op(A) op(B) (op = transpose
