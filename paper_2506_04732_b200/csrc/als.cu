@@ -934,17 +934,19 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       const int keep = sp.carry.dim(0), r1 = sp.carry.dim(1);
       const int rest = (int)(nx.size() / r1);
       DTensor nn({keep + sp.extra, nx.dim(1), nx.dim(2)});
-      gemm(false, false, keep, rest, r1, 1.0, sp.carry.p, r1, nx.p, rest, 0.0, nn.p, rest);
       if (sp.extra > 0) dfill(nn.p + (size_t)keep * rest, 0.0, (size_t)sp.extra * rest);
-      cores[l + 1] = std::move(nn);
       {
+        // the carry product (next core) and the four interface recurrences
+        // of the moved bond are independent: one program
         GemmBatch gb;
+        gb.add(0, false, false, keep, rest, r1, sp.carry.p, r1, 0, nx.p, rest, 0, nn.p, rest, 0);
         sw.la[l + 1] = step_a_left(gb, 0, sw.la[l], cores[l], A.cores[l], sw.acg[l]);
         sw.ln[l + 1] = step_n_left(gb, 0, sw.ln[l], cores[l], A.cores[l], sw.acg[l]);
         sw.lg[l + 1] = step_g_left(gb, 0, sw.lg[l], cores[l], A.cores[l], rhs.cores[l]);
         sw.lb[l + 1] = step_b_left(gb, 0, sw.lb[l], cores[l], rhs.cores[l]);
         gb.run();
       }
+      cores[l + 1] = std::move(nn);
     }
     for (int l = d - 1; l >= 0; --l) {
       DTensor u, grad;
@@ -973,16 +975,18 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       const int nk = keep + sp.extra;
       DTensor np({pv.dim(0), pv.dim(1), nk});
       if (sp.extra > 0) dfill(np.p, 0.0, np.size());
-      gemm(false, false, rows, keep, r0, 1.0, pv.p, r0, sp.carry.p, keep, 0.0, np.p, nk);
-      cores[l - 1] = std::move(np);
       {
+        // the carry product (previous core) and the four interface
+        // recurrences of the moved bond are independent: one program
         GemmBatch gb;
+        gb.add(0, false, false, rows, keep, r0, pv.p, r0, 0, sp.carry.p, keep, 0, np.p, nk, 0);
         sw.ra[l] = step_a_right(gb, 0, sw.ra[l + 1], cores[l], A.cores[l], sw.acg[l]);
         sw.rn[l] = step_n_right(gb, 0, sw.rn[l + 1], cores[l], A.cores[l], sw.acg[l]);
         sw.rg[l] = step_g_right(gb, 0, sw.rg[l + 1], cores[l], A.cores[l], rhs.cores[l]);
         sw.rb[l] = step_b_right(gb, 0, sw.rb[l + 1], cores[l], rhs.cores[l]);
         gb.run();
       }
+      cores[l - 1] = std::move(np);
     }
     current_res = measure_residual(A, sw.acg, cores, rhs, bnorm);
     rep.residuals.push_back(current_res);
