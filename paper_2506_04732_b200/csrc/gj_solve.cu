@@ -5,15 +5,17 @@
 // The local systems of an implicit step (I + dt L projected on orthonormal
 // interface bases, tt_solver.py:350-362 solves them with numpy.linalg.solve)
 // are well conditioned and their diagonal pivots are large.  Every
-// multiplier is checked against the threshold-pivoting bound kPivThresh
-// (below); if one exceeds it, or a pivot is zero, the kernel declines
+// multiplier is checked against kPivThresh = 1 (below): partial pivoting
+// makes no interchange exactly when all |l| <= 1, and then these are GEPP's
+// factors; if one exceeds it, or a pivot is zero, the kernel declines
 // (*info = -1) and the caller runs the partial-pivoting kernel.
 //
 // Panel p (rows/columns [k0, k1), k1 = k0 + 32), normalised block
 // Gauss-Jordan:
-//   CTA 0 (previous phase) factored the diagonal block D_p = L U (one
-//   32-step loop: U, L^{-1} and U^{-1} together, multipliers checked) and
-//   published D^{-1} = U^{-1} L^{-1} and U^{-1} (32 x 32 each).
+//   CTA 0 (previous phase) factored the diagonal block D_p = L U (in
+//   groups of four steps: U, L^{-1} and U^{-1} together, multipliers
+//   checked, see gj_diag) and published D^{-1} = U^{-1} L^{-1} and U^{-1}
+//   (32 x 32 each).
 //   Every other row block I (above AND below the panel) is a tile task
 //   together with a column block J of [k1, N] (column N = right-hand side):
 //       W_J = D^{-1} A[p, J]            (the panel rows, normalised)
@@ -22,12 +24,13 @@
 //   A[I, p] U^{-1} are formed and checked (|l| <= kPivThresh).  A CTA walks a
 //   contiguous J-major chunk of tasks, so W_J is formed once per CTA and
 //   column block, and the next task's global loads are in flight (in
-//   registers) while the current one computes.  The tile of row block 0
+//   registers) while the current one computes; operand staging is double
+//   buffered, one CTA barrier per task.  The tile of row block 0
 //   stores W_J to a double-buffered 32 x (N+1) row panel, which the next
 //   phase reads as those rows' current values.
-//   CTA 0 takes the tile holding the next diagonal block and factors it
-//   while the other CTAs work (lookahead), so a panel costs ONE grid
-//   barrier.
+//   CTA 0 updates the next diagonal block (special_tile: 32 x 32 products
+//   on all warps) and factors it while the other CTAs work (lookahead), so
+//   a panel costs ONE grid barrier.
 // After the last panel every diagonal block is the identity: b holds x.
 //
 // Algorithmic cost N^3 (vs 2/3 N^3 + back substitution for LU): on this
