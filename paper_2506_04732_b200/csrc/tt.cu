@@ -26,17 +26,27 @@ __global__ void scale_cols_kernel(double* X, int rows, int cols, int ld, const d
   }
 }
 
-// out block (r0o, mid, r1o) <- scale * in (r0i, mid, r1i) at offsets.
-__global__ void place_block_kernel(double* out, int r0o, int mid, int r1o, const double* in,
-                                   int r0i, int r1i, int off0, int off1, double scale) {
-  long long n = (long long)r0i * mid * r1i;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)n;
-       e += gridDim.x * blockDim.x) {
-    int c = (int)(e % r1i);
-    int t = e / r1i;
-    int m = (int)(t % mid);
-    int a = (int)(t / mid);
-    out[((long long)(a + off0) * mid + m) * r1o + (c + off1)] = scale * in[e];
+// One core of a TT sum written in one pass: out (r0o, mid, r1o) holds
+// fa * a at offsets (0, 0), fb * b at offsets (ob0, ob1), zeros elsewhere
+// (the blocks are disjoint: block diagonal, or side by side in the first
+// and last cores).
+__global__ void sum_core_kernel(double* out, int r0o, int mid, int r1o, const double* a, int r0a,
+                                int r1a, double fa, const double* b, int r0b, int r1b, double fb,
+                                int ob0, int ob1) {
+  const long long n = (long long)r0o * mid * r1o;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e % r1o);
+    const long long t = e / r1o;
+    const int m = (int)(t % mid), i = (int)(t / mid);
+    double v = 0.0;
+    if (i < r0a && j < r1a) {
+      v = fa * a[((long long)i * mid + m) * r1a + j];
+    } else {
+      const int ib = i - ob0, jb = j - ob1;
+      if (ib >= 0 && jb >= 0 && ib < r0b && jb < r1b) v = fb * b[((long long)ib * mid + m) * r1b + jb];
+    }
+    out[e] = v;
   }
 }
 
@@ -213,18 +223,13 @@ Train tt_add(const Train& a, const Train& b, double sa, double sb) {
     const int r0 = l == 0 ? 1 : ca.dim(0) + cb.dim(0);
     const int r1 = l == d - 1 ? 1 : ca.dim(-1) + cb.dim(-1);
     DTensor o(with_bonds(ca, r0, r1));
-    dfill(o.p, 0.0, o.size());
     const int ob0 = l == 0 ? 0 : ca.dim(0), ob1 = l == d - 1 ? 0 : ca.dim(-1);
-    long long na = (long long)ca.size(), nb = (long long)cb.size();
+    const long long no = (long long)o.size();
     {
-      LaunchScope ls("vector", 0, 16.0*na);
-      place_block_kernel<<<grid_of(na), 256, 0, stream()>>>(o.p, r0, mid, r1, ca.p, ca.dim(0),
-                                                            ca.dim(-1), 0, 0, fa);
-    }
-    {
-      LaunchScope ls("vector", 0, 16.0*nb);
-      place_block_kernel<<<grid_of(nb), 256, 0, stream()>>>(o.p, r0, mid, r1, cb.p, cb.dim(0),
-                                                            cb.dim(-1), ob0, ob1, fb);
+      LaunchScope ls("vector", 0, 8.0 * (no + (long long)ca.size() + (long long)cb.size()));
+      sum_core_kernel<<<grid_of(no), 256, 0, stream()>>>(o.p, r0, mid, r1, ca.p, ca.dim(0),
+                                                         ca.dim(-1), fa, cb.p, cb.dim(0),
+                                                         cb.dim(-1), fb, ob0, ob1);
     }
     T2S2_CHECK_LAUNCH();
     out.cores.push_back(std::move(o));
