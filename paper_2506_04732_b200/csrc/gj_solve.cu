@@ -29,8 +29,12 @@
 //   stores W_J to a double-buffered 32 x (N+1) row panel, which the next
 //   phase reads as those rows' current values.
 //   CTA 0 updates the next diagonal block (special_tile: 32 x 32 products
-//   on all warps) and factors it while the other CTAs work (lookahead), so
-//   a panel costs ONE grid barrier.
+//   on all warps) and factors it while the other CTAs work (lookahead).
+//   No grid-wide barrier: the tile CTAs wait for an arrival count (every
+//   CTA of the previous phases, CTA 0 after publishing the next D^{-1}),
+//   CTA 0 waits only for the three tile tasks that produce its next
+//   diagonal block; the row panels are triple buffered so CTA 0 may run
+//   one phase ahead.
 // After the last panel every diagonal block is the identity: b holds x.
 //
 // Algorithmic cost N^3 (vs 2/3 N^3 + back substitution for LU): on this
@@ -69,8 +73,9 @@ struct GjArgs {
   double* A;      // column-major N x N (clobbered)
   double* b;      // right-hand side (column N), overwritten with x
   double* inv;    // npan * kInv
-  double* wbuf;   // 2 x (kP x (N+1)), column-major ld kP
+  double* wbuf;   // 3 x (kP x (N+1)), column-major ld kP (phase p: buffer p % 3)
   int* info;      // 0, or -1: a multiplier exceeded 1 / zero pivot
+  unsigned* sync; // [0] arrivals, [1 + p] finished feeder tasks of phase p (zeroed by the host)
   unsigned long long* prof;
 };
 
@@ -87,6 +92,33 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ void gj_fail(const GjArgs& a) { atomicExch(a.info, -1); }
+
+// Phase hand-off without a grid-wide barrier: every CTA adds one arrival per
+// phase (CTA 0 after factoring the next diagonal block, the others after
+// their tile tasks); a CTA waits for a count of arrivals, or — CTA 0 — only
+// for the tile tasks that produce its next diagonal block.  Release: the
+// CTA's stores, a CTA barrier, one thread's fence and atomic; acquire: one
+// thread's ld.acquire spin, then a CTA barrier (loads use ld.global.cg).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cta_signal(unsigned* p) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(p, 1u);
+  }
+}
+// wait until *p >= target (or, abortable, until *info != 0)
+__device__ __forceinline__ void cta_wait(const unsigned* p, unsigned target, const int* info,
+                                         bool abortable) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(p) < target)
+      if (abortable && *(volatile const int*)info != 0) break;
+  __syncthreads();
+}
 
 // Geometry of one phase.
 struct Phase {
@@ -138,7 +170,7 @@ struct Phase {
 // previous panel live in the row-panel buffer of the previous phase.
 __device__ __forceinline__ const double* src_ptr(const GjArgs& a, const Phase& ph, int r, int c) {
   if (ph.kprev >= 0 && r >= ph.kprev && r < ph.k0)
-    return a.wbuf + (size_t)((ph.p - 1) & 1) * kP * (a.N + 1) + (size_t)c * kP + (r - ph.kprev);
+    return a.wbuf + (size_t)((ph.p - 1) % 3) * kP * (a.N + 1) + (size_t)c * kP + (r - ph.kprev);
   return c < a.N ? a.A + (size_t)c * a.N + r : a.b + r;
 }
 __device__ __forceinline__ double* dst_ptr(const GjArgs& a, int r, int c) {
@@ -197,7 +229,7 @@ struct RowSrc {
 };
 __device__ __forceinline__ RowSrc row_src(const GjArgs& a, const Phase& ph, int r) {
   if (ph.kprev >= 0 && r >= ph.kprev && r < ph.k0)
-    return {a.wbuf + (size_t)((ph.p - 1) & 1) * kP * (a.N + 1) + (r - ph.kprev), kP, true};
+    return {a.wbuf + (size_t)((ph.p - 1) % 3) * kP * (a.N + 1) + (r - ph.kprev), kP, true};
   return {a.A + r, a.N, false};
 }
 __device__ __forceinline__ const double* elem(const GjArgs& a, const RowSrc& rs, int r, int c) {
@@ -284,7 +316,7 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    double* wdst = a.wbuf + (size_t)(ph.p & 1) * kP * (a.N + 1);
+    double* wdst = a.wbuf + (size_t)(ph.p % 3) * kP * (a.N + 1);
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -400,7 +432,7 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
         dmma(am[j][0], am[j][1], fm, s.ui[col * kLdP + kr]);
       }
     }
-    double* wdst = a.wbuf + (size_t)(ph.p & 1) * kP * (a.N + 1);
+    double* wdst = a.wbuf + (size_t)(ph.p % 3) * kP * (a.N + 1);
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -584,9 +616,11 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     a.prof[cta * 4 + (slot)] += tq - tp;       \
     tp = tq;                                   \
   }
+  unsigned* arrivals = a.sync;
+  unsigned* feed = a.sync + 1;  // feed[p]: finished feeder tasks of phase p
   if (cta == 0) {
-    // *info = 0 before the first grid barrier; every check that can set it
-    // runs after that barrier
+    // *info = 0 before the first hand-off; every check that can set it runs
+    // after that
     if (tid == 0) *a.info = 0;
     __syncthreads();
     const int kb = N < kP ? N : kP;
@@ -595,25 +629,45 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       if (r < kb && c < kb) s.dg[c * 33 + r] = __ldcg(a.A + (size_t)c * N + r);
     }
     gj_diag(a, 0, kb, s);
+    cta_signal(arrivals);  // arrival 1: D_0^{-1} published
   }
-  grid.sync();
   TileRegs R;
+  // The tile tasks of phase p that produce the next diagonal block of phase
+  // p + 1 ("feeders": row blocks 0, 1 x column blocks 0, 1 minus the
+  // special task itself) — CTA 0 waits for these only.
+  auto nfeed = [&](const Phase& ph) {
+    const int ni = ph.nbelow < 2 ? ph.nbelow : 2, nj = ph.ncb < 2 ? ph.ncb : 2;
+    return ph.kb2 > 0 ? ni * nj - 1 : 0;
+  };
+  auto is_feeder = [&](const Phase& ph, const Task& k) {
+    return ph.kb2 > 0 && k.I < 2 && k.J < 2 && k.I < ph.nbelow;
+  };
   for (int p = 0; p < npan; ++p) {
-    if (__ldcg(a.info) != 0) break;  // declined: stop early (uniform after the barrier)
     GJ_PHASE(3)
     const Phase ph(N, p);
     const bool has_diag = ph.kb2 > 0;
     const int ntile = ph.nrb * ph.ncb - (has_diag ? 1 : 0);
-    const bool special = has_diag && cta == 0;
+    const bool special = has_diag && cta == 0 && G > 1;
     if (special) {
-      // the next diagonal block: W of its columns, multipliers checked,
-      // updated block kept in shared memory, then factored
-      special_tile(a, ph, s);
-      unsigned long long td = pr ? gtimer() : 0;
-      gj_diag(a, p + 1, ph.kb2, s);
-      if (pr) a.prof[9] += gtimer() - td;
-    }
-    if (!special || G == 1) {
+      // wait only for the feeders of phase p - 1, then the next diagonal
+      // block: W of its columns, multipliers checked, updated block kept in
+      // shared memory, factored
+      if (p > 0) cta_wait(feed + (p - 1), (unsigned)nfeed(Phase(N, p - 1)), a.info, true);
+      if (__ldcg(a.info) == 0) {
+        special_tile(a, ph, s);
+        unsigned long long td = pr ? gtimer() : 0;
+        gj_diag(a, p + 1, ph.kb2, s);
+        if (pr) a.prof[9] += gtimer() - td;
+      }
+      cta_signal(arrivals);
+    } else {
+      // all arrivals of the earlier phases (CTA 0's: D_p^{-1} published)
+      if (G > 1) cta_wait(arrivals, 1u + (unsigned)G * (unsigned)p, a.info, false);
+      const bool live = __ldcg(a.info) == 0;
+      if (has_diag && G == 1 && live) {
+        special_tile(a, ph, s);
+        gj_diag(a, p + 1, ph.kb2, s);
+      }
       // a contiguous chunk of the J-major task list (consecutive tasks share
       // W); the next task's loads are in flight while one computes.  A
       // one-CTA launch (small N) does all of it after the diagonal block.
@@ -622,56 +676,67 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       const int t0 = (int)((long long)ntile * me / G1), t1 = (int)((long long)ntile * (me + 1) / G1);
       if (t0 < t1) {
         Task k = task_of(ph, t0 + off);
-        tile_load(a, ph, k, true, R);
-        load_inv(a, p, s);
+        if (live) {
+          tile_load(a, ph, k, true, R);
+          load_inv(a, p, s);
+        }
         int lastJ = -1;
         for (int tt = t0; tt < t1; ++tt) {
-          const bool neww = k.J != lastJ;
-          const int buf = (tt - t0) & 1;
-          tile_stage(R, neww, s, buf);
-          double cv[4][2][2];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) cv[i][j][h] = R.cv[i][j][h];
-          __syncthreads();
           Task kn = k;
-          if (tt + 1 < t1) {
+          if (live) {
+            const bool neww = k.J != lastJ;
+            const int buf = (tt - t0) & 1;
+            tile_stage(R, neww, s, buf);
+            double cv[4][2][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) cv[i][j][h] = R.cv[i][j][h];
+            __syncthreads();
+            if (tt + 1 < t1) {
+              kn = task_of(ph, tt + 1 + off);
+              tile_load(a, ph, kn, kn.J != k.J, R);
+            }
+            // multipliers of rows below the panel are checked once per row
+            // block, in its first column block
+            tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s, buf);
+            lastJ = k.J;
+          } else if (tt + 1 < t1) {
             kn = task_of(ph, tt + 1 + off);
-            tile_load(a, ph, kn, kn.J != k.J, R);
           }
-          // multipliers of rows below the panel are checked once per row
-          // block, in its first column block
-          tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s, buf);
-          lastJ = k.J;
+          if (G > 1 && is_feeder(ph, k)) cta_signal(feed + p);  // signalled even when skipped
           k = kn;
         }
       }
+      __syncthreads();
+      if (G > 1) cta_signal(arrivals);
     }
     GJ_PHASE(0)
-    grid.sync();
-    GJ_PHASE(1)
   }
   // the system is now the identity on every panel: b holds x except the
   // last panel's rows, which are in its row-panel buffer (a single panel
   // never ran a tile phase: x = D^{-1} b)
-  if (__ldcg(a.info) == 0 && cta == 0) {
-    const int p = npan - 1, k0 = p * kP, kb = N - k0;
-    if (npan > 1) {
-      if (tid < kb) a.b[k0 + tid] = __ldcg(a.wbuf + (size_t)(p & 1) * kP * (N + 1) + (size_t)N * kP + tid);
-    } else {
-      double* sy = s.dg;
-      if (tid < kP) sy[tid] = tid < kb ? __ldcg(a.b + tid) : 0.0;
-      __syncthreads();
-      if (tid < kb) {
-        double v = 0.0;
-        for (int k = 0; k < kb; ++k) v = fma(__ldcg(a.inv + k * kP + tid), sy[k], v);
-        a.b[tid] = v;
+  if (cta == 0) {
+    if (G > 1) cta_wait(arrivals, 1u + (unsigned)G * (unsigned)npan, a.info, false);
+    if (__ldcg(a.info) == 0) {
+      const int p = npan - 1, k0 = p * kP, kb = N - k0;
+      if (npan > 1) {
+        if (tid < kb) a.b[k0 + tid] = __ldcg(a.wbuf + (size_t)(p % 3) * kP * (N + 1) + (size_t)N * kP + tid);
+      } else {
+        double* sy = s.dg;
+        if (tid < kP) sy[tid] = tid < kb ? __ldcg(a.b + tid) : 0.0;
+        __syncthreads();
+        if (tid < kb) {
+          double v = 0.0;
+          for (int k = 0; k < kb; ++k) v = fma(__ldcg(a.inv + k * kP + tid), sy[k], v);
+          a.b[tid] = v;
+        }
       }
     }
   }
+  (void)grid;
   GJ_PHASE(2)
 #undef GJ_PHASE
 }
@@ -711,14 +776,16 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   }
   const int npan = (N + kP - 1) / kP;
   double* inv = allocator().alloc((size_t)npan * kInv);
-  double* wbuf = allocator().alloc((size_t)2 * kP * (N + 1));
+  double* wbuf = allocator().alloc((size_t)3 * kP * (N + 1));
   static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
   unsigned long long* pbuf = nullptr;
   if (prof) {
     pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
     T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
   }
-  GjArgs a{N, A, b, inv, wbuf, info_dev, pbuf};  // *info zeroed by the kernel
+  unsigned* sync = reinterpret_cast<unsigned*>(allocator().alloc((size_t)(npan + 2) / 2 + 1));
+  T2S2_CUDA(cudaMemsetAsync(sync, 0, sizeof(unsigned) * (size_t)(npan + 2), stream()));
+  GjArgs a{N, A, b, inv, wbuf, info_dev, sync, pbuf};  // *info zeroed by the kernel
   void* params[] = {&a};
   {
     // algorithmic: N^3 (Gauss-Jordan) + 2 N^2; bytes: one read and write of the matrix
@@ -728,6 +795,7 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   }
   allocator().release(inv);
   allocator().release(wbuf);
+  allocator().release(reinterpret_cast<double*>(sync));
   if (prof) {
     unsigned long long h[16];
     T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));

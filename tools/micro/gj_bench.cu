@@ -107,13 +107,13 @@ int main() {
   cudaMalloc(&A, sizeof(double) * N * N);
   cudaMalloc(&b, sizeof(double) * N);
   cudaMalloc(&inv, sizeof(double) * 64 * kInv);
-  cudaMalloc(&wbuf, sizeof(double) * 2 * kP * (N + 1));
+  cudaMalloc(&wbuf, sizeof(double) * 3 * kP * (N + 1));
   cudaMalloc(&info, 4);
   cudaMalloc(&cyc, 16);
   cudaMemset(A, 0, sizeof(double) * N * N);
   cudaMemset(inv, 0, sizeof(double) * 64 * kInv);
-  cudaMemset(wbuf, 0, sizeof(double) * 2 * kP * (N + 1));
-  GjArgs a{N, A, b, inv, wbuf, info, nullptr};
+  cudaMemset(wbuf, 0, sizeof(double) * 3 * kP * (N + 1));
+  GjArgs a{N, A, b, inv, wbuf, info, nullptr, nullptr};
   const int smem = sizeof(Smem);
   cudaFuncSetAttribute(diag_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(tile_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
