@@ -93,6 +93,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ void gj_fail(const GjArgs& a) { atomicExch(a.info, -1); }
 
+// named CTA barriers (id 0 is __syncthreads)
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // Phase hand-off without a grid-wide barrier: every CTA adds one arrival per
 // phase (CTA 0 after factoring the next diagonal block, the others after
 // their tile tasks); a CTA waits for a count of arrivals, or — CTA 0 — only
@@ -478,12 +486,15 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
 //      row st of U is final, then Z[:, j>st] -= Y[:, st] U[st, j].
 // Group g (steps 4g..4g+3) is warp g's own columns: that warp factors it
 // alone — pivot rows and the pivot by shuffles, registers only — and
-// publishes the group's four multiplier columns and four Y columns; after
-// ONE CTA barrier every other warp applies the group to its columns as four
-// shuffle mini-steps (the pivot rows are in lane st of the same warp).
-// Eight barriers per block instead of 32: a shared-memory round trip
-// through a CTA barrier costs ~200 cycles on B200 and dominated the
-// step-per-barrier version (24.6k -> 14.1k cycles, tools/micro/gj_bench.cu).
+// publishes the group's four multiplier columns and four Y columns.  The
+// next owner (warp g + 1) takes each step through a two-warp named barrier
+// as soon as it is published, so it starts its own group right after the
+// last one; every other warp waits at one named barrier per group and
+// applies the four steps as shuffle mini-steps (the pivot rows are in lane
+// st of the same warp).  Measured (tools/micro/gj_bench.cu): one CTA
+// barrier per step 24.6k cycles, per group 14.1k, with the pipelined
+// next-owner hand-off 10.5k (a shared-memory round trip through a CTA
+// barrier costs ~200 cycles on B200).
 // Rolled over the groups: this runs once per panel between tile phases and
 // must stay small in the instruction cache.  Then D^{-1} = U^{-1} L^{-1} by
 // DMMA.
@@ -513,9 +524,17 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
   // l and the four U^{-1} columns y; after ONE barrier every other warp
   // applies the group to its own columns as four shuffle mini-steps
   // (pivot rows from lane st of the same warp).
+  // Hand-offs by named barriers: the owner of group g hands each step's
+  // columns to the owner of group g + 1 through a two-warp barrier (ids
+  // 3..10), which applies it at once and starts its own group as soon as
+  // group g is complete; every other warp waits at the group barrier (ids
+  // 1, 2: all warps but the next owner) and applies the four steps then.
 #pragma unroll 1
   for (int grp = 0; grp < kP / 4; ++grp) {
     const int st0 = 4 * grp, par = grp & 1;
+    const bool has_next = grp + 1 < kP / 4;
+    const int gbar = 1 + par, gcount = has_next ? kThr - 32 : kThr;
+    const int pbar0 = 3 + 4 * par;
     if (g == grp) {
 #pragma unroll
       for (int sidx = 0; sidx < 4; ++sidx) {
@@ -528,6 +547,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
         ok = ok && fabs(l) <= kPivThresh;
         s.gl[par][sidx][i] = l;
         s.gy[par][sidx][i] = y;
+        if (has_next) named_arrive(pbar0 + sidx, 64);
         if (i <= st) zv[sidx] = y;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -541,9 +561,23 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
           }
         }
       }
-    }
-    __syncthreads();
-    if (g != grp) {
+      named_arrive(gbar, gcount);
+    } else if (g == grp + 1) {
+      // next owner: each step as soon as it is published
+#pragma unroll
+      for (int sidx = 0; sidx < 4; ++sidx) {
+        const int st = st0 + sidx;
+        named_sync(pbar0 + sidx, 64);
+        const double l = s.gl[par][sidx][i], y = s.gy[par][sidx][i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double u = __shfl_sync(0xffffffffu, dv[q], st);
+          dv[q] = fma(-l, u, dv[q]);
+          zv[q] = fma(-y, u, zv[q]);
+        }
+      }
+    } else {
+      named_sync(gbar, gcount);
 #pragma unroll
       for (int sidx = 0; sidx < 4; ++sidx) {
         const int st = st0 + sidx;
@@ -565,6 +599,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
       }
     }
   }
+  __syncthreads();
   GJ_T(1)
   if (!ok) gj_fail(a);
   // D^{-1} = U^{-1} L^{-1} (DMMA, 32 x 32 x 32); publish D^{-1} and U^{-1}
