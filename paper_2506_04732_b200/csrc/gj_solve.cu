@@ -193,7 +193,7 @@ struct Smem {
   double ws[kT * kLdP];   // W = D^{-1} A[p, J] (32 x n): B operand [n*kLdP + k]
   double dg[kP * 33];     // diagonal block being factored, [c*33 + r]
   double za[kP * kLdP], xb[kP * kLdP];  // U^{-1}, L^{-1} as DMMA operands (gj_diag)
-  double gl[2][4][kP], gy[2][4][kP];  // gj_diag: a group's l and y columns (double buffered)
+  double gl[kP / 4][4][kP], gy[kP / 4][4][kP];  // gj_diag: each group's l and y columns
 };
 
 // Load D^{-1}, U^{-1} of panel p into shared memory.
@@ -531,7 +531,9 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
   // 1, 2: all warps but the next owner) and applies the four steps then.
 #pragma unroll 1
   for (int grp = 0; grp < kP / 4; ++grp) {
-    const int st0 = 4 * grp, par = grp & 1;
+    // one buffer per group: the next owner moves on to produce group g + 2
+    // while other warps may still read group g
+    const int st0 = 4 * grp, par = grp & 1, buf = grp;
     const bool has_next = grp + 1 < kP / 4;
     const int gbar = 1 + par, gcount = has_next ? kThr - 32 : kThr;
     const int pbar0 = 3 + 4 * par;
@@ -545,8 +547,8 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
         const double l = i > st ? dv[sidx] * rinv : 0.0;   // multiplier l_{i,st}
         const double y = i <= st ? zv[sidx] * rinv : 0.0;  // (U^{-1})_{i,st}
         ok = ok && fabs(l) <= kPivThresh;
-        s.gl[par][sidx][i] = l;
-        s.gy[par][sidx][i] = y;
+        s.gl[buf][sidx][i] = l;
+        s.gy[buf][sidx][i] = y;
         if (has_next) named_arrive(pbar0 + sidx, 64);
         if (i <= st) zv[sidx] = y;
 #pragma unroll
@@ -568,7 +570,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
       for (int sidx = 0; sidx < 4; ++sidx) {
         const int st = st0 + sidx;
         named_sync(pbar0 + sidx, 64);
-        const double l = s.gl[par][sidx][i], y = s.gy[par][sidx][i];
+        const double l = s.gl[buf][sidx][i], y = s.gy[buf][sidx][i];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const double u = __shfl_sync(0xffffffffu, dv[q], st);
@@ -581,7 +583,7 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
 #pragma unroll
       for (int sidx = 0; sidx < 4; ++sidx) {
         const int st = st0 + sidx;
-        const double l = s.gl[par][sidx][i], y = s.gy[par][sidx][i];
+        const double l = s.gl[buf][sidx][i], y = s.gy[buf][sidx][i];
         if (g > grp) {  // columns ahead: D and Z
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
