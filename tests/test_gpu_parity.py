@@ -475,3 +475,19 @@ def test_norm_and_round_wide_cores(pk, rank):
     full_ok = float(np.prod([float(c.shape[1]) for c in s])) <= 2e6
     if full_ok:
         assert np.linalg.norm(ot.tt_full(r.cores) - ot.tt_full(ro)) <= 1e-9 * np.linalg.norm(ot.tt_full(ro))
+
+
+@pytest.mark.parametrize("n", [264, 1601, 1848])
+def test_dense_local_solve_deterministic(pk, n):
+    """The Gauss-Jordan solve hands panels between CTAs and warps without
+    grid barriers (arrival counts, named barriers): repeated solves of one
+    system must be bit-identical (N = 1601: a one-row last panel)."""
+    from paper_2506_04732_b200 import _native
+
+    rng = np.random.default_rng(7 + n)
+    a = rng.standard_normal((n, n))
+    a += np.diag(np.abs(a).sum(0))
+    b = rng.standard_normal(n)
+    ref = _native.dense_solve(a, b)
+    for _ in range(8):
+        assert np.array_equal(_native.dense_solve(a, b), ref)
