@@ -1,4 +1,4 @@
-// Dense fp64 kernels: tiled GEMM (FFMA), permutation, vector ops and
+// Dense fp64 kernels: tiled GEMM (DMMA), permutation, vector ops and
 // deterministic reductions.
 #include "blas.h"
 
@@ -6,31 +6,53 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
 namespace t2s2 {
 
 // ---------------------------------------------------------------------------
-// GEMM: 64x64 output tile per CTA, BK = 16, 256 threads, 4x4 per thread.
-// Operands are staged through shared memory with bounds checks so the same
+// GEMM: 32x32x32 or 64x64x16 output tiles per CTA, 256 threads (8 warps of
+// DMMA).  Operands are staged through shared memory with bounds checks so the same
 // kernel serves the many tiny contractions of the sweep as well as the
 // larger trailing updates.
 // ---------------------------------------------------------------------------
 
 namespace {
 
-// Tile TM x TN x TK, 256 threads on a 16x16 grid (RM x RN outputs each).
-// The next K-tile is fetched into registers while the current one is
-// consumed from shared memory, so each tile costs one exposed L2 latency at
-// most; small problems use 32x32x32 tiles to spread over more SMs.
-// FP64 tensor-core MMA (DMMA, mma.sync m8n8k4): D[8x8] += A[8x4] B[4x8].
-// Fragments: lane holds A[lane/4][lane%4], B[lane%4][lane/4],
-// C/D[lane/4][2*(lane%4) + {0,1}].
+// Tile TM x TN x TK, 256 threads, FP64 tensor-core MMA (DMMA, mma.sync
+// m8n8k4): D[8x8] += A[8x4] B[4x8].  Fragments: lane holds A[lane/4][lane%4],
+// B[lane%4][lane/4], C/D[lane/4][2*(lane%4) + {0,1}].
+// Operand K-tiles are staged by cp.async (8-byte elements, zero-filled out
+// of bounds) through a kStages-deep shared-memory ring: kStages - 1 K-tiles
+// are in flight while one is consumed, so a long-K tile costs about one
+// exposed L2 latency in total instead of one per K-tile (the chains of the
+// sweep are 1-12 K-tiles of 32 on a handful of CTAs).  The DMMA sequence and
+// its operands are the same as with a single register prefetch, so results
+// are bit-identical.
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+constexpr int kStages = 4;
+// dynamic shared memory of the GEMM program: the larger of the two tile rings
+constexpr int kGemmSmem = kStages * 8 * (32 * (32 + 4) * 2 > 16 * (64 + 4) * 2
+                                             ? 32 * (32 + 4) * 2
+                                             : 16 * (64 + 4) * 2);
+
+__device__ __forceinline__ void cp_async8(unsigned dst, const double* src, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(pred ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // Row offset of a 2-level row index: i -> (i / d) * hi + (i % d) * lo.
@@ -42,13 +64,12 @@ __device__ __forceinline__ long long row_off(int i, int d, long long hi, long lo
 // One TM x TN output tile (tile coordinates bx, by of batch entry bz) of a
 // general GEMM: A(i,k) = A[row(i) + k*ak], B(k,j) = B[k*bk + j*bj],
 // C(i,j) = C[crow(i) + j*cj] (row() two-level, see GemmProb).  Operand
-// tiles are fetched with consecutive threads on the contiguous index, into
-// registers one K-tile ahead of the DMMA on shared memory.
+// tiles are fetched with consecutive threads on the contiguous index.
 template <int TM, int TN, int TK>
-__device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz) {
+__device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz, double* smem) {
   constexpr int PA = TM * TK / 256, PB = TK * TN / 256;
-  __shared__ double As[TK][TM + 4];  // +4: conflict-free DMMA fragment loads
-  __shared__ double Bs[TK][TN + 4];
+  constexpr int LA = TM + 4, LB = TN + 4;  // +4: conflict-free DMMA fragment loads
+  constexpr int SA = TK * LA, SS = TK * (LA + LB);  // per stage: A tile then B tile
   const double* A = g.A + bz * g.sA;
   const double* B = g.B + bz * g.sB;
   double* C = g.C + bz * g.sC;
@@ -57,65 +78,83 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
   const int tid = threadIdx.x;
   const bool a_ifast = g.alo == 1;  // rows contiguous: threads walk i
   const bool b_jfast = g.bj == 1;
-  // loop-invariant per-thread row offsets
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  // loop-invariant per-thread source offsets and shared-memory slots
   long long aoff[PA];
-  int ai[PA], akk[PA];
+  int akk[PA];
+  unsigned adst[PA];
+  bool arow[PA];
 #pragma unroll
   for (int t = 0; t < PA; ++t) {
     const int e = tid + t * 256;
-    ai[t] = a_ifast ? e % TM : e / TK;
+    const int ai = a_ifast ? e % TM : e / TK;
     akk[t] = a_ifast ? e / TM : e % TK;
-    const int gi = row0 + ai[t];
-    aoff[t] = gi < M ? row_off(gi, g.ad, g.ahi, g.alo) : 0;
+    const int gi = row0 + ai;
+    arow[t] = gi < M;
+    aoff[t] = (arow[t] ? row_off(gi, g.ad, g.ahi, g.alo) : 0) + (long long)akk[t] * g.ak;
+    adst[t] = sbase + 8u * (unsigned)(akk[t] * LA + ai);
   }
-  int bkk[PB], bjj[PB];
+  int bkk[PB];
+  bool bcol[PB];
+  long long boff[PB];
+  unsigned bdst[PB];
 #pragma unroll
   for (int t = 0; t < PB; ++t) {
     const int e = tid + t * 256;
-    bjj[t] = b_jfast ? e % TN : e / TK;
+    const int bj = b_jfast ? e % TN : e / TK;
     bkk[t] = b_jfast ? e / TN : e % TK;
+    const int gj = col0 + bj;
+    bcol[t] = gj < N;
+    boff[t] = (long long)bkk[t] * g.bk + (bcol[t] ? (long long)gj * g.bj : 0);
+    bdst[t] = sbase + 8u * (unsigned)(SA + bkk[t] * LB + bj);
   }
-  double ra[PA], rb[PB];
-  auto fetch = [&](int k0) {
+  const int nk = (K + TK - 1) / TK;
+  auto issue = [&](int kt) {  // K-tile kt into ring slot kt % kStages (always commits a group)
+    if (kt < nk) {
+      const int k0 = kt * TK;
+      const unsigned so = 8u * (unsigned)((kt % kStages) * SS);
 #pragma unroll
-    for (int t = 0; t < PA; ++t) {
-      const int gi = row0 + ai[t], gk = k0 + akk[t];
-      ra[t] = (gi < M && gk < K) ? A[aoff[t] + (long long)gk * g.ak] : 0.0;
-    }
+      for (int t = 0; t < PA; ++t) {
+        const bool ok = arow[t] && k0 + akk[t] < K;
+        cp_async8(adst[t] + so, ok ? A + aoff[t] + (long long)k0 * g.ak : A, ok);
+      }
 #pragma unroll
-    for (int t = 0; t < PB; ++t) {
-      const int gk = k0 + bkk[t], gj = col0 + bjj[t];
-      rb[t] = (gk < K && gj < N) ? B[(long long)gk * g.bk + (long long)gj * g.bj] : 0.0;
+      for (int t = 0; t < PB; ++t) {
+        const bool ok = bcol[t] && k0 + bkk[t] < K;
+        cp_async8(bdst[t] + so, ok ? B + boff[t] + (long long)k0 * g.bk : B, ok);
+      }
     }
+    cp_async_commit();
   };
   // 8 warps on a 4 x 2 grid of (TM/4) x (TN/2) warp tiles of 8x8 DMMA blocks
   constexpr int WM = TM / 4, WN = TN / 2, MB = WM / 8, NB = WN / 8;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * WN;
   double tc[MB][NB][2] = {};
-  fetch(0);
-  for (int k0 = 0; k0 < K; k0 += TK) {
 #pragma unroll
-    for (int t = 0; t < PA; ++t) As[akk[t]][ai[t]] = ra[t];
-#pragma unroll
-    for (int t = 0; t < PB; ++t) Bs[bkk[t]][bjj[t]] = rb[t];
-    __syncthreads();
-    if (k0 + TK < K) fetch(k0 + TK);
+  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kStages - 2>();  // this thread's copies of K-tile kt landed
+    __syncthreads();               // everyone's did, and slot (kt - 1) % kStages is free
+    issue(kt + kStages - 1);
+    const double* As = smem + (kt % kStages) * SS;
+    const double* Bs = As + SA;
 #pragma unroll
     for (int kk = 0; kk < TK; kk += 4) {
       const int kr = kk + (lane & 3);
       double af[MB], bf[NB];
 #pragma unroll
-      for (int i = 0; i < MB; ++i) af[i] = As[kr][wm0 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < MB; ++i) af[i] = As[kr * LA + wm0 + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) bf[j] = Bs[kr][wn0 + j * 8 + (lane >> 2)];
+      for (int j = 0; j < NB; ++j) bf[j] = Bs[kr * LB + wn0 + j * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < MB; ++i)
 #pragma unroll
         for (int j = 0; j < NB; ++j) dmma_8x8x4(tc[i][j][0], tc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();  // drain the (empty) trailing groups
+  __syncthreads();     // the ring is reused by the next tile
   const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
@@ -142,6 +181,7 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
 constexpr int kReduceTile = 4096;
 
 __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
+  extern __shared__ __align__(16) double gemm_smem[];
   cg::grid_group grid = cg::this_grid();
   if (prog.guard && *prog.guard == 0) return;  // uniform over the grid: flag set by an earlier kernel
   for (int s = 0; s < prog.nstage; ++s) {
@@ -169,11 +209,11 @@ __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant
       } else if (g.big) {
         const int tn = (g.N + 63) / 64, tm = (g.M + 63) / 64;
         const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
-        gemm_tile<64, 64, 16>(g, rem % tn, rem / tn, bz);
+        gemm_tile<64, 64, 16>(g, rem % tn, rem / tn, bz, gemm_smem);
       } else {
         const int tn = (g.N + 31) / 32, tm = (g.M + 31) / 32;
         const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
-        gemm_tile<32, 32, 32>(g, rem % tn, rem / tn, bz);
+        gemm_tile<32, 32, 32>(g, rem % tn, rem / tn, bz, gemm_smem);
       }
     }
     if (s + 1 < prog.nstage) grid.sync();
@@ -432,23 +472,49 @@ void GemmBatch::run() {
     }
     static int occ = 0;
     if (occ == 0) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_program_kernel, 256, 0);
+      T2S2_CUDA(cudaFuncSetAttribute(gemm_program_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_program_kernel, 256, kGemmSmem);
       if (occ < 1) occ = 1;
     }
     int grid = max_tiles < nsm * occ ? max_tiles : nsm * occ;
     if (sm_budget() > 0 && grid > sm_budget()) grid = sm_budget();
     if (grid < 1) grid = 1;
+    // T2S2_GEMM_TRACE=1: time each program alone and print its shape (development aid)
+    static const bool trace = getenv("T2S2_GEMM_TRACE") != nullptr;
+    cudaEvent_t te[2];
+    if (trace) {
+      cudaEventCreate(&te[0]);
+      cudaEventCreate(&te[1]);
+      cudaEventRecord(te[0], stream());
+    }
     {
       LaunchScope ls("gemm", flops_ * prog.nprob / (double)items_.size(), 0.0);
       if (prog.nstage == 1) {
-        gemm_program_kernel<<<grid, 256, 0, stream()>>>(prog);
+        gemm_program_kernel<<<grid, 256, kGemmSmem, stream()>>>(prog);
       } else {
         void* params[] = {&prog};
         T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gemm_program_kernel, dim3(grid), dim3(256),
-                                              params, 0, stream()));
+                                              params, kGemmSmem, stream()));
       }
     }
     T2S2_CHECK_LAUNCH();
+    if (trace) {
+      cudaEventRecord(te[1], stream());
+      cudaEventSynchronize(te[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, te[0], te[1]);
+      fprintf(stderr, "GEMMPROG us=%.2f grid=%d nstage=%d", ms * 1e3f, grid, prog.nstage);
+      for (int st = 0; st < prog.nstage; ++st) {
+        fprintf(stderr, " |");
+        for (int q = prog.stage_first[st]; q < prog.stage_first[st + 1]; ++q)
+          fprintf(stderr, " %dx%dx%d*%d/%d%s", prog.p[q].M, prog.p[q].N, prog.p[q].K, prog.p[q].batch,
+                  prog.p[q].tiles, prog.p[q].kind ? "R" : (prog.p[q].big ? "B" : ""));
+      }
+      fprintf(stderr, "\n");
+      cudaEventDestroy(te[0]);
+      cudaEventDestroy(te[1]);
+    }
   }
   items_.clear();
   temps_.clear();  // stream-ordered: safe to recycle once the launch is enqueued
