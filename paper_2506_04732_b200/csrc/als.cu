@@ -99,8 +99,11 @@ __global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
 // probe[0] += u.nu, probe[1] += c.u, probe[2] += #non-finite(u): one
 // deterministic two-level reduction per candidate (tt_solver.py:332-334 and
 // the isfinite check at :370/:398), read back together with the LU info.
-__global__ void probe_partial_kernel(const double* __restrict__ u, const double* __restrict__ nu,
-                                     const double* __restrict__ c, int n, double* part) {
+// One launch: the last CTA to arrive (ticket) sums the per-CTA partials in
+// CTA order and re-arms the ticket.
+__global__ void probe_kernel(const double* __restrict__ u, const double* __restrict__ nu,
+                             const double* __restrict__ c, int n, double* part,
+                             unsigned* ticket, double* out) {
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double x = u[i];
@@ -126,14 +129,19 @@ __global__ void probe_partial_kernel(const double* __restrict__ u, const double*
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[threadIdx.x][w];
     part[blockIdx.x * 3 + threadIdx.x] = t;
   }
-}
-
-__global__ void probe_final_kernel(const double* part, int nb, double* out) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   if (threadIdx.x < 3) {
     double t = 0.0;
-    for (int b = 0; b < nb; ++b) t += part[b * 3 + threadIdx.x];
+    for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + b * 3 + threadIdx.x);
     out[threadIdx.x] = t;
   }
+  if (threadIdx.x == 0) *ticket = 0u;
 }
 
 __global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
@@ -180,12 +188,6 @@ void bmm(bool ta, bool tb, int M, int N, int K, const double* A, int lda, long l
 }
 
 DTensor op_layout(const DTensor& ac) { return permute(ac, {1, 3, 0, 2}); }  // (m, A, a, n)
-
-DTensor ones(std::vector<int> shape) {
-  DTensor t(std::move(shape));
-  dfill(t.p, 1.0, t.size());
-  return t;
-}
 
 // Dimensions of an operator core (ra, nm, nn, rA).
 struct OpDims {
@@ -489,8 +491,10 @@ void lstsq_dense(const DTensor& Mcm, const DTensor& rhs, DTensor& out) {
 
 // Device scratch for candidate scores: 3 doubles per probe slot + LU info.
 struct Probe {
-  DTensor buf{std::vector<int>{16}};
+  DTensor buf{std::vector<int>{16}};  // 4 slots x 3, LU info at [12], ticket at [14]
+  Probe() { T2S2_CUDA(cudaMemsetAsync(buf.p, 0, 16 * sizeof(double), stream())); }
   int* info() { return reinterpret_cast<int*>(buf.p + 12); }
+  unsigned* ticket() { return reinterpret_cast<unsigned*>(buf.p + 14); }
   void clear_info() { T2S2_CUDA(cudaMemsetAsync(info(), 0, sizeof(int), stream())); }
   void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c) {
     const int n = (int)u.size();
@@ -499,11 +503,7 @@ struct Probe {
     double* part = allocator().alloc((size_t)nb * 3);
     {
       LaunchScope ls("reduce", 4.0 * n, 24.0 * n);
-      probe_partial_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part);
-    }
-    {
-      LaunchScope ls("reduce", 0, 0);
-      probe_final_kernel<<<1, 32, 0, stream()>>>(part, nb, buf.p + 3 * slot);
+      probe_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part, ticket(), buf.p + 3 * slot);
     }
     T2S2_CHECK_LAUNCH();
     allocator().release(part);
@@ -590,9 +590,7 @@ struct SplitSync {
   int read(const DTensor& s, const DTensor* zs, std::vector<double>& hz) {
     const int zk = zs ? zs->dim(0) : 0;
     DTensor buf({1 + kk + zk});
-    dcopy(buf.p, keep_mask.p, 1);
-    dcopy(buf.p + 1, s.p, kk);
-    if (zk) dcopy(buf.p + 1 + kk, zs->p, zk);
+    pack(buf.p, {{keep_mask.p, 1}, {s.p, (size_t)kk}, {zk ? zs->p : nullptr, (size_t)zk}});
     std::vector<double> h(1 + kk + zk);
     to_host(h.data(), buf.p, h.size());
     hz.assign(h.begin() + 1 + kk, h.end());
@@ -624,8 +622,7 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
   const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({keep, r1});
-  dcopy(out.carry.p, Vt.p, (size_t)keep * r1);
-  scale_rows(out.carry.p, keep, r1, r1, s.p);
+  copy_scaled(out.carry.p, r1, Vt.p, r1, keep, r1, s.p, nullptr);
   if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
@@ -634,8 +631,10 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
     out.extra = extra > 0 ? extra : 0;
   }
   out.core = DTensor({r0, n, keep + out.extra});
-  copy2d(out.core.p, keep + out.extra, U.p, kk, m, keep);
-  if (out.extra > 0) copy2d(out.core.p + keep, keep + out.extra, zu.p, zk, m, out.extra);
+  if (out.extra > 0)
+    copy2d_pair(out.core.p, keep + out.extra, U.p, kk, keep, zu.p, zk, out.extra, m);
+  else
+    copy2d(out.core.p, keep, U.p, kk, m, keep);
   return out;
 }
 
@@ -661,8 +660,7 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
   const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({r0, keep});
-  copy2d(out.carry.p, keep, U.p, kk, r0, keep);
-  scale_cols(out.carry.p, r0, keep, keep, s.p);
+  copy_scaled(out.carry.p, keep, U.p, kk, r0, keep, nullptr, s.p);
   if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
@@ -671,8 +669,7 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
     out.extra = extra > 0 ? extra : 0;
   }
   out.core = DTensor({keep + out.extra, n, r1});
-  dcopy(out.core.p, Vt.p, (size_t)keep * cols);
-  if (out.extra > 0) dcopy(out.core.p + (size_t)keep * cols, zvt.p, (size_t)out.extra * cols);
+  pack(out.core.p, {{Vt.p, (size_t)keep * cols}, {zvt.p, (size_t)out.extra * cols}});
   return out;
 }
 
@@ -683,8 +680,8 @@ double measure_residual(const Train& A, const std::vector<DTensor>& acg,
   const int d = A.d();
   // both Gram chains in one program (4 stages per core for <Ax,Ax>, 3 for <Ax,b>)
   GemmBatch gb;
-  DTensor phi = ones({1, 1, 1, 1});
-  DTensor psi = ones({1, 1, 1});
+  DTensor phi({1, 1, 1, 1}), psi({1, 1, 1});
+  fill_many({{phi.p, 1}, {psi.p, 1}}, 1.0);
   std::vector<DTensor> keep;
   for (int l = 0; l < d; ++l) {
     DTensor nphi = step_n_left(gb, 4 * l, phi, x[l], A.cores[l], acg[l]);
@@ -896,10 +893,18 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
 
   for (int sweep = 0; sweep < cfg.max_sweeps; ++sweep) {
     right_orthonormalize(cores);
-    sw.ra[d] = ones({1, 1, 1});
-    sw.rn[d] = ones({1, 1, 1, 1});
-    sw.rg[d] = ones({1, 1, 1});
-    sw.rb[d] = ones({1, 1});
+    // the boundary interfaces of both ends, one launch
+    sw.ra[d] = DTensor({1, 1, 1});
+    sw.rn[d] = DTensor({1, 1, 1, 1});
+    sw.rg[d] = DTensor({1, 1, 1});
+    sw.rb[d] = DTensor({1, 1});
+    sw.la[0] = DTensor({1, 1, 1});
+    sw.ln[0] = DTensor({1, 1, 1, 1});
+    sw.lg[0] = DTensor({1, 1, 1});
+    sw.lb[0] = DTensor({1, 1});
+    fill_many({{sw.ra[d].p, 1}, {sw.rn[d].p, 1}, {sw.rg[d].p, 1}, {sw.rb[d].p, 1},
+               {sw.la[0].p, 1}, {sw.ln[0].p, 1}, {sw.lg[0].p, 1}, {sw.lb[0].p, 1}},
+              1.0);
     {
       GemmBatch gb;  // all four chains over the cores: 4 stages per core
       for (int l = d - 1, s0 = 0; l > 0; --l, s0 += 4) {
@@ -910,10 +915,6 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       }
       gb.run();
     }
-    sw.la[0] = ones({1, 1, 1});
-    sw.ln[0] = ones({1, 1, 1, 1});
-    sw.lg[0] = ones({1, 1, 1});
-    sw.lb[0] = ones({1, 1});
 
     DTensor end_grad;  // residual gradient of the last forward visit
     int end_choice = 0;

@@ -285,6 +285,43 @@ __device__ double block_sum(double v) {
   return v;  // valid in warp 0
 }
 
+__global__ void copy_scaled_kernel(double* dst, int ldd, const double* src, int lds, int rows,
+                                   int cols, const double* rs, const double* cs) {
+  const int n = rows * cols;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    double v = src[(long long)r * lds + c];
+    if (rs) v *= rs[r];
+    if (cs) v *= cs[c];
+    dst[(long long)r * ldd + c] = v;
+  }
+}
+
+__global__ void copy2d_pair_kernel(double* dst, int ldd, const double* s1, int ld1, int c1,
+                                   const double* s2, int ld2, int c2, int rows) {
+  const int cols = c1 + c2, n = rows * cols;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int r = e / cols, c = e - r * cols;
+    dst[(long long)r * ldd + c] = c < c1 ? s1[(long long)r * ld1 + c] : s2[(long long)r * ld2 + c - c1];
+  }
+}
+
+struct Segments {
+  double* dst[8];
+  const double* src[8];
+  long long n[8];
+  int k;
+  double v;
+};
+
+// fill (src == null) or copy segments; blockIdx.y = segment
+__global__ void segments_kernel(Segments a) {
+  const int q = blockIdx.y;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < a.n[q];
+       e += (long long)gridDim.x * blockDim.x)
+    a.dst[q][e] = a.src[q] ? a.src[q][e] : a.v;
+}
+
 __global__ void dot_partial_kernel(const double* x, const double* y, long long n, double* part) {
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -683,6 +720,70 @@ void copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols
     copy2d_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols);
   }
   T2S2_CHECK_LAUNCH();
+}
+
+void copy_scaled(double* dst, int ldd, const double* src, int lds, int rows, int cols,
+                 const double* rs, const double* cs) {
+  long long n = (long long)rows * cols;
+  if (n <= 0) return;
+  {
+    LaunchScope ls("vector", (double)n, 16.0 * n);
+    copy_scaled_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols, rs, cs);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+void copy2d_pair(double* dst, int ldd, const double* s1, int ld1, int c1, const double* s2, int ld2,
+                 int c2, int rows) {
+  long long n = (long long)rows * (c1 + c2);
+  if (n <= 0) return;
+  {
+    LaunchScope ls("vector", 0, 16.0 * n);
+    copy2d_pair_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, s1, ld1, c1, s2, ld2, c2, rows);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+static void run_segments(Segments& a, long long most) {
+  if (a.k == 0) return;
+  {
+    LaunchScope ls("vector", 0, 8.0 * most);
+    segments_kernel<<<dim3(grid_for(most), a.k), 256, 0, stream()>>>(a);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+void fill_many(std::initializer_list<std::pair<double*, size_t>> arrays, double v) {
+  Segments a{};
+  a.v = v;
+  long long most = 0;
+  for (const auto& pr : arrays) {
+    if (!pr.second) continue;
+    if (a.k == 8) {
+      run_segments(a, most);
+      a.k = 0;
+      most = 0;
+    }
+    a.dst[a.k] = pr.first;
+    a.src[a.k] = nullptr;
+    a.n[a.k++] = (long long)pr.second;
+    most = std::max(most, (long long)pr.second);
+  }
+  run_segments(a, most);
+}
+
+void pack(double* dst, std::initializer_list<std::pair<const double*, size_t>> parts) {
+  Segments a{};
+  long long most = 0, off = 0;
+  for (const auto& pr : parts) {
+    if (!pr.second) continue;
+    a.dst[a.k] = dst + off;
+    a.src[a.k] = pr.first;
+    a.n[a.k++] = (long long)pr.second;
+    off += (long long)pr.second;
+    most = std::max(most, (long long)pr.second);
+  }
+  run_segments(a, most);
 }
 
 void ddot_dev(const double* x, const double* y, size_t n, double* out) {

@@ -2,6 +2,9 @@
 // tensordot, vector ops and deterministic reductions.
 #pragma once
 
+#include <initializer_list>
+#include <utility>
+
 #include "common.h"
 
 namespace t2s2 {
@@ -99,6 +102,17 @@ double dnrm2(const double* x, size_t n);
 
 // Copy a (rows x cols) block between row-major arrays with leading dims.
 void copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols);
+// dst[i, j] = src[i, j] * rs[i] * cs[j] (a null scale is 1; with one scale the
+// product is the single rounding of copy2d followed by scale_rows/scale_cols)
+void copy_scaled(double* dst, int ldd, const double* src, int lds, int rows, int cols,
+                 const double* rs, const double* cs);
+// dst[:, :c1] = s1, dst[:, c1:c1+c2] = s2 (rows x ...), one launch
+void copy2d_pair(double* dst, int ldd, const double* s1, int ld1, int c1, const double* s2, int ld2,
+                 int c2, int rows);
+// fill several arrays with one value in one launch (at most 8)
+void fill_many(std::initializer_list<std::pair<double*, size_t>> arrays, double v);
+// concatenate up to 4 device arrays into dst in one launch
+void pack(double* dst, std::initializer_list<std::pair<const double*, size_t>> parts);
 
 // out (cols x rows) = in^T for a row-major rows x cols matrix.
 void transpose(const double* in, double* out, int rows, int cols);

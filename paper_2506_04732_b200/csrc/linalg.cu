@@ -769,16 +769,24 @@ __global__ void __launch_bounds__(512)
         const int i = lane + 32 * r;
         vv[r] = (i >= j && i < mr) ? v[i] : 0.0;
       }
+      // the CPW columns' dot products and butterfly reductions interleaved
+      // (independent chains; each column's arithmetic is unchanged)
+      double w[CPW];
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) {
+        w[q] = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) w[q] = fma(vv[r], a[q][r], w[q]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) w[q] += __shfl_xor_sync(0xffffffffu, w[q], o);
 #pragma unroll
       for (int q = 0; q < CPW; ++q) {
         const int c = warp + q * nw;
         if (c > j && c < n) {
-          double w = 0.0;
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) w = fma(vv[r], a[q][r], w);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-          const double tw = t * w;
+          const double tw = t * w[q];
 #pragma unroll
           for (int r = 0; r < RPL; ++r) a[q][r] = fma(-tw, vv[r], a[q][r]);
         }

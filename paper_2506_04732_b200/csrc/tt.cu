@@ -188,8 +188,7 @@ Train tt_round(const Train& t, double tol, int max_rank) {
     DTensor nc(with_bonds(c, r0, r));
     copy2d(nc.p, r, U.p, kk, m, r);
     DTensor carry({r, r1});
-    dcopy(carry.p, Vt.p, (size_t)r * r1);
-    scale_rows(carry.p, r, r1, r1, s.p);
+    copy_scaled(carry.p, r1, Vt.p, r1, r, r1, s.p, nullptr);
     DTensor& nx = w[l + 1];
     const int rest = (int)((long long)nx.size() / r1);
     DTensor nn(with_bonds(nx, r, nx.dim(-1)));
