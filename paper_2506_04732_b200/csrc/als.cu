@@ -52,6 +52,60 @@ __global__ void galerkin_matrix_kernel(int rx, int n, int ry, int ra, int rb,
   }
 }
 
+// The same block, factored: T_a[(m,y),(nn,Y)] = sum_b ac[a,m,nn,b] par[y,b,Y]
+// does not depend on (x, X), so CTA c = (nn, Y) forms its slice of T for
+// every a in shared memory once and then writes the rx columns (X, nn, Y)
+// as B[(x,m,y), col] = sum_a pal[x,a,X] T_a[(m,y)] — per element ra fused
+// multiply-adds from shared memory instead of ra (rb + 1) plus the operand
+// loads and index divisions.  Every t and every s is formed by the same fma
+// sequence as galerkin_matrix_kernel above, so B is bit-identical.
+__global__ void __launch_bounds__(256)
+    galerkin_factored_kernel(int rx, int n, int ry, int ra, int rb, const double* __restrict__ pal,
+                             const double* __restrict__ ac, const double* __restrict__ par,
+                             double* __restrict__ B) {
+  extern __shared__ double gsm[];
+  const int nry = n * ry, N = rx * nry, tid = threadIdx.x;
+  double* T = gsm;             // ra x nry
+  double* P = T + ra * nry;    // pal, rx x ra x rx
+  for (int e = tid; e < rx * ra * rx; e += blockDim.x) P[e] = pal[e];
+  for (int c = blockIdx.x; c < nry; c += gridDim.x) {
+    const int nn = c / ry, Y = c - nn * ry;
+    __syncthreads();  // P loaded; the previous slice's readers are done
+    for (int e = tid; e < ra * nry; e += blockDim.x) {
+      const int a = e / nry, my = e - a * nry, m = my / ry, y = my - m * ry;
+      const double* acp = ac + (((long long)a * n + m) * n + nn) * rb;
+      const double* prp = par + (long long)y * rb * ry + Y;
+      double t = 0.0;
+      for (int b = 0; b < rb; ++b) t = fma(acp[b], prp[(long long)b * ry], t);
+      T[e] = t;
+    }
+    __syncthreads();
+    for (int X = 0; X < rx; ++X) {
+      double* Bc = B + ((long long)X * nry + c) * N;
+      int x = 0, my = tid;
+      while (my >= nry && x < rx) {
+        my -= nry;
+        ++x;
+      }
+      for (int row = tid; row < N; row += blockDim.x) {
+        const double* pl = P + (x * ra) * rx + X;
+        double s = 0.0;
+        for (int a = 0; a < ra; ++a) {
+          const double p = pl[a * rx];
+          if (p == 0.0) continue;
+          s = fma(p, T[a * nry + my], s);
+        }
+        Bc[row] = s;
+        my += blockDim.x;
+        while (my >= nry) {
+          my -= nry;
+          ++x;
+        }
+      }
+    }
+  }
+}
+
 // G[a,b,m,P,Q] = sum_k ac[a,k,m,P] ac[b,k,m,Q] (diagonal of A^T A per core).
 __global__ void gram_diag_kernel(int ra, int n, int rb, const double* __restrict__ ac,
                                  double* __restrict__ G) {
@@ -436,8 +490,20 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
   DTensor B({(int)N, (int)N});
   {
     LaunchScope ls("galerkin_build", 2.0*(double)N*N*ra*(rb+1), 8.0*(double)N*N);
-    galerkin_matrix_kernel<<<dim3(ceil_div(N, 256), N < 4096 ? (int)N : 4096), 256, 0, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p,
-                                                                  par.p, B.p);
+    const size_t smem = sizeof(double) * ((size_t)ra * n * ry + (size_t)rx * ra * rx);
+    if (smem <= 96 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        T2S2_CUDA(cudaFuncSetAttribute(galerkin_factored_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr = true;
+      }
+      galerkin_factored_kernel<<<n * ry, 256, smem, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p, par.p,
+                                                               B.p);
+    } else {
+      galerkin_matrix_kernel<<<dim3(ceil_div(N, 256), N < 4096 ? (int)N : 4096), 256, 0, stream()>>>(
+          rx, n, ry, ra, rb, pal.p, ac.p, par.p, B.p);
+    }
   }
   T2S2_CHECK_LAUNCH();
   return B;
