@@ -113,6 +113,26 @@ void resolve_pending(t2s2_context* c) {
 }
 }  // namespace
 cudaStream_t stream() { return g_ctx->stream; }
+bool profiling() { return g_ctx->profiling; }
+
+StatsMark stats_mark() {
+  StatsMark m;
+  for (const FamilyStat& f : g_ctx->fams) {
+    m.launches.push_back(f.launches);
+    m.flops.push_back(f.flops);
+    m.bytes.push_back(f.bytes);
+  }
+  return m;
+}
+
+void stats_replay(const StatsMark& before, const StatsMark& after, int times) {
+  for (size_t f = 0; f < after.launches.size() && f < g_ctx->fams.size(); ++f) {
+    const bool old = f < before.launches.size();
+    g_ctx->fams[f].launches += times * (after.launches[f] - (old ? before.launches[f] : 0));
+    g_ctx->fams[f].flops += times * (after.flops[f] - (old ? before.flops[f] : 0.0));
+    g_ctx->fams[f].bytes += times * (after.bytes[f] - (old ? before.bytes[f] : 0.0));
+  }
+}
 
 }  // namespace t2s2
 

@@ -107,6 +107,17 @@ struct LaunchScope {
 Allocator& allocator();  // the current context's allocator
 int sm_budget();         // CTAs a whole-GPU cooperative kernel may use (context setting)
 cudaStream_t stream();   // the current context's stream
+bool profiling();        // per-launch CUDA-event timing switched on (t2s2_stats_reset)
+
+// Launch statistics of a captured CUDA graph: mark before and after the
+// capture, then stats_replay(before, after, -1) once (captured launches did
+// not run) and stats_replay(before, after, +1) per graph launch.
+struct StatsMark {
+  std::vector<long long> launches;
+  std::vector<double> flops, bytes;
+};
+StatsMark stats_mark();
+void stats_replay(const StatsMark& before, const StatsMark& after, int times);
 
 // A dense row-major device array with a host-known shape.  Owns its
 // buffer (move-only).

@@ -506,6 +506,51 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
     T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_pre_kernel, dim3(G), dim3(kThreads), params,
                                           0, stream()));
   }
+  // One CUDA graph holds `poll` whole iterations (matvec program + update;
+  // every pointer is fixed for this solve and the kernels read their state
+  // from the device), captured once and replayed between host polls: the
+  // host no longer builds and launches two cooperative kernels per
+  // iteration.  Iterations after convergence are device no-ops, as without
+  // the graph.  The remainder below a multiple of `poll` runs eagerly.
+  static bool graphs_ok = getenv("T2S2_NO_GRAPH") == nullptr && getenv("T2S2_GEMM_TRACE") == nullptr;
+  if (graphs_ok && !profiling() && maxiter >= 2 * poll) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const StatsMark before = stats_mark();
+    bool captured = false;
+    T2S2_CUDA(cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal));
+    try {
+      for (int k = 0; k < poll; ++k) {
+        A(p, q, &st->active);
+        int itv = k;
+        void* params[] = {&st, &q, &x, &r, &diag, &p, &n, &at, &itv, &part};
+        LaunchScope ls("cg", 12.0 * n, 88.0 * n);
+        T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_step_kernel, dim3(G), dim3(kThreads),
+                                              params, 0, stream()));
+      }
+      captured = true;
+    } catch (const Error&) {
+    }
+    const cudaError_t ec = cudaStreamEndCapture(stream(), &graph);
+    if (captured && ec == cudaSuccess && graph &&
+        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+      const StatsMark after = stats_mark();
+      stats_replay(before, after, -1);
+      for (; it + poll <= maxiter; it += poll) {
+        if (it > 0 && !read_flag(&st->active)) break;
+        T2S2_CUDA(cudaGraphLaunch(exec, stream()));
+        stats_replay(before, after, 1);
+      }
+    } else {
+      // capture unsupported here: run eagerly from now on
+      graphs_ok = false;
+      const StatsMark after = stats_mark();
+      stats_replay(before, after, -1);
+      (void)cudaGetLastError();
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
   for (; it < maxiter; ++it) {
     if (it > 0 && it % poll == 0 && !read_flag(&st->active)) break;
     A(p, q, &st->active);  // skipped on the device once converged
