@@ -678,9 +678,13 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
     const int gc = (int)(grad->size() / m);
     DTensor z = grad->clone();
     DTensor tmp({kk, gc});
-    gemm(true, false, kk, gc, m, 1.0, U.p, kk, z.p, gc, 0.0, tmp.p, gc);
-    scale_rows(tmp.p, kk, gc, gc, sync.mask());
-    gemm(false, false, m, gc, kk, -1.0, U.p, kk, tmp.p, gc, 1.0, z.p, gc);
+    {
+      GemmBatch gb;  // tmp = diag(mask) U^T z, then z -= U tmp: one launch
+      gb.add(0, true, false, kk, gc, m, U.p, kk, 0, z.p, gc, 0, tmp.p, gc, 0);
+      gb.scale_last(sync.mask(), nullptr);
+      gb.add(1, false, false, m, gc, kk, U.p, kk, 0, tmp.p, gc, 0, z.p, gc, 0, 1, -1.0, 1.0);
+      gb.run();
+    }
     svd_thin(m, gc, z.p, zu, zs, zvt);
     zk = zs.dim(0);
   }
@@ -717,9 +721,13 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
     const int gr = (int)(grad->size() / cols);
     DTensor z = grad->clone();
     DTensor tmp({gr, kk});
-    gemm(false, true, gr, kk, cols, 1.0, z.p, cols, Vt.p, cols, 0.0, tmp.p, kk);
-    scale_cols(tmp.p, gr, kk, kk, sync.mask());
-    gemm(false, false, gr, cols, kk, -1.0, tmp.p, kk, Vt.p, cols, 1.0, z.p, cols);
+    {
+      GemmBatch gb;  // tmp = z Vt^T diag(mask), then z -= tmp Vt: one launch
+      gb.add(0, false, true, gr, kk, cols, z.p, cols, 0, Vt.p, cols, 0, tmp.p, kk, 0);
+      gb.scale_last(nullptr, sync.mask());
+      gb.add(1, false, false, gr, cols, kk, tmp.p, kk, 0, Vt.p, cols, 0, z.p, cols, 0, 1, -1.0, 1.0);
+      gb.run();
+    }
     svd_thin(gr, cols, z.p, zu, zs, zvt);
   }
   std::vector<double> hz;

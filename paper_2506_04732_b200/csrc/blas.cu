@@ -168,7 +168,14 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
         const int gj = col0 + wn0 + j * 8 + (lane & 3) * 2 + h;
         if (gj >= N) continue;
         double* c = C + co + (long long)gj * g.cj;
-        *c = beta == 0.0 ? alpha * tc[i][j][h] : alpha * tc[i][j][h] + beta * (*c);
+        if (g.rs || g.cs) {
+          double v = alpha * tc[i][j][h];
+          if (g.rs) v *= g.rs[gi];
+          if (g.cs) v *= g.cs[gj];
+          *c = v;
+        } else {
+          *c = beta == 0.0 ? alpha * tc[i][j][h] : alpha * tc[i][j][h] + beta * (*c);
+        }
       }
   }
 }
@@ -203,7 +210,14 @@ __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant
           for (int j = 0; j < g.batch; ++j) acc += g.A[j * mn + e];
           const int i = (int)(e / g.N), c = (int)(e - (long long)i * g.N);
           double* cp = g.C + row_off(i, g.cd, g.chi, g.clo) + (long long)c * g.cj;
-          *cp = g.beta == 0.0 ? g.alpha * acc : g.alpha * acc + g.beta * *cp;
+          if (g.rs || g.cs) {
+            double v = g.alpha * acc;
+            if (g.rs) v *= g.rs[i];
+            if (g.cs) v *= g.cs[c];
+            *cp = v;
+          } else {
+            *cp = g.beta == 0.0 ? g.alpha * acc : g.alpha * acc + g.beta * *cp;
+          }
         }
         __syncthreads();
       } else if (g.big) {
@@ -474,6 +488,17 @@ void GemmBatch::add_general(int stage, int M, int N, int K, const GemmOperand& a
     }
   }
   items_.push_back({2 * stage, g});
+}
+
+void GemmBatch::scale_last(const double* rs, const double* cs) {
+  // the last item is the problem itself or, after a split-K, its reduction
+  T2S2_REQUIRE(!items_.empty() && items_.back().g.beta == 0.0 &&
+                   (items_.back().g.kind == 1 ||
+                    (items_.back().g.batch == 1 && items_.back().g.ad == (1 << 30))) &&
+                   items_.back().g.cd == (1 << 30),
+               kErrShape, "GemmBatch::scale_last: plain beta = 0 problem expected");
+  items_.back().g.rs = rs;
+  items_.back().g.cs = cs;
 }
 
 void GemmBatch::run() {

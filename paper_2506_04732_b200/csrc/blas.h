@@ -38,6 +38,8 @@ struct GemmProb {
   int big;   // 64x64x16 tiles, else 32x32x32
   int kind;  // 0 GEMM; 1 split-K reduction: C = alpha sum_j A[j] + beta C (A: batch x M x N)
   double alpha, beta;
+  const double* rs;  // optional epilogue scales (beta == 0 only): C(i,j) = alpha acc rs[i] cs[j]
+  const double* cs;
 };
 
 struct GemmProgram {
@@ -66,6 +68,10 @@ class GemmBatch {
   void add_general(int stage, int M, int N, int K, const GemmOperand& a, const double* B,
                    long long bk, long long bj, long long sB, const GemmOperand& c, int batch = 1,
                    double alpha = 1.0, double beta = 0.0);
+  // scale the rows / columns of the last added problem's result (plain
+  // batch-1 problems with beta = 0; after a split-K the scales go to its
+  // reduction): the product of copy + scale_rows/cols
+  void scale_last(const double* rs, const double* cs);
   void run();
   void set_guard(const int* g) { guard_ = g; }
 
