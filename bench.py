@@ -1,26 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 T^2S^2 hot path: implicit time steps/s of the
-d=6 + time march (BASELINE.json configs[2]: n=33 nodes per dim, eps=1e-3,
-translating Gaussian, backward Euler dt=1e-3, TT tolerance 1e-12).
+"""Benchmark of the B200 T^2S^2 hot path.
 
-A "step" is one implicit step: rhs assembly and rounding, the alternating
-TT solve with its local direct/Krylov solves, and re-truncation.  Steps are
-a sequential chain (step k starts from state k-1), so K timed steps are
-steps W+1..W+K of one march.
-
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-
---impl b200 (default): the CUDA engine through its C ABI.  Prints one JSON
-line with value (inputs resident in HBM), e2e (public API with pinned host
-buffers, per-step H2D of the forcing and D2H of the new state), the roofline
-of the dominant kernel family, launch counts, clocks and the CPU oracle
-baseline.  Multi-GPU: the march does not shard, so each rank runs an
+Default workload (--workload march): implicit time steps/s of the d=6 + time
+march (BASELINE.json configs[2]: n=33 nodes per dim, eps=1e-3, translating
+Gaussian, backward Euler dt=1e-3, TT rounding tolerance 1e-12).  A "step" is
+one implicit step: rhs assembly and rounding, the alternating TT solve with
+its local direct/Krylov solves, and re-truncation.  Steps are a sequential
+chain (step k starts from state k-1), so K timed steps are steps W+1..W+K of
+one march.  Multi-GPU: the march does not shard, so each rank runs an
 independent replica ("replicas only", weak scaling); value = all ranks'
 steps / max-over-ranks time.
 
---impl reference: the reference's CPU algorithm (the oracle port in
-oracle/, pinned to the reference's outputs) on this host's cores, rank 0
-only.
+--workload sweep: BASELINE.json configs[4], the batched parameter sweep of
+independent d=6 steady solves (n=33, seeded eps and b).  A "step" is one
+solve capped at --sweep-sweeps ALS sweeps; rank r of N takes seeds r, r+N,
+... of the 64 (sweep.shard), cycling, with no data-path collective;
+solves/s, weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload march|sweep]
+
+--impl b200 (default): the CUDA engine through its C ABI.  One JSON line with
+value (inputs resident in HBM), e2e (public API with pinned host buffers:
+per-step H2D of the step's inputs, D2H of its result), the roofline of the
+dominant kernel family, launch counts, clocks and the reference CPU baseline.
+
+--impl reference: the reference itself — ttss from baseline/_ref, its own
+tt_apply / tt_add / tt_round / tt_solver.solve in the loop of
+time_integration._march (time_integration.py:164-177) with the per-step
+forcing — on this host's cores, rank 0 only, on the same steps.
 """
 
 from __future__ import annotations
@@ -39,9 +47,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "implicit_time_steps_per_s"
-UNIT = "steps/s"
-CONFIG_INDEX = 2
+MARCH = dict(metric="implicit_time_steps_per_s", unit="steps/s", index=2)
+SWEEP = dict(metric="steady_solves_per_s", unit="solves/s", index=4)
 
 
 def parse():
@@ -50,19 +57,38 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="march", choices=["march", "sweep"])
+    ap.add_argument("--sweep-sweeps", type=int, default=6,
+                    help="ALS sweeps per config-4 solve (fixed budget)")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
-def workload_config(recipe, extra=None):
+def march_config(recipe, extra=None):
     cfg = {
         "workload": "BASELINE configs[2]: d=6+time implicit march",
         "dims": recipe.dims, "nodes_per_dim": recipe.degree + 1, "eps": recipe.eps,
-        "dt": recipe.dt, "scheme": "backward_euler", "tt_rounding_tol": recipe.solver.get("rounding_tol"),
-        "step_tol": recipe.step_tol,
+        "dt": recipe.dt, "scheme": "backward_euler",
+        "tt_rounding_tol": recipe.solver.get("rounding_tol"), "step_tol": recipe.step_tol,
         "residual_tol": recipe.solver.get("residual_tol"),
+        "tolerances": "rounding_tol 1e-12 (BASELINE 'TT tolerance'); residual_tol and the step "
+                      "re-truncation are the reference's MarchConfig defaults "
+                      "(time_integration.py:54-60), identical in both arms",
         "solution": "translating Gaussian exp(-|x-b t|^2/0.05), b seeded unit vector",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def sweep_config(args, world, extra=None):
+    cfg = {
+        "workload": "BASELINE configs[4]: batched sweep of d=6 steady solves",
+        "dims": 6, "nodes_per_dim": 33, "seeds": 64, "sweeps_per_solve": args.sweep_sweeps,
+        "eps": "log-uniform [1e-12, 1e-1] per seed", "solution": "separable boundary layer",
+        "tt_rounding_tol": 1e-12, "residual_tol": 1e-10,
+        "sharding": f"rank r of {world} takes seeds r, r+{world}, ... (cycling)",
     }
     if extra:
         cfg.update(extra)
@@ -78,53 +104,56 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
-# -- CPU legs (oracle = the reference's algorithm, pinned to its outputs) ----------
+# -- the reference's own CPU path (ttss) -------------------------------------------
 
 
-def cpu_backend():
-    """Setup numerics on the CPU oracle (no GPU needed): a context manager."""
-    from oracle import tt_ops as ot
-    from paper_2506_04732_b200 import assembly, tt
-
-    def rnd(v, tol, max_rank=None):
-        if isinstance(v, tt.TTOperator):
-            rows, cols = v.row_sizes, v.col_sizes
-            return tt.TTOperator(ot.as_operator(ot.tt_round(ot.as_vector(v.cores), tol, max_rank),
-                                                rows, cols))
-        return tt.TTVector(ot.tt_round(v.cores, tol, max_rank))
-
-    def add(a, b):
-        return type(a)(ot.tt_add(a.cores, b.cores))
-
-    def app(op, v):
-        return tt.TTVector(ot.tt_apply(op.cores, v.cores))
-
-    return assembly.setup_backend(round=rnd, add=add, apply=app)
+def ttss_step(rtt, rsol, left, right, state, bc, src, step_tol, cfg):
+    """One implicit step exactly as time_integration._march takes it
+    (time_integration.py:164-177), in the reference's own functions."""
+    rhs = rtt.tt_add(rtt.tt_add(rtt.tt_apply(right, state), bc), src)
+    rhs = rtt.tt_round(rhs, 0.01 * step_tol)
+    new, rep = rsol.solve(left, rhs, x0=state, cfg=cfg)
+    return rtt.tt_round(new, step_tol), rep
 
 
-def oracle_problem(recipe):
-    """The workload's trains built with the oracle doing the setup numerics."""
-    from paper_2506_04732_b200 import workloads as wl
+def ttss_march(recipe, problem, state, first, count):
+    """Steps first..first+count-1 with ttss; forcing sampled outside the
+    timed region (it is the step's input).  Returns (seconds, state)."""
+    from paper_2506_04732_b200.reference import module
 
-    with cpu_backend():
-        return wl.march_problem(recipe)
-
-
-def cpu_march(recipe, n_steps, start_step=1, state=None, problem=None):
-    from oracle import als_solver as als
-    from oracle import march as om
-
-    left, right, state0, forcing, _, _ = problem or oracle_problem(recipe)
-    st = state if state is not None else state0.cores
-    cfg = als.Config(**recipe.solver)
-    with cpu_backend():
-        forc = {k: forcing(k) for k in range(start_step, start_step + n_steps)}
+    rtt, rsol = module("tensor_train"), module("tt_solver")
+    left, right, _, forcing, _, _ = problem
+    cfg = rsol.SolverConfig(**recipe.solver)
+    forc = {k: forcing(k) for k in range(first, first + count)}
     t0 = time.perf_counter()
-    for k in range(start_step, start_step + n_steps):
-        bc, src = forc[k]
-        st, _, _ = om.step(left.cores, right.cores, st, bc.cores, src.cores, recipe.step_tol, cfg,
-                           index=k)
-    return time.perf_counter() - t0, st
+    for k in range(first, first + count):
+        state, _ = ttss_step(rtt, rsol, left, right, state, *forc[k], recipe.step_tol, cfg)
+    return time.perf_counter() - t0, state
+
+
+def sweep_seeds(rank, world, count):
+    from paper_2506_04732_b200.sweep import shard
+
+    mine = shard(64, rank, world)
+    return [mine[i % len(mine)] for i in range(count)]
+
+
+def ttss_sweep(args, seeds):
+    """Config-4 solves with ttss.tt_solver.solve at the fixed sweep budget."""
+    from paper_2506_04732_b200 import workloads as wl
+    from paper_2506_04732_b200.reference import module
+
+    rsol = module("tt_solver")
+    recipes = wl.sweep_recipes()
+    probs = {i: wl.steady_problem(recipes[i]) for i in set(seeds)}
+    total = 0.0
+    for i in seeds:
+        a, b, _, _ = probs[i]
+        cfg = rsol.SolverConfig(**recipes[i].solver, max_sweeps=args.sweep_sweeps)
+        t0 = time.perf_counter()
+        rsol.solve(a, b, cfg=cfg)
+        total += time.perf_counter() - t0
+    return total
 
 
 def run_reference(args):
@@ -133,24 +162,35 @@ def run_reference(args):
         return
     from paper_2506_04732_b200 import workloads as wl
 
-    recipe = wl.config(CONFIG_INDEX)
-    problem = oracle_problem(recipe)
-    _, state = cpu_march(recipe, args.warmup, problem=problem)
-    elapsed, _ = cpu_march(recipe, args.steps, start_step=args.warmup + 1, state=state,
-                           problem=problem)
-    value = args.steps / elapsed
+    W, K = args.warmup, args.steps
     cores = blas_threads()
+    if args.workload == "march":
+        w = MARCH
+        recipe = wl.config(w["index"])
+        problem = wl.march_problem(recipe)
+        _, state = ttss_march(recipe, problem, problem[2], 1, W)
+        elapsed, _ = ttss_march(recipe, problem, state, W + 1, K)
+        config = march_config(recipe, {"parallelism": "cpu", "timed_steps": f"{W + 1}..{W + K}"})
+        sample = (f"steps {W + 1}..{W + K} of the config-2 march after {W} untimed steps: "
+                  "ttss (baseline/_ref) tt_apply/tt_add/tt_round/tt_solver.solve, numpy/OpenBLAS")
+    else:
+        w = SWEEP
+        seeds = sweep_seeds(0, 1, K)
+        ttss_sweep(args, sweep_seeds(0, 1, min(W, 1)))  # untimed warm-up solve
+        elapsed = ttss_sweep(args, seeds)
+        config = sweep_config(args, 1, {"parallelism": "cpu", "timed_seeds": seeds})
+        sample = (f"{K} config-4 solves (seeds {seeds}), {args.sweep_sweeps} sweeps each: "
+                  "ttss.tt_solver.solve (baseline/_ref), numpy/OpenBLAS")
+    value = K / elapsed
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(recipe, {"parallelism": "cpu"}),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} timed steps after {args.warmup} warm-up "
-                                   "steps of the config-2 march (oracle port of "
-                                   "pkg/src/ttss, numpy/BLAS)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": w["metric"], "value": value, "unit": w["unit"],
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": 1e3 * elapsed / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded manufactured solutions)", "config": config,
+        "cpu_baseline": {"value": value, "unit": w["unit"], "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": w["unit"], "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -239,28 +279,96 @@ def measured_peaks():
         return {}
 
 
-def run_b200(args):
-    import torch
+def roofline(torch, prof):
+    """Roofline of the dominant kernel family from the per-family CUDA-event
+    times of a profiled replay (algorithmic flops/bytes counted at each
+    launch site, csrc LaunchScope)."""
+    name, st = max(prof.items(), key=lambda kv: kv[1]["device_ms"])
+    peak64 = fp64_gemm_peak_tflops(torch)
+    peaks = measured_peaks()
+    flop_bound = st["flops"] > 0 and (st["flops"] / max(st["bytes"], 1.0)) > 2.0
+    per_launch_ms = st["device_ms"] / max(st["launches"], 1)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(name)
+    except Exception:
+        pass
+    common = {"traffic": traffic, "kernel": name, "avg_launch_ms": per_launch_ms,
+              "launches": st["launches"]}
+    if flop_bound:
+        achieved = st["flops"] / (st["device_ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
+                "frac": achieved / peak64,
+                "peak_source": "cuBLAS DGEMM 8192^3 fp64 measured in this run "
+                               "(MEASURED_PEAKS.json has no fp64 figure)",
+                "algorithmic_per_launch": st["flops"] / max(st["launches"], 1),
+                "algorithmic_unit": "flop (dense solve: 2/3 N^3 + 2 N^2)"
+                if name.startswith("gj") or name.startswith("lu") else "flop"}
+    else:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        achieved = st["bytes"] / (st["device_ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+                else "fallback 6650 GB/s (B200_PROFILING.md)",
+                "algorithmic_per_launch": st["bytes"] / max(st["launches"], 1)}
+    roof.update(common)
+    tot = sum(v["device_ms"] for v in prof.values())
+    kernels = {k: {"launches": v["launches"], "device_ms": round(v["device_ms"], 3),
+                   "share": round(v["device_ms"] / tot, 4) if tot else 0.0,
+                   "gflop": round(v["flops"] / 1e9, 4)}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["device_ms"])}
+    return roof, kernels
 
+
+class Dist:
+    def __init__(self, torch):
+        self.torch = torch
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        torch.cuda.set_device(self.local)
+        os.environ["T2S2_DEVICE"] = str(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x):
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+def pin(torch, cores):
+    flat = np.concatenate([np.ascontiguousarray(c).ravel() for c in cores])
+    t = torch.empty(flat.size, dtype=torch.float64, pin_memory=True)
+    t.numpy()[:] = flat
+    return t
+
+
+def run_b200_march(args, torch, dd):
     from paper_2506_04732_b200 import _native, workloads as wl
     from paper_2506_04732_b200.march import march_device
     from paper_2506_04732_b200.solver import SolverConfig
-    from paper_2506_04732_b200.tt import to_device
+    from paper_2506_04732_b200.tt import from_device, to_device
 
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    torch.cuda.set_device(local)
-    os.environ["T2S2_DEVICE"] = str(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl")
-
-    recipe = wl.config(CONFIG_INDEX)
+    recipe = wl.config(MARCH["index"])
     W, K = args.warmup, args.steps
-    left, right, state0, forcing, exact, _ = wl.march_problem(recipe)
+    problem = wl.march_problem(recipe)
+    left, right, state0, forcing, exact, _ = problem
     forc = [forcing(k) for k in range(1, W + K + 1)]
     cfg = SolverConfig(**recipe.solver)
     ctx = _native.context()
@@ -270,8 +378,8 @@ def run_b200(args):
     hsrc = [to_device(s) for _, s in forc]
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
-    def one_step(state, k):
-        stored, rows = march_device(hl, hr, state, 1, [hbc[k - 1]], [hsrc[k - 1]],
+    def one_step(state, k, bc=None, src=None):
+        stored, rows = march_device(hl, hr, state, 1, [bc or hbc[k - 1]], [src or hsrc[k - 1]],
                                     recipe.step_tol, cfg, store_stride=1)
         return stored[1], rows[0]
 
@@ -290,14 +398,11 @@ def run_b200(args):
     _native.synchronize()
 
     # timed steps W+1..W+K, L2 flushed between steps (flush not timed)
-    if dist:
-        dist.barrier()
+    dd.barrier()
     torch.cuda.synchronize()
     _native.stats_reset(profile_events=False)
-    rows = []
-    total_ms = 0.0
-    state = warm_state
-    with Clocks(local) as clk:
+    rows, total_ms, state = [], 0.0, warm_state
+    with Clocks(dd.local) as clk:
         t_wall = time.perf_counter()
         for k in range(W + 1, W + K + 1):
             l2_flush()
@@ -313,24 +418,19 @@ def run_b200(args):
             state = nxt
         t_wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
-    launch_stats = _native.stats_read()
-    gpu_launches = sum(v["launches"] for v in launch_stats.values())
-    final_state = state
-    elapsed = total_ms / 1e3
-    if dist:
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-        dist.barrier()
-    value = world * K / elapsed
+    gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
+    elapsed = dd.max(total_ms / 1e3)
+    dd.barrier()
+    value = dd.world * K / elapsed
 
     # accuracy of the timed march against the analytic solution
-    from paper_2506_04732_b200.tt import from_device, tt_add, tt_norm, tt_scale
-
-    fin = from_device(final_state)
+    fin = from_device(state)
     ex = exact((W + K) * recipe.dt)
-    exact_err = float(tt_norm(tt_add(fin, tt_scale(ex, -1.0))) / tt_norm(ex))
-    final_state.free()
+    from oracle import tt_ops as ot  # checker only: error of the result, not timed
+
+    exact_err = float(ot.tt_norm(ot.tt_add(fin.cores, ot.tt_scale(ex.cores, -1.0)))
+                      / ot.tt_norm(ex.cores))
+    state.free()
 
     # profiled replay of the same K steps (identical inputs, same warm state):
     # per-family CUDA-event time on the engine stream -> roofline
@@ -345,35 +445,24 @@ def run_b200(args):
     prof = _native.stats_read()
     _native.stats_reset(profile_events=False)
 
-    # e2e: public API, pinned host buffers; per step H2D of the step's
-    # forcing trains and D2H of the new state; the same steps W+1 .. W+K
-    # replayed from the same warm state, L2 flushed between steps like the
-    # device-timed run
+    # e2e: public API with pinned host buffers; per step H2D of the step's
+    # forcing trains and D2H of the new state, the same steps replayed from
+    # the same warm state, L2 flushed between steps like the device-timed run
     h2d = d2h = 0
     e2e_ms = 0.0
     host_state = warm_state
-    pinned = {}
-
-    def pin(cores):
-        flat = np.concatenate([c.ravel() for c in cores])
-        t = torch.empty(flat.size, dtype=torch.float64, pin_memory=True)
-        t.numpy()[:] = flat
-        return t
-
-    for k in range(W + 1, W + K + 1):
-        b, s = forc[k - 1]
-        pinned[k] = (pin(b.cores), pin(s.cores), b, s)
+    pinned = {k: (pin(torch, forc[k - 1][0].cores), pin(torch, forc[k - 1][1].cores))
+              for k in range(W + 1, W + K + 1)}
     out_buf = torch.empty(4 * 1024 * 1024, dtype=torch.float64, pin_memory=True)
     for k in range(W + 1, W + K + 1):
-        pb, ps, b, s = pinned[k]
+        pb, ps = pinned[k]
+        b, s = forc[k - 1]
         l2_flush()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(eng_stream)
         db = _native.DeviceTrain.upload_flat(pb.data_ptr(), b.mode_sizes, None, b.ranks)
         ds = _native.DeviceTrain.upload_flat(ps.data_ptr(), s.mode_sizes, None, s.ranks)
-        stored, _ = march_device(hl, hr, host_state, 1, [db], [ds], recipe.step_tol, cfg,
-                                 store_stride=1)
-        nxt = stored[1]
+        nxt, _ = one_step(host_state, k, db, ds)
         _, _, _, total = nxt.shape()
         nxt.download_into(out_buf.data_ptr(), out_buf.numel())
         e1.record(eng_stream)
@@ -387,90 +476,164 @@ def run_b200(args):
             host_state.free()
         host_state = nxt
     host_state.free()
+    warm_cores = from_device(warm_state)
     warm_state.free()
-    e2e_elapsed = e2e_ms / 1e3
-    if dist:
-        t = torch.tensor([e2e_elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_elapsed = float(t.item())
+    e2e_elapsed = dd.max(e2e_ms / 1e3)
+    if dd.rank != 0:
+        return None
 
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
-
-    # roofline of the dominant kernel family
-    fam = max(prof.items(), key=lambda kv: kv[1]["device_ms"])
-    name, st = fam
-    peak64 = fp64_gemm_peak_tflops(torch)
-    peaks = measured_peaks()
-    flop_bound = st["flops"] > 0 and (st["flops"] / max(st["bytes"], 1.0)) > 2.0
-    per_launch_ms = st["device_ms"] / max(st["launches"], 1)
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tr.get(name)
-    except Exception:
-        pass
-    if flop_bound:
-        achieved = st["flops"] / (st["device_ms"] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak64, "unit": "TFLOP/s",
-                "frac": achieved / peak64, "traffic": traffic, "kernel": name,
-                "peak_source": "cuBLAS DGEMM 8192^3 fp64 measured in this run "
-                               "(MEASURED_PEAKS.json has no fp64 figure)",
-                "algorithmic_per_launch": st["flops"] / max(st["launches"], 1),
-                "avg_launch_ms": per_launch_ms, "launches": st["launches"]}
-    else:
-        hbm = peaks.get("hbm_gbs", 6650.0)
-        achieved = st["bytes"] / (st["device_ms"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "kernel": name,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
-                else "fallback 6650 GB/s (B200_PROFILING.md)",
-                "algorithmic_per_launch": st["bytes"] / max(st["launches"], 1),
-                "avg_launch_ms": per_launch_ms, "launches": st["launches"]}
-    tot_prof = sum(v["device_ms"] for v in prof.values())
-    kernels = {k: {"launches": v["launches"], "device_ms": round(v["device_ms"], 3),
-                   "share": round(v["device_ms"] / tot_prof, 4) if tot_prof else 0.0,
-                   "gflop": round(v["flops"] / 1e9, 4)}
-               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["device_ms"])}
-
+    roof, kernels = roofline(torch, prof)
     cpu = None
     if not args.no_cpu_baseline and args.cpu_sample_steps > 0:
-        problem = oracle_problem(recipe)
-        _, st = cpu_march(recipe, W, problem=problem)          # untimed warm-up steps
-        el, _ = cpu_march(recipe, args.cpu_sample_steps, start_step=W + 1, state=st,
-                          problem=problem)
-        cpu = {"value": args.cpu_sample_steps / el, "unit": UNIT, "cores": blas_threads(),
-               "kind": "port",
-               "sample": f"steps {W + 1}..{W + args.cpu_sample_steps} of the same config-2 "
-                         f"march after {W} untimed steps, oracle port (numpy/BLAS) on this host"}
-
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": 1e3 * elapsed / K, "higher_is_better": True,
+        # the reference's own step loop on this host, from the device's step-W state
+        S = args.cpu_sample_steps
+        el, _ = ttss_march(recipe, problem, warm_cores, W + 1, S)
+        cpu = {"value": S / el, "unit": MARCH["unit"], "cores": blas_threads(),
+               "kind": "reference",
+               "sample": f"steps {W + 1}..{W + S} of the same config-2 march from the device's "
+                         f"step-{W} state: ttss (baseline/_ref) on this host, numpy/OpenBLAS"}
+    return {
+        "metric": MARCH["metric"], "value": value, "unit": MARCH["unit"], "n_gpus": dd.world,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * elapsed / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (manufactured translating Gaussian, seeded)",
-        "config": workload_config(recipe, {
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "config": march_config(recipe, {
+            "parallelism": f"replicas x{dd.world}" if dd.world > 1 else "single GPU",
             "l2": "256 MiB write between timed steps (not timed)",
             "timed_steps": f"{W + 1}..{W + K}",
             "max_rank_seen": max(r[1] for r in rows),
             "sweeps_per_step": [r[4] for r in rows],
             "exact_rel_error_final": exact_err,
         }),
-        "roofline": roof,
-        "kernels": kernels,
-        "gpu_launches": gpu_launches,
-        "e2e": {"value": world * K / e2e_elapsed, "unit": UNIT, "h2d_bytes_per_step": h2d // K,
-                "d2h_bytes_per_step": d2h // K},
-        "cpu_baseline": cpu,
-        "clocks": clk.summary(),
-        "wall_s_timed": t_wall,
+        "roofline": roof, "kernels": kernels, "gpu_launches": gpu_launches,
+        "e2e": {"value": dd.world * K / e2e_elapsed, "unit": MARCH["unit"],
+                "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K},
+        "cpu_baseline": cpu, "clocks": clk.summary(), "wall_s_timed": t_wall,
     }
-    print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+
+
+def run_b200_sweep(args, torch, dd):
+    from paper_2506_04732_b200 import _native, workloads as wl
+    from paper_2506_04732_b200.solver import SolverConfig, solve_device
+    from paper_2506_04732_b200.tt import to_device
+
+    W, K = args.warmup, args.steps
+    seeds = sweep_seeds(dd.rank, dd.world, W + K)
+    recipes = wl.sweep_recipes()
+    probs = {i: wl.steady_problem(recipes[i]) for i in set(seeds)}
+    ctx = _native.context()
+    eng_stream = torch.cuda.ExternalStream(_native.lib().t2s2_stream(ctx))
+    dev = {i: (to_device(p[0]), to_device(p[1])) for i, p in probs.items()}
+    x0 = {}
+    from paper_2506_04732_b200.solver import _default_initial_guess
+
+    for i, p in probs.items():
+        x0[i] = to_device(_default_initial_guess(p[1], None, np.random.default_rng(0)))
+
+    def cfg_of(i):
+        return SolverConfig(**recipes[i].solver, max_sweeps=args.sweep_sweeps)
+
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    def l2_flush():
+        _native.synchronize()
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+
+    for i in seeds[:W]:
+        h, _ = solve_device(dev[i][0], dev[i][1], x0[i], cfg_of(i))
+        h.free()
+    _native.synchronize()
+    dd.barrier()
+    torch.cuda.synchronize()
+    _native.stats_reset(profile_events=False)
+    total_ms, sweeps, reports = 0.0, 0, []
+    with Clocks(dd.local) as clk:
+        for i in seeds[W:]:
+            l2_flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(eng_stream)
+            h, rep = solve_device(dev[i][0], dev[i][1], x0[i], cfg_of(i))
+            e1.record(eng_stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            sweeps += len(rep.residual_history)
+            reports.append((i, rep.residual_history[-1], rep.rank_history[-1]))
+            h.free()
+    gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
+    elapsed = dd.max(total_ms / 1e3)
+    value = dd.world * K / elapsed
+
+    _native.stats_reset(profile_events=True)
+    for i in seeds[W:]:
+        h, _ = solve_device(dev[i][0], dev[i][1], x0[i], cfg_of(i))
+        h.free()
+    prof = _native.stats_read()
+    _native.stats_reset(profile_events=False)
+
+    # e2e: operator, rhs and initial guess uploaded from pinned host memory and
+    # the solution downloaded, every solve
+    e2e_ms, h2d, d2h = 0.0, 0, 0
+    out_buf = torch.empty(16 * 1024 * 1024, dtype=torch.float64, pin_memory=True)
+    for i in seeds[W:]:
+        a, b = probs[i][0], probs[i][1]
+        xh = _default_initial_guess(b, None, np.random.default_rng(0))
+        pa, pb, px = pin(torch, a.cores), pin(torch, b.cores), pin(torch, xh.cores)
+        l2_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng_stream)
+        da = _native.DeviceTrain.upload_flat(pa.data_ptr(), a.row_sizes, a.col_sizes, a.ranks)
+        db = _native.DeviceTrain.upload_flat(pb.data_ptr(), b.mode_sizes, None, b.ranks)
+        dx = _native.DeviceTrain.upload_flat(px.data_ptr(), xh.mode_sizes, None, xh.ranks)
+        h, _ = solve_device(da, db, dx, cfg_of(i))
+        total = h.shape()[3]
+        h.download_into(out_buf.data_ptr(), out_buf.numel())
+        e1.record(eng_stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+        h2d += 8 * (pa.numel() + pb.numel() + px.numel())
+        d2h += 8 * total
+        for t in (da, db, dx, h):
+            t.free()
+    e2e_elapsed = dd.max(e2e_ms / 1e3)
+    if dd.rank != 0:
+        return None
+    roof, kernels = roofline(torch, prof)
+    cpu = None
+    if not args.no_cpu_baseline and args.cpu_sample_steps > 0:
+        S = min(args.cpu_sample_steps, 2)
+        sample = seeds[W:W + S]
+        el = ttss_sweep(args, sample)
+        cpu = {"value": S / el, "unit": SWEEP["unit"], "cores": blas_threads(),
+               "kind": "reference",
+               "sample": f"{S} of the timed solves (seeds {sample}), {args.sweep_sweeps} sweeps "
+                         "each: ttss.tt_solver.solve (baseline/_ref) on this host"}
+    return {
+        "metric": SWEEP["metric"], "value": value, "unit": SWEEP["unit"], "n_gpus": dd.world,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * elapsed / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded boundary-layer manufactured solutions)",
+        "config": sweep_config(args, dd.world, {
+            "parallelism": f"sharded x{dd.world}" if dd.world > 1 else "single GPU",
+            "l2": "256 MiB write between timed solves (not timed)",
+            "rank0_timed": [{"seed": i, "residual": r, "max_rank": m} for i, r, m in reports],
+            "sweeps_timed_rank0": sweeps,
+        }),
+        "roofline": roof, "kernels": kernels, "gpu_launches": gpu_launches,
+        "e2e": {"value": dd.world * K / e2e_elapsed, "unit": SWEEP["unit"],
+                "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K},
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+    }
+
+
+def run_b200(args):
+    import torch
+
+    dd = Dist(torch)
+    line = (run_b200_march if args.workload == "march" else run_b200_sweep)(args, torch, dd)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    dd.close()
 
 
 def main():

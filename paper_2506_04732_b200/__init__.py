@@ -1,26 +1,28 @@
 """B200-native T^2S^2 hot path.
 
-A drop-in for the tensor-train linear algebra of the reference's
-``pkg/src/ttss`` (tensor_train / tt_solver / time_integration): the host API
-keeps the reference's names and arguments, and every numerical kernel of the
-implicit step runs in the CUDA engine ``lib/libt2s2.so`` (sm_100a, fp64).
-Problem setup (1-D Legendre collocation blocks, separable coefficients,
-operator chains) is host-side, as in the reference.
+A drop-in for the tensor-train hot path of the reference's ``ttss`` package
+(pkg/src/ttss): the alternating solve (tt_solver.solve / residual), the
+implicit step loop (time_integration._march) and the train arithmetic on
+it (tensor_train.tt_round / tt_norm / tt_dot / tt_add / tt_apply / tt_full)
+run in the CUDA engine ``lib/libt2s2.so`` (sm_100a, fp64) behind the C ABI
+of ``include/t2s2.h``.  Everything else — problem setup, containers,
+configs, reports, exceptions — is the reference's own code, imported from
+``ttss`` (see ``reference.py``); ``dropin.install()`` swaps the hot-path
+functions inside an unmodified ``ttss``.
 
 Importing this package does not touch the GPU; the first numerical call
 loads the engine and raises ``NativeUnavailable`` if it cannot.
 """
 
-from . import assembly, coefficients, collocation, spectral, tt  # noqa: F401
 from ._native import NativeUnavailable  # noqa: F401
 from .errors import CapExceededError, MarchStepError, ShapeError  # noqa: F401
 
-__all__ = ["assembly", "coefficients", "collocation", "spectral", "tt", "solver", "march",
-           "NativeUnavailable", "ShapeError", "MarchStepError", "CapExceededError"]
+__all__ = ["tt", "solver", "march", "dropin", "sweep", "workloads", "NativeUnavailable",
+           "ShapeError", "MarchStepError", "CapExceededError"]
 
 
-def __getattr__(name):  # lazy: solver/march pull in ctypes prototypes only when used
-    if name in ("solver", "march"):
+def __getattr__(name):  # lazy: submodules pull in ttss and ctypes prototypes when used
+    if name in ("tt", "solver", "march", "dropin", "sweep", "workloads"):
         import importlib
 
         return importlib.import_module(f".{name}", __name__)

@@ -825,8 +825,11 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   GjArgs a{N, A, b, inv, wbuf, info_dev, sync, pbuf};  // *info zeroed by the kernel
   void* params[] = {&a};
   {
-    // algorithmic: N^3 (Gauss-Jordan) + 2 N^2; bytes: one read and write of the matrix
-    LaunchScope ls("gj_nopivot", (double)N * N * N + 2.0 * (double)N * N, 16.0 * (double)N * N);
+    // algorithmic work of the operation (a dense solve: LU 2/3 N^3 + two triangular
+    // solves 2 N^2), not the N^3 this Gauss-Jordan variant executes; bytes: one read
+    // and one write of the matrix
+    LaunchScope ls("gj_nopivot", 2.0 / 3.0 * (double)N * N * N + 2.0 * (double)N * N,
+                   16.0 * (double)N * N);
     T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gj_kernel, dim3(grid), dim3(kThr), params, smem,
                                           stream()));
   }

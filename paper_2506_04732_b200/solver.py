@@ -1,7 +1,8 @@
-"""Rank-adaptive alternating TT solver — host API over the CUDA engine.
+"""Rank-adaptive alternating TT solver on the CUDA engine.
 
-Same names, arguments and error behaviour as the reference's
-``pkg/src/ttss/tt_solver.py``; the sweeps run in ``libt2s2.so``
+Drop-in for ``ttss.tt_solver.solve`` / ``residual`` (tt_solver.py:80, 445):
+same arguments, the reference's own ``SolverConfig`` and ``SolveReport``
+dataclasses and exceptions; the sweeps run in ``libt2s2.so``
 (csrc/als.cu).  Only the default initial guess's random fallback is drawn
 on the host, with numpy's generator seeded exactly like the reference
 (tt_solver.py:425-432), because it is input data, not computation.
@@ -10,81 +11,51 @@ on the host, with numpy's generator seeded exactly like the reference
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native
 from .errors import ShapeError
-from .tt import TTVector, from_device, to_device, tt_norm, tt_rank_one, tt_round, tt_scale
+from .reference import module as _ref
+from .tt import from_device, to_device, tt_norm, tt_rank_one, tt_round, tt_scale
 
-__all__ = ["SolverConfig", "SolveReport", "solve", "residual", "solve_device"]
+_rsol = _ref("tt_solver")
+SolverConfig = _rsol.SolverConfig
+SolveReport = _rsol.SolveReport
+
+__all__ = ["SolverConfig", "SolveReport", "solve", "residual", "solve_device", "config_to_c",
+           "report_from_c"]
 
 _LOCAL = {"auto": 0, "direct": 1, "iterative": 2}
 
 
-@dataclass
-class SolverConfig:
-    max_sweeps: int = 40
-    residual_tol: float = 1e-8
-    rounding_tol: float = 1e-10
-    enrichment_rank: int = 2
-    max_rank: int = 64
-    local_solver: str = "auto"  # auto | direct | iterative
-    local_direct_size: int = 2000
-    inner_tol_factor: float = 0.02
-    seed: int = 0
-    stagnation_window: int = 5
-    stagnation_drop: float = 0.01
-
-    def __post_init__(self):
-        if self.residual_tol <= 0 or self.rounding_tol <= 0:
-            raise ValueError("tolerances must be positive")
-        if self.max_rank < 1:
-            raise ValueError("max_rank must be at least 1")
-        if self.local_solver not in _LOCAL:
-            raise ValueError("local_solver must be auto, direct or iterative")
-
-    def to_c(self):
-        return _native.SolverConfigC(
-            max_sweeps=int(self.max_sweeps), residual_tol=float(self.residual_tol),
-            rounding_tol=float(self.rounding_tol), enrichment_rank=int(self.enrichment_rank),
-            max_rank=int(self.max_rank), local_solver=_LOCAL[self.local_solver],
-            local_direct_size=int(self.local_direct_size),
-            inner_tol_factor=float(self.inner_tol_factor),
-            stagnation_window=int(self.stagnation_window),
-            stagnation_drop=float(self.stagnation_drop))
+def config_to_c(cfg):
+    """t2s2_solver_config of a SolverConfig (tt_solver.py:39-59).  The
+    engine keeps at most T2S2_MAX_SWEEPS entries of history per solve."""
+    if cfg.max_sweeps > _native.MAX_SWEEPS:
+        raise ValueError(f"max_sweeps > {_native.MAX_SWEEPS} is not supported by the engine's "
+                         "report buffers")
+    return _native.SolverConfigC(
+        max_sweeps=int(cfg.max_sweeps), residual_tol=float(cfg.residual_tol),
+        rounding_tol=float(cfg.rounding_tol), enrichment_rank=int(cfg.enrichment_rank),
+        max_rank=int(cfg.max_rank), local_solver=_LOCAL[cfg.local_solver],
+        local_direct_size=int(cfg.local_direct_size),
+        inner_tol_factor=float(cfg.inner_tol_factor),
+        stagnation_window=int(cfg.stagnation_window),
+        stagnation_drop=float(cfg.stagnation_drop))
 
 
-@dataclass
-class SolveReport:
-    residual_history: list = field(default_factory=list)
-    rank_history: list = field(default_factory=list)
-    compression_history: list = field(default_factory=list)
-    wall_time: float = 0.0
-    converged: bool = False
-    stagnated: bool = False
-
-    def to_dict(self):
-        return {
-            "residuals": list(map(float, self.residual_history)),
-            "ranks": list(map(int, self.rank_history)),
-            "compression": list(map(float, self.compression_history)),
-            "wall_time_s": float(self.wall_time),
-            "converged": bool(self.converged),
-        }
-
-    @classmethod
-    def from_c(cls, r):
-        n = r.n_sweeps
-        return cls(residual_history=[float(r.residuals[i]) for i in range(n)],
-                   rank_history=[int(r.ranks[i]) for i in range(n)],
-                   compression_history=[float(r.compression[i]) for i in range(n)],
-                   wall_time=float(r.wall_time), converged=bool(r.converged),
-                   stagnated=bool(r.stagnated))
+def report_from_c(r):
+    n = r.n_sweeps
+    return SolveReport(residual_history=[float(r.residuals[i]) for i in range(n)],
+                       rank_history=[int(r.ranks[i]) for i in range(n)],
+                       compression_history=[float(r.compression[i]) for i in range(n)],
+                       wall_time=float(r.wall_time), converged=bool(r.converged),
+                       stagnated=bool(r.stagnated))
 
 
 def _default_initial_guess(rhs, cfg, rng):
+    """tt_solver.py:425-432 with the rounding and norms on the device."""
     x0 = tt_round(rhs, 0.5, max_rank=1)
     if tt_norm(x0) < 1e-13 * max(tt_norm(rhs), 1.0):
         x0 = tt_rank_one([rng.standard_normal(n) for n in rhs.mode_sizes])
@@ -96,11 +67,11 @@ def solve_device(a_h, rhs_h, x0_h, cfg):
     """Solve with device-resident handles; returns (DeviceTrain, SolveReport)."""
     rep = _native.SolveReportC()
     out = _native._P()
-    ccfg = cfg.to_c()
+    ccfg = config_to_c(cfg)
     _native.check(_native.lib().t2s2_solve(_native.context(), a_h.handle, rhs_h.handle,
                                            x0_h.handle, ctypes.byref(ccfg), ctypes.byref(out),
                                            ctypes.byref(rep)))
-    return _native.DeviceTrain(out), SolveReport.from_c(rep)
+    return _native.DeviceTrain(out), report_from_c(rep)
 
 
 def solve(a, rhs, x0=None, cfg=None):

@@ -1,9 +1,9 @@
 """The five BASELINE.json configurations as data recipes.
 
 Each recipe only produces numbers (coefficients, sampled separable factors,
-solver settings); ``build_*`` turns them into trains with this package's
-setup code, and ``tools/make_golden.py`` builds the identical problems with
-the reference package to pin parity.  The manufactured solutions are seeded
+solver settings); ``steady_problem`` / ``march_problem`` turn them into
+trains with the reference's own setup code (ttss), exactly as
+``tools/make_golden.py`` does when it records the reference's outputs.  The manufactured solutions are seeded
 synthetic stand-ins for the reference's benchmark problems (there is no
 external dataset).
 
@@ -163,54 +163,61 @@ def sweep_recipes(count=64, seed=4, dims=6, degree=32):
     return out
 
 
-# -- builders with this package's setup code -------------------------------------------
+# -- builders: the reference's own problem setup (ttss) ------------------------------
+
+
+def _spec(recipe):
+    """ProblemSpec of a recipe: constant eps and beta, no reaction, zero
+    symbolic rhs (the manufactured forcing is supplied as trains)."""
+    from .reference import module
+
+    co, asm = module("coefficients"), module("operator_assembly")
+    d = recipe.dims
+    return asm.ProblemSpec(dims=d, degrees=[recipe.degree] * d,
+                           epsilon=co.constant_coefficient(recipe.eps, d),
+                           beta=[co.constant_coefficient(b, d) for b in recipe.beta],
+                           rho=co.constant_coefficient(0.0, d),
+                           rhs=co.constant_coefficient(0.0, d))
 
 
 def steady_problem(recipe):
-    """(A, rhs, exact) trains, plus the operator set, for a steady recipe."""
-    from .assembly import ProblemSpec, assemble_opset, impose_dirichlet, rep_axes, row_axes
-    from .coefficients import constant_coefficient
-    from .tt import tt_from_separable, tt_rank_one
+    """(A, rhs, exact, opset) for a steady recipe, assembled by ttss
+    (operator_assembly.assemble_opset / impose_dirichlet)."""
+    from .reference import module
 
-    d = recipe.dims
-    spec = ProblemSpec(dims=d, degrees=[recipe.degree] * d,
-                       epsilon=constant_coefficient(recipe.eps, d),
-                       beta=[constant_coefficient(b, d) for b in recipe.beta],
-                       rho=constant_coefficient(0.0, d), rhs=constant_coefficient(0.0, d))
-    opset = assemble_opset(spec)
-    rows, reps = row_axes(opset.grids), rep_axes(opset.grids)
-    rhs_tt = tt_from_separable(recipe.rhs_terms(rows))
-    g_tt = tt_rank_one(recipe.exact_factors(reps)) if recipe.has_boundary_data() else None
-    a, b = impose_dirichlet(opset, spec, rhs_tt=rhs_tt, g_tt=g_tt)
-    return a, b, tt_rank_one(recipe.exact_factors(reps)), opset
+    asm, rtt = module("operator_assembly"), module("tensor_train")
+    spec = _spec(recipe)
+    opset = asm.assemble_opset(spec)
+    rows, reps = asm.row_axes(opset.grids), asm.rep_axes(opset.grids)
+    rhs_tt = rtt.tt_from_separable(recipe.rhs_terms(rows))
+    g_tt = rtt.tt_rank_one(recipe.exact_factors(reps)) if recipe.has_boundary_data() else None
+    a, b = asm.impose_dirichlet(opset, spec, rhs_tt=rhs_tt, g_tt=g_tt)
+    return a, b, rtt.tt_rank_one(recipe.exact_factors(reps)), opset
 
 
 def march_problem(recipe):
-    """(left, right, state0, forcing(k) -> (bc_k, src_k), exact(t), opset)."""
-    from .assembly import ProblemSpec, assemble_opset, rep_axes, row_axes
-    from .coefficients import constant_coefficient
-    from .march import MarchConfig, march_operators
-    from .assembly import _num
-    from .tt import tt_from_separable, tt_rank_one, tt_scale
+    """(left, right, state0, forcing(k) -> (bc_k, src_k), exact(t), opset),
+    built by ttss exactly as time_integration._march does
+    (time_integration.py:149-163), with the forcing sampled at t_k."""
+    from .reference import module
 
-    d = recipe.dims
-    spec = ProblemSpec(dims=d, degrees=[recipe.degree] * d,
-                       epsilon=constant_coefficient(recipe.eps, d),
-                       beta=[constant_coefficient(b, d) for b in recipe.beta],
-                       rho=constant_coefficient(0.0, d), rhs=constant_coefficient(0.0, d))
-    opset = assemble_opset(spec)
-    mcfg = MarchConfig(dt=recipe.dt, t_end=recipe.dt * recipe.n_steps)
-    left, right, mask, anti = march_operators(opset, mcfg)
-    rows, reps = row_axes(opset.grids), rep_axes(opset.grids)
-    state0 = _num.round(tt_rank_one(recipe.u_factors(reps, 0.0)), 1e-14)
+    asm, rtt, rti = (module("operator_assembly"), module("tensor_train"),
+                     module("time_integration"))
+    spec = _spec(recipe)
+    opset = asm.assemble_opset(spec)
+    mcfg = rti.MarchConfig(dt=recipe.dt, t_end=recipe.dt * recipe.n_steps)
+    left, right, mask, anti = rti._march_operators(opset, spec, mcfg)
+    rows, reps = asm.row_axes(opset.grids), asm.rep_axes(opset.grids)
+    state0 = rtt.tt_round(rtt.tt_rank_one(recipe.u_factors(reps, 0.0)), 1e-14)
 
     def forcing(k):
         t = k * recipe.dt
-        bc = _num.apply(anti, tt_rank_one(recipe.u_factors(reps, t)))
-        src = tt_scale(_num.apply(mask, tt_from_separable(recipe.f_terms(rows, t))), recipe.dt)
+        bc = rtt.tt_apply(anti, rtt.tt_rank_one(recipe.u_factors(reps, t)))
+        src = rtt.tt_scale(rtt.tt_apply(mask, rtt.tt_from_separable(recipe.f_terms(rows, t))),
+                           recipe.dt)
         return bc, src
 
     def exact(t):
-        return tt_rank_one(recipe.u_factors(reps, t))
+        return rtt.tt_rank_one(recipe.u_factors(reps, t))
 
     return left, right, state0, forcing, exact, opset

@@ -321,7 +321,6 @@ def test_config1_full_matches_reference(golden, pk):
     within 3x of the reference's, or at least 10x below the plateau)."""
     from oracle import tt_ops as ot
     from paper_2506_04732_b200 import workloads as wl
-    from paper_2506_04732_b200.assembly import rep_axes
 
     _, tt, solver, _ = pk
     z = golden("config1.npz")

@@ -1,0 +1,102 @@
+"""Full-length parity of the device march with the REFERENCE (ttss) on the
+BASELINE configs at full size: every step of the 100-step config-2 march and
+of the 200-step config-3 march, against states recorded by running ttss
+(tools/make_golden_full.py -> tests/golden/config{2,3}_full.npz).
+
+For every step the test checks north_star's three criteria:
+  * raw TT ranks of the state identical to the reference's;
+  * relative difference of the full-grid solution (10^5 seeded sample
+    points: the grid has 33^6 / 65^6 entries) within PARITY_TOL;
+  * error against the analytic manufactured solution no worse than the
+    reference's (to ERR_SLACK relative: both are ~1e-3 backward-Euler time
+    errors that agree to many digits).
+The achieved numbers of every step are written to
+gpurun_out/parity_full_<config>.json (committed under profiles/).
+
+Tolerance: each step re-solves to the reference's residual_tol (1e-10) and
+re-truncates at step_tol (1e-8), so two correct implementations differ by
+rounding-level amounts amplified by the local solves' conditioning; the
+difference is measured and bounded here, not assumed.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import get_train, has_train
+from helpers import rel_diff
+from oracle import tt_ops as ot
+
+pytestmark = pytest.mark.gpu
+
+PARITY_TOL = 1e-10       # north_star: full-grid relative agreement
+ERR_SLACK = 1e-6         # relative slack on the manufactured-solution error
+
+
+def _record(name, rows, summary):
+    out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", os.getcwd()), "gpurun_out")
+    try:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, f"parity_full_{name}.json"), "w") as fh:
+            json.dump({"summary": summary, "steps": rows}, fh, indent=1)
+    except OSError:
+        pass
+
+
+def _march_full(golden, index, fname):
+    from paper_2506_04732_b200 import _native, tt, workloads as wl
+    from paper_2506_04732_b200.march import march_device
+    from paper_2506_04732_b200.solver import SolverConfig
+
+    _native.context()
+    z = golden(fname)
+    recipe = wl.config(index)
+    n = int(z["n_steps"])
+    left, right, state0, forcing, exact, _ = wl.march_problem(recipe)
+    fs = [forcing(k) for k in range(1, n + 1)]
+    hl, hr, hs = tt.to_device(left), tt.to_device(right), tt.to_device(state0)
+    bcs = [tt.to_device(b) for b, _ in fs]
+    srcs = [tt.to_device(s) for _, s in fs]
+    cfg = SolverConfig(**recipe.solver)
+    stored, rows = march_device(hl, hr, hs, n, bcs, srcs, recipe.step_tol, cfg, store_stride=1)
+    states = {k: tt.from_device(h).cores for k, h in stored.items()}
+    for h in [hl, hr, hs] + bcs + srcs + list(stored.values()):
+        h.free()
+    out, worst = [], {"rel_diff": 0.0, "rank_mismatch": 0, "err_excess": 0.0}
+    for k in range(1, n + 1):
+        got = states[k]
+        ref_ranks = tuple(int(r) for r in z[f"ranks{k}"])
+        row = {"step": k, "ranks": list(ot.ranks_of(got)), "ranks_ref": list(ref_ranks),
+               "residual": rows[k - 1][3], "residual_ref": float(np.array(z[f"res{k}"])[-1]),
+               "sweeps": rows[k - 1][4], "sweeps_ref": int(np.array(z[f"res{k}"]).size)}
+        ex = exact(k * recipe.dt).cores
+        err = ot.tt_norm(ot.tt_add(got, ot.tt_scale(ex, -1.0))) / ot.tt_norm(ex)
+        row["exact_err"], row["exact_err_ref"] = float(err), float(z[f"err{k}"])
+        if has_train(z, f"state{k}"):
+            row["rel_diff"] = rel_diff(got, get_train(z, f"state{k}"))
+            worst["rel_diff"] = max(worst["rel_diff"], row["rel_diff"])
+        worst["rank_mismatch"] += int(tuple(row["ranks"]) != ref_ranks)
+        worst["err_excess"] = max(worst["err_excess"], err / row["exact_err_ref"] - 1.0)
+        out.append(row)
+    summary = dict(worst, config=index, steps=n, final_exact_err=out[-1]["exact_err"],
+                   final_exact_err_ref=out[-1]["exact_err_ref"],
+                   sweeps=sum(r["sweeps"] for r in out),
+                   sweeps_ref=sum(r["sweeps_ref"] for r in out))
+    _record(f"config{index}", out, summary)
+    return out, summary
+
+
+@pytest.mark.parametrize("index,fname", [(2, "config2_full.npz"), (3, "config3_full.npz")])
+def test_march_full_length_matches_reference(golden, index, fname):
+    rows, summary = _march_full(golden, index, fname)
+    bad_ranks = [(r["step"], r["ranks"], r["ranks_ref"]) for r in rows
+                 if r["ranks"] != r["ranks_ref"]]
+    assert not bad_ranks, bad_ranks[:5]
+    bad_vals = [(r["step"], r["rel_diff"]) for r in rows
+                if "rel_diff" in r and r["rel_diff"] > PARITY_TOL]
+    assert not bad_vals, (summary, bad_vals[:5])
+    bad_err = [(r["step"], r["exact_err"], r["exact_err_ref"]) for r in rows
+               if r["exact_err"] > r["exact_err_ref"] * (1 + ERR_SLACK)]
+    assert not bad_err, bad_err[:5]

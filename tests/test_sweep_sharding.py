@@ -22,29 +22,20 @@ def _free_port():
 
 
 def _cpu_build(recipe):
-    """Product setup with the oracle doing the setup numerics (CPU)."""
-    from oracle import tt_ops as ot
-    from paper_2506_04732_b200 import assembly, tt, workloads as wl
+    """The workload's setup (ttss, host numpy: no GPU involved)."""
+    from paper_2506_04732_b200 import workloads as wl
 
-    def rnd(v, tol, max_rank=None):
-        if isinstance(v, tt.TTOperator):
-            return tt.TTOperator(ot.as_operator(ot.tt_round(ot.as_vector(v.cores), tol, max_rank),
-                                                v.row_sizes, v.col_sizes))
-        return tt.TTVector(ot.tt_round(v.cores, tol, max_rank))
-
-    with assembly.setup_backend(round=rnd, add=lambda a, b: type(a)(ot.tt_add(a.cores, b.cores)),
-                                apply=lambda o, v: tt.TTVector(ot.tt_apply(o.cores, v.cores))):
-        return wl.steady_problem(recipe)
+    return wl.steady_problem(recipe)
 
 
 def _cpu_solve(a, b, cfg):
     from oracle import als_solver as als
-    from paper_2506_04732_b200 import tt
+    from paper_2506_04732_b200.reference import module
 
     kw = {k: v for k, v in cfg.items()}
     x0 = als.initial_guess(b.cores, als.Config(**kw), np.random.default_rng(kw.get("seed", 0)))
     x, rep = als.solve(a.cores, b.cores, x0=x0, cfg=als.Config(**kw))
-    return tt.TTVector(x), rep
+    return module("tensor_train").TTVector(x), rep
 
 
 _GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config4_small.npz")

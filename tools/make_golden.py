@@ -238,7 +238,7 @@ def sweep_small(fname, count=4, sweeps=30):
     save(fname, st)
 
 
-def ref_march(recipe, n_keep):
+def ref_march(recipe, n_keep, keep_forcing=True, keep_every=1, keep_ops=True):
     d = recipe.dims
     spec = spec_of(d, recipe.degree, recipe.eps, recipe.beta, 0.0, rhs=0.0)
     op = assemble_opset(spec)
@@ -247,8 +247,12 @@ def ref_march(recipe, n_keep):
     rows, reps = row_axes(op.grids), rep_axes(op.grids)
     state = rtt.tt_round(rtt.tt_rank_one(recipe.u_factors(reps, 0.0)), 1e-14)
     st = {}
-    put_train(st, "left", left.cores)
-    put_train(st, "right", right.cores)
+    if keep_ops:
+        put_train(st, "left", left.cores)
+        put_train(st, "right", right.cores)
+    else:  # fingerprints: the tests rebuild the operators with ttss's own setup
+        st["left_sums"] = np.array([np.abs(c).sum() for c in left.cores])
+        st["right_sums"] = np.array([np.abs(c).sum() for c in right.cores])
     put_train(st, "state0", state.cores)
     cfg = rsol.SolverConfig(**recipe.solver)
     walls = []
@@ -265,9 +269,12 @@ def ref_march(recipe, n_keep):
         walls.append(time.time() - t0)
         exact = rtt.tt_rank_one(recipe.u_factors(reps, t))
         err = rtt.tt_norm(rtt.tt_add(state, rtt.tt_scale(exact, -1.0))) / rtt.tt_norm(exact)
-        put_train(st, f"bc{k}", bc.cores)
-        put_train(st, f"src{k}", src.cores)
-        put_train(st, f"state{k}", state.cores)
+        if keep_forcing:
+            put_train(st, f"bc{k}", bc.cores)
+            put_train(st, f"src{k}", src.cores)
+        if k % keep_every == 0 or k == n_keep:
+            put_train(st, f"state{k}", state.cores)
+        st[f"ranks{k}"] = np.array(state.ranks)
         st[f"res{k}"] = np.array(rep.residual_history)
         st[f"err{k}"] = np.array(err)
         print(f"  step {k}: {walls[-1]:.2f}s ranks {state.ranks} res "
