@@ -492,12 +492,7 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
     LaunchScope ls("galerkin_build", 2.0*(double)N*N*ra*(rb+1), 8.0*(double)N*N);
     const size_t smem = sizeof(double) * ((size_t)ra * n * ry + (size_t)rx * ra * rx);
     if (smem <= 96 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        T2S2_CUDA(cudaFuncSetAttribute(galerkin_factored_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        attr = true;
-      }
+      max_dynamic_smem((const void*)galerkin_factored_kernel, 96 * 1024);
       galerkin_factored_kernel<<<n * ry, 256, smem, stream()>>>(rx, n, ry, ra, rb, pal.p, ac.p, par.p,
                                                                B.p);
     } else {
@@ -529,7 +524,7 @@ void dense_solve_pivoted(DTensor& M, const DTensor& rhs, DTensor& out, int* info
 // dense_solve_pivoted.
 void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   out = rhs.clone();
-  if (lu_solve_nopivot(M.dim(0), M.p, out.p, info_dev)) return;
+  if (gj_solve_nopivot(M.dim(0), M.p, out.p, info_dev)) return;
   dense_solve_pivoted(M, rhs, out, info_dev);
 }
 
@@ -805,6 +800,7 @@ struct Sweep {
   }
 
   Probe probe;
+  bool gal_direct = false;  // the last update's Galerkin candidate came from a dense solve
 
   // Guarded update of core l (tt_solver.py:337-422).  Candidate scores
   // q = u^T N u - 2 c^T u, the finiteness checks and the LU info travel to
@@ -830,6 +826,7 @@ struct Sweep {
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
     const double inner_rtol = std::fmax(cfg.inner_tol_factor * current_res, 1e-12);
     const bool try_gal = gal_rejects < gal_cap;
+    gal_direct = try_gal && direct;
     DTensor u_gal, nu_gal;
     if (try_gal) {
       if (direct) {
@@ -992,6 +989,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
 
     DTensor end_grad;  // residual gradient of the last forward visit
     int end_choice = 0;
+    bool end_direct = false;
     for (int l = 0; l < d; ++l) {
       DTensor u, grad;
       int choice;
@@ -1001,6 +999,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
         cores[l] = std::move(u);
         end_grad = std::move(grad);
         end_choice = choice;
+        end_direct = sw.gal_direct;
         break;
       }
       Split sp = split_forward(u, &grad, cfg, d);
@@ -1026,11 +1025,14 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     for (int l = d - 1; l >= 0; --l) {
       DTensor u, grad;
       int choice;
-      if (l == d - 1 && d > 1 && end_choice == 1) {
+      if (l == d - 1 && d > 1 && end_choice == 1 && end_direct) {
         // The backward pass re-visits core d-1 with unchanged interfaces:
         // its Galerkin system is the one just solved, so the (deterministic)
-        // solve would return the current core bit for bit, q_gal == q_old
-        // and the candidate is accepted (tt_solver.py:383-387).  Reuse it.
+        // dense solve would return the current core bit for bit, q_gal ==
+        // q_old and the candidate is accepted (tt_solver.py:383-387).  Reuse
+        // it.  Not for a GMRES candidate: the reference restarts GMRES from
+        // the new core (x0 = u_old), which iterates on unless the forward run
+        // reached its tolerance (tt_solver.py:367-377), so that case re-solves.
         u = cores[l].clone();
         grad = std::move(end_grad);
         choice = 1;

@@ -1,6 +1,7 @@
 // C ABI of the engine (include/t2s2.h): context management, train
 // upload/download and the hot-path entry points.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,7 +27,10 @@ struct Pending {
 
 struct t2s2_context {
   int device = 0;
+  int sms = 0;        // multiprocessor count of the device
   int sm_budget = 0;  // 0: all SMs
+  std::unordered_map<const void*, int> smem_limit;  // kernel -> raised dynamic smem bytes
+  std::unordered_map<std::string, int> occ_cache;   // kernel/threads/smem -> CTAs per SM
   cudaStream_t stream = nullptr;
   t2s2::Allocator alloc;
   std::string last_error;
@@ -60,6 +64,26 @@ struct Bind {  // makes ctx current for the duration of an API call
 }  // namespace
 
 Allocator& allocator() { return g_ctx->alloc; }
+int num_sms() { return g_ctx->sms; }
+
+void max_dynamic_smem(const void* kernel, int bytes) {
+  auto it = g_ctx->smem_limit.find(kernel);
+  if (it != g_ctx->smem_limit.end() && it->second >= bytes) return;
+  T2S2_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_ctx->smem_limit[kernel] = bytes;
+}
+
+int occupancy(const void* kernel, int threads, int smem) {
+  char key[64];
+  snprintf(key, sizeof key, "%p/%d/%d", kernel, threads, smem);
+  auto it = g_ctx->occ_cache.find(key);
+  if (it != g_ctx->occ_cache.end()) return it->second;
+  int occ = 0;
+  T2S2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, (size_t)smem));
+  if (occ < 1) occ = 1;
+  g_ctx->occ_cache.emplace(key, occ);
+  return occ;
+}
 int sm_budget() { return g_ctx->sm_budget; }
 
 LaunchScope::LaunchScope(const char* family, double flops, double bytes) {
@@ -226,6 +250,9 @@ int t2s2_context_create(int device, t2s2_context** out) {
   auto ctx = std::make_unique<t2s2_context>();
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess) return T2S2_ERR_CUDA;
+  if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      ctx->sms < 1)
+    return T2S2_ERR_CUDA;
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return T2S2_ERR_CUDA;
   ctx->alloc.stream = ctx->stream;
@@ -423,7 +450,7 @@ int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const d
     DTensor A2({n, n}), rhs2({n});
     dcopy(A2.p, A.p, (size_t)n * n);
     dcopy(rhs2.p, rhs.p, n);
-    if (lu_solve_nopivot(n, A2.p, rhs2.p, info)) {
+    if (gj_solve_nopivot(n, A2.p, rhs2.p, info)) {
       T2S2_CUDA(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, stream()));
       T2S2_CUDA(cudaStreamSynchronize(stream()));
       if (h == 0) dcopy(rhs.p, rhs2.p, n);

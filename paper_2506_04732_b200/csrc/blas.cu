@@ -526,30 +526,12 @@ void GemmBatch::run() {
     }
     // a stage cut by the problem limit continues in the next program
     prog.stage_first[prog.nstage] = prog.nprob;
-    static int nsm = 0;
-    if (nsm == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    static int occ = 0;
-    if (occ == 0) {
-      T2S2_CUDA(cudaFuncSetAttribute(gemm_program_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_program_kernel, 256, kGemmSmem);
-      if (occ < 1) occ = 1;
-    }
+    const int nsm = num_sms();
+    max_dynamic_smem((const void*)gemm_program_kernel, kGemmSmem);
+    const int occ = occupancy((const void*)gemm_program_kernel, 256, kGemmSmem);
     int grid = max_tiles < nsm * occ ? max_tiles : nsm * occ;
     if (sm_budget() > 0 && grid > sm_budget()) grid = sm_budget();
     if (grid < 1) grid = 1;
-    // T2S2_GEMM_TRACE=1: time each program alone and print its shape (development aid)
-    static const bool trace = getenv("T2S2_GEMM_TRACE") != nullptr;
-    cudaEvent_t te[2];
-    if (trace) {
-      cudaEventCreate(&te[0]);
-      cudaEventCreate(&te[1]);
-      cudaEventRecord(te[0], stream());
-    }
     {
       LaunchScope ls("gemm", flops_ * prog.nprob / (double)items_.size(), 0.0);
       if (prog.nstage == 1) {
@@ -561,22 +543,6 @@ void GemmBatch::run() {
       }
     }
     T2S2_CHECK_LAUNCH();
-    if (trace) {
-      cudaEventRecord(te[1], stream());
-      cudaEventSynchronize(te[1]);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, te[0], te[1]);
-      fprintf(stderr, "GEMMPROG us=%.2f grid=%d nstage=%d", ms * 1e3f, grid, prog.nstage);
-      for (int st = 0; st < prog.nstage; ++st) {
-        fprintf(stderr, " |");
-        for (int q = prog.stage_first[st]; q < prog.stage_first[st + 1]; ++q)
-          fprintf(stderr, " %dx%dx%d*%d/%d%s", prog.p[q].M, prog.p[q].N, prog.p[q].K, prog.p[q].batch,
-                  prog.p[q].tiles, prog.p[q].kind ? "R" : (prog.p[q].big ? "B" : ""));
-      }
-      fprintf(stderr, "\n");
-      cudaEventDestroy(te[0]);
-      cudaEventDestroy(te[1]);
-    }
   }
   items_.clear();
   temps_.clear();  // stream-ordered: safe to recycle once the launch is enqueued

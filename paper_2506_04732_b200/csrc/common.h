@@ -59,6 +59,11 @@ struct Allocator {
   cudaStream_t stream = nullptr;
   std::unordered_map<size_t, std::vector<double*>> free_lists;
   std::unordered_map<double*, size_t> live;
+  // set while a CUDA graph is being captured on the stream: a cache miss
+  // then throws instead of calling cudaMallocAsync (a graph-owned
+  // allocation would leak into the free lists), and the caller falls back
+  // to eager launches
+  bool capturing = false;
   static size_t size_class(size_t n) {
     size_t c = 32;
     while (c < n) c <<= 1;
@@ -73,6 +78,7 @@ struct Allocator {
       p = fl.back();
       fl.pop_back();
     } else {
+      T2S2_REQUIRE(!capturing, kErrCuda, "allocator cache miss during graph capture");
       void* v = nullptr;
       T2S2_CUDA(cudaMallocAsync(&v, c * sizeof(double), stream));
       p = static_cast<double*>(v);
@@ -105,6 +111,11 @@ struct LaunchScope {
 };
 
 Allocator& allocator();  // the current context's allocator
+// Per-device launch properties, cached in the current context (one context
+// per host thread and device, so no shared mutable state between threads):
+int num_sms();                                          // multiprocessors of the device
+void max_dynamic_smem(const void* kernel, int bytes);   // raise the kernel's dynamic smem limit
+int occupancy(const void* kernel, int threads, int smem);  // resident CTAs per SM (>= 1)
 int sm_budget();         // CTAs a whole-GPU cooperative kernel may use (context setting)
 cudaStream_t stream();   // the current context's stream
 bool profiling();        // per-launch CUDA-event timing switched on (t2s2_stats_reset)

@@ -778,21 +778,13 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
 #undef GJ_PHASE
 }
 
-int g_sms = 0;
-
 }  // namespace
 
 #ifndef GJ_MICRO
 
 bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
-  if (g_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static const int grid_env = getenv("T2S2_NP_GRID") ? atoi(getenv("T2S2_NP_GRID")) : 0;
-  int grid = sm_budget() > 0 && sm_budget() < g_sms ? sm_budget() : g_sms;
-  if (grid_env > 0 && grid_env < grid) grid = grid_env;
+  const int sms = num_sms();
+  int grid = sm_budget() > 0 && sm_budget() < sms ? sm_budget() : sms;
   if (N < 1 || N > 8192) return false;
   // no more CTAs than the first (largest) phase has tile tasks: a smaller
   // grid makes every grid barrier cheaper; tiny systems run on one CTA
@@ -806,23 +798,13 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
     if (want < grid) grid = want;
   }
   const size_t smem = sizeof(Smem);
-  static bool attr = false;
-  if (!attr) {
-    T2S2_CUDA(cudaFuncSetAttribute(gj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  max_dynamic_smem((const void*)gj_kernel, (int)smem);
   const int npan = (N + kP - 1) / kP;
   double* inv = allocator().alloc((size_t)npan * kInv);
   double* wbuf = allocator().alloc((size_t)3 * kP * (N + 1));
-  static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
-  unsigned long long* pbuf = nullptr;
-  if (prof) {
-    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
-    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
-  }
   unsigned* sync = reinterpret_cast<unsigned*>(allocator().alloc((size_t)(npan + 2) / 2 + 1));
   T2S2_CUDA(cudaMemsetAsync(sync, 0, sizeof(unsigned) * (size_t)(npan + 2), stream()));
-  GjArgs a{N, A, b, inv, wbuf, info_dev, sync, pbuf};  // *info zeroed by the kernel
+  GjArgs a{N, A, b, inv, wbuf, info_dev, sync, nullptr};  // *info zeroed by the kernel
   void* params[] = {&a};
   {
     // algorithmic work of the operation (a dense solve: LU 2/3 N^3 + two triangular
@@ -836,15 +818,6 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   allocator().release(inv);
   allocator().release(wbuf);
   allocator().release(reinterpret_cast<double*>(sync));
-  if (prof) {
-    unsigned long long h[16];
-    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
-    T2S2_CUDA(cudaStreamSynchronize(stream()));
-    fprintf(stderr, "gj N=%d cta0: work %.1f sync %.1f final %.1f top %.1f (diag %.1f) | cta1: work %.1f sync %.1f final %.1f top %.1f us\n",
-            N, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[9] / 1e3, h[4] / 1e3, h[5] / 1e3,
-            h[6] / 1e3, h[7] / 1e3);
-    allocator().release(reinterpret_cast<double*>(pbuf));
-  }
   return true;
 }
 

@@ -1,4 +1,5 @@
 // Device GMRES(restart) and Jacobi-PCG (see iterative.h).
+#include <atomic>
 #include <cfloat>
 #include <cstdlib>
 #include <cmath>
@@ -417,7 +418,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   int inner = 0;
   // host polls of the device convergence flag (each one drains the stream);
   // iterations past convergence are no-ops on the device (guarded)
-  static const int poll = getenv("T2S2_KRYLOV_POLL") ? atoi(getenv("T2S2_KRYLOV_POLL")) : 16;
+  constexpr int poll = 16;  // host convergence poll interval (iterations)
   if (rnorm < atol) {
     allocator().release(V);
     allocator().release(r);
@@ -498,7 +499,7 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   if (G < 1) G = 1;
   int it = 0;
   double at = atol;
-  static const int poll = getenv("T2S2_KRYLOV_POLL") ? atoi(getenv("T2S2_KRYLOV_POLL")) : 20;
+  constexpr int poll = 20;  // iterations per captured graph / host poll
   {
     LaunchScope ls("cg", 6.0 * n, 40.0 * n);
     int itv = 0;
@@ -512,13 +513,16 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   // host no longer builds and launches two cooperative kernels per
   // iteration.  Iterations after convergence are device no-ops, as without
   // the graph.  The remainder below a multiple of `poll` runs eagerly.
-  static bool graphs_ok = getenv("T2S2_NO_GRAPH") == nullptr && getenv("T2S2_GEMM_TRACE") == nullptr;
+  // T2S2_NO_GRAPH=1 runs the same iterations eagerly (tests check the
+  // replay is bit-identical to it)
+  static std::atomic<bool> graphs_ok{getenv("T2S2_NO_GRAPH") == nullptr};
   if (graphs_ok && !profiling() && maxiter >= 2 * poll) {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     const StatsMark before = stats_mark();
     bool captured = false;
     T2S2_CUDA(cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal));
+    allocator().capturing = true;
     try {
       for (int k = 0; k < poll; ++k) {
         A(p, q, &st->active);
@@ -531,6 +535,7 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
       captured = true;
     } catch (const Error&) {
     }
+    allocator().capturing = false;
     const cudaError_t ec = cudaStreamEndCapture(stream(), &graph);
     if (captured && ec == cudaSuccess && graph &&
         cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
@@ -542,8 +547,10 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
         stats_replay(before, after, 1);
       }
     } else {
-      // capture unsupported here: run eagerly from now on
-      graphs_ok = false;
+      // an allocator cache miss aborted this capture: eager launches this
+      // time; a capture that completed but cannot be instantiated means
+      // graphs are unsupported here: eager from now on
+      if (captured) graphs_ok = false;
       const StatsMark after = stats_mark();
       stats_replay(before, after, -1);
       (void)cudaGetLastError();

@@ -679,12 +679,7 @@ __global__ void __launch_bounds__(512)
 template <int RPL, int NPX>
 void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double* Vt, size_t smem,
                      int thr) {
-  static bool attr = false;  // one flag per instantiation
-  if (!attr) {
-    T2S2_CUDA(cudaFuncSetAttribute(svd_warp_kernel<RPL, NPX>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-    attr = true;
-  }
+  max_dynamic_smem((const void*)svd_warp_kernel<RPL, NPX>, (int)kSmemCap);
   svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt);
 }
 
@@ -862,12 +857,7 @@ __global__ void __launch_bounds__(512)
 template <int RPL, int CPW, bool WANTQ>
 void launch_wqr(int blocks, int thr, size_t smem, int m, int n, int chunk, const double* A, double* Q,
                 double* R, int cm) {
-  static bool attr = false;  // one flag per instantiation
-  if (!attr) {
-    T2S2_CUDA(cudaFuncSetAttribute(wqr_kernel<RPL, CPW, WANTQ>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-    attr = true;
-  }
+  max_dynamic_smem((const void*)wqr_kernel<RPL, CPW, WANTQ>, (int)kSmemCap);
   wqr_kernel<RPL, CPW, WANTQ><<<blocks, thr, smem, stream()>>>(m, n, chunk, A, Q, R, cm);
 }
 
@@ -905,8 +895,7 @@ bool wqr(int blocks, int m, int n, int chunk, const double* A, double* Q, double
 
 void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_r: empty matrix");
-  static const bool old_qr = getenv("T2S2_QR_OLD") != nullptr;
-  if (!old_qr && n <= 64 && m >= n) {
+  if (n <= 64 && m >= n) {
     // warp-level TSQR: leaves of <= 384 rows (and >= 2n so the stack shrinks)
     const int k = m < n ? m : n;
     const int cap = n > 32 ? 256 : 384;  // rows per leaf (see wqr)
@@ -946,12 +935,7 @@ void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
     return;
   }
   const int blocks = ceil_div(m, chunk);
-  static bool attr = false;
-  if (!attr) {
-    T2S2_CUDA(cudaFuncSetAttribute(qr_r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kSmemCap));
-    attr = true;
-  }
+  max_dynamic_smem((const void*)qr_r_kernel, (int)kSmemCap);
   DTensor stacked({blocks * n, n});
   {
     LaunchScope ls("qr", 2.0 * m * (double)n * n, 8.0 * m * (double)n);
@@ -973,8 +957,7 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
   const int k = m < n ? m : n;
   Q = DTensor({m, k});
   R = DTensor({k, n});
-  static const bool old_qr = getenv("T2S2_QR_OLD") != nullptr;
-  if (!old_qr && m >= n && m <= (n > 32 ? 256 : 384) && n <= 64) {
+  if (m >= n && m <= (n > 32 ? 256 : 384) && n <= 64) {
     bool ok;
     {
       LaunchScope ls("qr", 4.0 * m * (double)n * k, 16.0 * m * (double)n);
@@ -989,7 +972,7 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
   // cores, 33*64 x 64): TSQR with Q — warp-level leaves, the stacked leaf
   // R factors factored recursively (Q2, R), Q = diag(Q_leaf) Q2 as one
   // small GEMM per leaf
-  if (!old_qr && m > n && n <= 64 && ((size_t)m * n + k) * sizeof(double) > kSmemCap) {
+  if (m > n && n <= 64 && ((size_t)m * n + k) * sizeof(double) > kSmemCap) {
     const int cap = n > 32 ? 256 : 384;
     const int leaves = (m + cap - 1) / cap;
     const int chunk = (m + leaves - 1) / leaves;
@@ -1026,12 +1009,7 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
     LaunchScope ls("qr", 4.0*m*(double)n*(m<n?m:n), 16.0*m*(double)n);
     const size_t need = ((size_t)m * n + k) * sizeof(double);
     if (need <= kSmemCap) {
-      static bool attr = false;
-      if (!attr) {
-        T2S2_CUDA(cudaFuncSetAttribute(qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemCap));
-        attr = true;
-      }
+      max_dynamic_smem((const void*)qr_kernel<true>, (int)kSmemCap);
       qr_kernel<true><<<1, threads_for(n), need, stream()>>>(m, n, A, W, Qc, tau, Q.p, R.p,
                                                               cm ? 1 : 0);
     } else {
@@ -1057,12 +1035,7 @@ void jacobi_svd(int p, int q, double* G, DTensor& U, DTensor& s, DTensor& Vt) {
     LaunchScope ls("svd_jacobi", 0, 0);
     const size_t need = ((size_t)p * q + (size_t)q * q + q) * sizeof(double);
     if (need <= kSmemCap) {
-      static bool attr = false;
-      if (!attr) {
-        T2S2_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
-        attr = true;
-      }
+      max_dynamic_smem((const void*)jacobi_kernel<true>, (int)kSmemCap);
       jacobi_kernel<true><<<1, threads_for((q + 1) / 2), need, stream()>>>(p, q, G, V, perm, U.p,
                                                                            s.p, Vt.p);
     } else {
@@ -1093,10 +1066,9 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
   {
     const int mp = m >= n ? m : n, np = m >= n ? n : m;
-    static const bool old_svd = getenv("T2S2_SVD_OLD") != nullptr;
     // warp-level kernel: np <= 16 columns, mp <= 384 rows
     const size_t wneed = (2 * (size_t)mp * np + 3 * (size_t)np * np + 2 * (size_t)np) * sizeof(double);
-    if (!old_svd && np <= 16 && mp <= 384 && wneed <= kSmemCap) {
+    if (np <= 16 && mp <= 384 && wneed <= kSmemCap) {
       U = m >= n ? DTensor({m, n}) : DTensor({m, m});
       s = DTensor({np});
       Vt = m >= n ? DTensor({n, n}) : DTensor({m, n});
@@ -1104,29 +1076,24 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
         LaunchScope ls("svd_jacobi", 4.0 * mp * (double)np * np, 8.0 * m * (double)n);
         const int thr = 32 * (np < 2 ? 2 : np);
         const int rpl = (mp + 31) / 32;
-#define T2S2_SVDW(NPX)                                                            \
+#define T2S2_SVD_WARP(NPX)                                                            \
   do {                                                                            \
     if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);   \
     else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr); \
     else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);           \
   } while (0)
-        if (np <= 4) T2S2_SVDW(4);
-        else if (np <= 8) T2S2_SVDW(8);
-        else if (np <= 12) T2S2_SVDW(12);
-        else T2S2_SVDW(16);
-#undef T2S2_SVDW
+        if (np <= 4) T2S2_SVD_WARP(4);
+        else if (np <= 8) T2S2_SVD_WARP(8);
+        else if (np <= 12) T2S2_SVD_WARP(12);
+        else T2S2_SVD_WARP(16);
+#undef T2S2_SVD_WARP
       }
       T2S2_CHECK_LAUNCH();
       return;
     }
     const size_t need = ((size_t)mp * np + 3 * (size_t)np * np + 4 * (size_t)np) * sizeof(double);
     if (need <= kSmemCap && np <= 64) {
-      static bool attr = false;
-      if (!attr) {
-        T2S2_CUDA(cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemCap));
-        attr = true;
-      }
+      max_dynamic_smem((const void*)svd_small_kernel, (int)kSmemCap);
       U = m >= n ? DTensor({m, n}) : DTensor({m, m});
       s = DTensor({np});
       Vt = m >= n ? DTensor({n, n}) : DTensor({m, n});

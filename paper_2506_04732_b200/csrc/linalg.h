@@ -29,16 +29,12 @@ void lu_solve(int N, const double* LU, const int* ipiv, double* b);
 // One cooperative launch: factor A (clobbered) and overwrite b with the
 // solution.  Returns false when N is too large for the smem panel.
 bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev);
-// Verified no-pivot LU solve (one cooperative launch): when partial pivoting
-// would make no interchange — every multiplier |l| <= 1 — it computes the
-// same factors without a pivot search.  (Dispatches to the block
-// Gauss-Jordan kernel, gj_solve.cu.)  Otherwise (or on a zero pivot) it
-// sets *info_dev = -1 and leaves A, b clobbered: rebuild and use the
-// pivoting kernel.  Returns false when not applicable (nothing launched).
-bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev);
-// The same contract by blocked Gauss-Jordan (gj_solve.cu): one grid barrier
-// per 32-column panel, no back-substitution chain.  lu_solve_nopivot
-// dispatches to it (T2S2_NP_OLD=1 keeps the LU kernel for comparison).
+// Verified no-pivot dense solve by blocked Gauss-Jordan (one cooperative
+// launch, gj_solve.cu): when partial pivoting would make no interchange —
+// every multiplier |l| <= 1 — it computes GEPP's factors without a pivot
+// search and overwrites b with the solution.  Otherwise (or on a zero
+// pivot) it sets *info_dev = -1 and leaves A, b clobbered: rebuild and use
+// the pivoting kernel.  Returns false when not applicable (nothing launched).
 bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev);
 
 }  // namespace t2s2

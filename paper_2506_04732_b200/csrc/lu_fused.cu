@@ -751,401 +751,27 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
   if (blockIdx.x == 0) back_substitute(a, sm);
 }
 
-// ---------------------------------------------------------------------------
-// No-pivot blocked LU, verified: Gaussian elimination with partial pivoting
-// performs no row interchange exactly when every multiplier satisfies
-// |l_ij| <= 1 (the diagonal is then the first maximum of its column at every
-// step), and then its factors are those of plain LU.  The local systems of
-// an implicit step (I + dt L projected on orthonormal bases) are almost
-// always of this kind, so they are factored without a pivot search: 64-wide
-// panels, the 64x64 diagonal block factored (and its triangular factors
-// inverted) by CTA 0, L21 = A21 U11^{-1} and U12 = L11^{-1} A12 as 64x64
-// DMMA tile products over all CTAs, then the trailing update
-// A22 -= L21 U12 likewise; CTA 0 updates the next diagonal block first and
-// factors it while the others finish the trailing tiles (lookahead), so a
-// panel costs two grid barriers.  Every multiplier is checked; if one
-// exceeds 1 (or a pivot is zero/non-finite) *info = -1 and the caller falls
-// back to the pivoting kernel on a fresh copy of the matrix.
-// ---------------------------------------------------------------------------
-
-constexpr int kNpThreads = 256;
-constexpr int kNb = 32;       // panel width
-constexpr int kTm = 64;       // trailing-update tile (kTm x kTm)
-constexpr int kTs = kTm + 4;  // smem tile stride (doubles)
-
-struct NpArgs {
-  int N;
-  double* A;    // column-major N x N
-  double* b;    // rhs, overwritten with x
-  int* info;    // 0, or -1: a multiplier exceeded 1 (pivoting needed)
-  unsigned long long* prof;
-};
-
-__device__ __forceinline__ void np_fail(const NpArgs& a) { atomicExch(a.info, -1); }
-
-// C[m x n] -= Aop[m x K] * Bop[K x n] (m, n <= 64, K <= 64): operands
-// column-major in global memory, DMMA m8n8k4 on 8 warps (2 x 4 grid of
-// 32 x 16 warp tiles).
-__device__ void np_tile(int m, int n, int K, const double* Ag, int lda, const double* Bg, int ldb,
-                        double* C, int ldc, double* sm) {
-  double* As = sm;              // As[k*kTs + i]
-  double* Bs = sm + kTm * kTs;  // Bs[j*kTs + k]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int Kp = (K + 3) & ~3;
-  const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
-  // this lane's C elements, loaded first so their latency overlaps the
-  // operand staging
-  double cv[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = wm0 + i * 8 + (lane >> 2), c = wn0 + j * 8 + (lane & 3) * 2 + h;
-        cv[i][j][h] = (r < m && c < n) ? __ldcg(C + (long long)c * ldc + r) : 0.0;
-      }
-  __syncthreads();
-  for (int e = tid; e < kTm * Kp; e += kNpThreads) {
-    const int c = e >> 6, r = e & 63;
-    As[c * kTs + r] = (r < m && c < K) ? __ldcg(Ag + (long long)c * lda + r) : 0.0;
-  }
-  for (int e = tid; e < kTm * Kp; e += kNpThreads) {
-    const int c = e / Kp, r = e - c * Kp;
-    Bs[c * kTs + r] = (r < K && c < n) ? __ldcg(Bg + (long long)c * ldb + r) : 0.0;
-  }
-  __syncthreads();
-  if (wm0 >= m || wn0 >= n) return;
-  double acc[4][2][2] = {};
-  for (int kk = 0; kk < Kp; kk += 4) {
-    const int kr = kk + (lane & 3);
-    double af[4], bf[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = As[kr * kTs + wm0 + i * 8 + (lane >> 2)];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) bf[j] = Bs[(wn0 + j * 8 + (lane >> 2)) * kTs + kr];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma_8x8x4_lu(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = wm0 + i * 8 + (lane >> 2);
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = wn0 + j * 8 + (lane & 3) * 2 + h;
-        if (r < m && c < n) C[(long long)c * ldc + r] = cv[i][j][h] - acc[i][j][h];
-      }
-  }
-}
-
-// Factor the kb x kb diagonal block at k0 in place (CTA 0), no
-// interchanges: one barrier per column; thread (column j, rows i0 + 8q)
-// loads its four values before it stores any, so the column step is one
-// shared-memory round trip.
-__device__ void np_diag(const NpArgs& a, int k0, double* sm) {
-  const int N = a.N, kb = N - k0 < kNb ? N - k0 : kNb;
-  const int tid = threadIdx.x;
-  double* D = sm;  // D[c*33 + i]
-  __syncthreads();
-  for (int e = tid; e < kNb * kNb; e += kNpThreads) {
-    const int c = e >> 5, i = e & 31;
-    D[c * 33 + i] = (i < kb && c < kb) ? __ldcg(a.A + (long long)(k0 + c) * N + k0 + i)
-                                       : (i == c ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  const int j = tid & 31, i0 = tid >> 5;
-  bool bad = false;
-  for (int s = 0; s < kb; ++s) {
-    const double piv = D[s * 33 + s];
-    const double us = D[j * 33 + s];
-    double ls[4], x[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      ls[q] = D[s * 33 + i0 + 8 * q];
-      x[q] = D[j * 33 + i0 + 8 * q];
-    }
-    const double rinv = 1.0 / piv;
-    if (tid == 0 && !(fabs(piv) > 0.0)) bad = true;
-    __syncthreads();  // every read of column s precedes its overwrite below
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + 8 * q;
-      if (i > s) {
-        const double l = ls[q] * rinv;
-        if (j > s) D[j * 33 + i] = fma(-l, us, x[q]);
-        if (j == s) {
-          D[s * 33 + i] = l;
-          if (!(fabs(l) <= 1.0)) bad = true;
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (__syncthreads_or(bad) && tid == 0) np_fail(a);
-  for (int e = tid; e < kNb * kNb; e += kNpThreads) {
-    const int c = e >> 5, i = e & 31;
-    if (i < kb && c < kb) a.A[(long long)(k0 + c) * N + k0 + i] = D[c * 33 + i];
-  }
-  __threadfence();
-  __syncthreads();
-}
-
-// L21 rows [r, r+m) = A21 U11^{-1} (row substitution, one thread per row,
-// checked |l| <= 1) or U12 columns [c, c+n) = L11^{-1} A12 (column
-// substitution, one thread per column); also the rhs column.
-__device__ void np_trsm_rows(const NpArgs& a, int k0, int kb, int r, int m, double* sm) {
-  const int N = a.N, tid = threadIdx.x;
-  double* U = sm;  // U[j*33 + i]
-  double* R = sm + 33 * 32;  // R[j*65 + t]: A21 rows
-  double* rd = R + 65 * 32;  // 1 / u_jj
-  __syncthreads();
-  for (int e = tid; e < kNb * kNb; e += kNpThreads) {
-    const int c = e >> 5, i = e & 31;
-    if (c < kb && i < kb) U[c * 33 + i] = __ldcg(a.A + (long long)(k0 + c) * N + k0 + i);
-  }
-  for (int e = tid; e < kb * 64; e += kNpThreads) {
-    const int c = e >> 6, t = e & 63;
-    R[c * 65 + t] = t < m ? __ldcg(a.A + (long long)(k0 + c) * N + r + t) : 0.0;
-  }
-  __syncthreads();
-  if (tid < kb) rd[tid] = __drcp_rn(U[tid * 33 + tid]);
-  __syncthreads();
-  bool bad = false;
-  if (tid < m) {
-    double l[kNb];
-#pragma unroll
-    for (int jj = 0; jj < kNb; ++jj) {
-      if (jj < kb) {
-        double v[4] = {R[jj * 65 + tid], 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < jj; ++q) v[q & 3] = fma(-l[q], U[jj * 33 + q], v[q & 3]);
-        l[jj] = ((v[0] + v[1]) + (v[2] + v[3])) * rd[jj];
-        if (!(fabs(l[jj]) <= 1.0)) bad = true;
-      }
-    }
-#pragma unroll
-    for (int jj = 0; jj < kNb; ++jj)
-      if (jj < kb) a.A[(long long)(k0 + jj) * N + r + tid] = l[jj];
-  }
-  if (__syncthreads_or(bad) && tid == 0) np_fail(a);
-}
-
-__device__ void np_trsm_cols(const NpArgs& a, int k0, int kb, int c, int n, double* sm) {
-  const int N = a.N, tid = threadIdx.x;
-  double* L = sm;  // L[j*33 + i]
-  __syncthreads();
-  for (int e = tid; e < kNb * kNb; e += kNpThreads) {
-    const int cc = e >> 5, i = e & 31;
-    if (cc < kb && i < kb) L[cc * 33 + i] = __ldcg(a.A + (long long)(k0 + cc) * N + k0 + i);
-  }
-  __syncthreads();
-  if (tid < n) {
-    double* col = c + tid < N ? a.A + (long long)(c + tid) * N + k0 : a.b + k0;
-    double u[kNb];
-#pragma unroll
-    for (int i = 0; i < kNb; ++i)
-      if (i < kb) u[i] = __ldcg(col + i);
-#pragma unroll
-    for (int i = 0; i < kNb; ++i) {
-      if (i < kb) {
-        double v[4] = {u[i], 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < i; ++q) v[q & 3] = fma(-L[q * 33 + i], u[q], v[q & 3]);
-        u[i] = (v[0] + v[1]) + (v[2] + v[3]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < kNb; ++i)
-      if (i < kb) col[i] = u[i];
-  }
-}
-
-__global__ void __launch_bounds__(kNpThreads, 1) lu_np_kernel(NpArgs a, LuArgs bs) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ double sm[];
-  const int N = a.N, G = gridDim.x, cta = blockIdx.x;
-  const int npan = (N + kNb - 1) / kNb;
-  unsigned long long tp = 0;
-  const bool pr = a.prof && cta < 2 && threadIdx.x == 0;
-  if (pr) tp = gtimer();
-#define T2S2_NP_PHASE(slot)                                \
-  if (pr) {                                                \
-    const unsigned long long tq = gtimer();                \
-    a.prof[cta * 4 + (slot)] += tq - tp;                   \
-    tp = tq;                                               \
-  }
-  if (cta == 0) np_diag(a, 0, sm);
-  grid.sync();
-  for (int p = 0; p < npan; ++p) {
-    const int k0 = p * kNb, kb = N - k0 < kNb ? N - k0 : kNb, r0 = k0 + kb, nt = N - r0;
-    T2S2_NP_PHASE(3)
-    // phase 2: L21 row tiles (64 rows), U12 column tiles (64 columns; the
-    // last one includes the rhs as column N)
-    const int nrow = (nt + kTm - 1) / kTm, ncol = (nt + 1 + kTm - 1) / kTm;
-    for (int t = cta; t < nrow + ncol; t += G) {
-      if (t < nrow) {
-        const int r = r0 + t * kTm;
-        np_trsm_rows(a, k0, kb, r, N - r < kTm ? N - r : kTm, sm);
-      } else {
-        const int c = r0 + (t - nrow) * kTm;
-        np_trsm_cols(a, k0, kb, c, N + 1 - c < kTm ? N + 1 - c : kTm, sm);
-      }
-    }
-    T2S2_NP_PHASE(0)
-    grid.sync();
-    T2S2_NP_PHASE(1)
-    if (nt == 0) break;
-    // phase 3: A22 -= L21 U12 over kTm x kTm tiles, b2 -= L21 y; CTA 0 takes
-    // tile (0, 0), which holds the next diagonal block, and factors that
-    // block while the other CTAs finish (lookahead)
-    // tile boundaries: a kNb-wide first strip (the next diagonal block),
-    // then kTm-wide strips
-    const int nblk = nt <= kNb ? 1 : 1 + (nt - kNb + kTm - 1) / kTm;
-    const int ntile = nblk * nblk + nblk;
-    auto strip = [&](int t, int& lo, int& len) {
-      lo = t == 0 ? r0 : r0 + kNb + (t - 1) * kTm;
-      const int w = t == 0 ? kNb : kTm;
-      len = N - lo < w ? N - lo : w;
-    };
-    if (cta == 0) {
-      const int m0 = nt < kNb ? nt : kNb;
-      np_tile(m0, m0, kb, a.A + (long long)k0 * N + r0, N, a.A + (long long)r0 * N + k0, N,
-              a.A + (long long)r0 * N + r0, N, sm);
-      __threadfence();
-      __syncthreads();
-      unsigned long long td = pr ? gtimer() : 0;
-      np_diag(a, r0, sm);
-      if (pr) a.prof[9] += gtimer() - td;
-    }
-    for (int t = cta; cta > 0 && t < ntile; t += G - 1) {
-      int r, m;
-      if (t < nblk * nblk) {
-        int c, n;
-        strip(t % nblk, r, m);
-        strip(t / nblk, c, n);
-        np_tile(m, n, kb, a.A + (long long)k0 * N + r, N, a.A + (long long)c * N + k0, N,
-                a.A + (long long)c * N + r, N, sm);
-      } else {
-        strip(t - nblk * nblk, r, m);
-        np_tile(m, 1, kb, a.A + (long long)k0 * N + r, N, a.b + k0, N, a.b + r, N, sm);
-      }
-    }
-    T2S2_NP_PHASE(2)
-    grid.sync();
-  }
-  T2S2_NP_PHASE(3)
-  if (cta == 0 && __ldcg(a.info) == 0) back_substitute(bs, sm);
-  if (pr && cta == 0) a.prof[8] += gtimer() - tp;
-#undef T2S2_NP_PHASE
-}
-
-int g_num_sms = 0;
-
 }  // namespace
 
-bool lu_solve_nopivot(int N, double* A, double* b, int* info_dev) {
-  static const bool old = getenv("T2S2_NP_OLD") != nullptr;
-  if (!old && !getenv("T2S2_LU_PIVOT_ONLY") && gj_solve_nopivot(N, A, b, info_dev)) return true;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static const bool off = getenv("T2S2_LU_PIVOT_ONLY") != nullptr;
-  static const int grid_env = getenv("T2S2_NP_GRID") ? atoi(getenv("T2S2_NP_GRID")) : 0;
-  int grid = sm_budget() > 0 && sm_budget() < g_num_sms ? sm_budget() : g_num_sms;
-  if (grid_env > 1 && grid_env < grid) grid = grid_env;
-  if (off || N > 8192 || grid < 2) return false;
-  size_t need = 2 * (size_t)kTm * kTs;
-  if (need < (size_t)N) need = N;
-  const size_t smem = need * sizeof(double);
-  if (smem > 220 * 1024) return false;
-  static size_t attr = 0;
-  if (smem > attr) {
-    T2S2_CUDA(cudaFuncSetAttribute(lu_np_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    attr = smem;
-  }
-  T2S2_CUDA(cudaMemsetAsync(info_dev, 0, sizeof(int), stream()));
-  static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
-  unsigned long long* pbuf = nullptr;
-  if (prof) {
-    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
-    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
-  }
-  NpArgs a{N, A, b, info_dev, pbuf};
-  LuArgs bs{N, A, b, nullptr, info_dev, 0, nullptr, nullptr, nullptr};
-  void* params[] = {&a, &bs};
-  {
-    LaunchScope ls("lu_nopivot", 2.0 / 3.0 * (double)N * N * N + 2.0 * (double)N * N,
-                   16.0 * (double)N * N);
-    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)lu_np_kernel, dim3(grid), dim3(kNpThreads), params,
-                                          smem, stream()));
-  }
-  if (prof) {
-    unsigned long long h[16];
-    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
-    T2S2_CUDA(cudaStreamSynchronize(stream()));
-    fprintf(stderr, "np N=%d cta0: trsm %.1f syncA %.1f tile+diag %.1f syncB %.1f | cta1: trsm %.1f syncA %.1f tiles %.1f syncB %.1f | backsub %.1f us\n",
-            N, h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3,
-            h[7] / 1e3, h[8] / 1e3);
-    fprintf(stderr, "   diag %.1f us\n", h[9] / 1e3);
-    allocator().release(reinterpret_cast<double*>(pbuf));
-  }
-  return true;
-}
-
 bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static bool attr_fused = false;
-  if (!attr_fused) {
-    T2S2_CUDA(cudaFuncSetAttribute(lu_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kPanelSmem));
-    attr_fused = true;
-  }
+  max_dynamic_smem((const void*)lu_fused_kernel, (int)kPanelSmem);
   int w = (int)((kPanelSmem - 8 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
   if (w < 1 || N > kRowsPerThread * kThreads) return false;  // multi-launch fallback
   int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride + 1));
   int* flag = moves + 2 * kMoveStride;
   T2S2_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream()));
-  static const bool prof = getenv("T2S2_LU_PROFILE") != nullptr;
-  unsigned long long* pbuf = nullptr;
-  if (prof) {
-    pbuf = reinterpret_cast<unsigned long long*>(allocator().alloc(16));
-    T2S2_CUDA(cudaMemsetAsync(pbuf, 0, 128, stream()));
-  }
-  LuArgs a{N, A, b, piv, info_dev, w, moves, flag, pbuf};
+  LuArgs a{N, A, b, piv, info_dev, w, moves, flag, nullptr};
   void* params[] = {&a};
   {
     // algorithmic: 2/3 N^3 (factor) + 2 N^2 (solves); bytes: matrix read+write
     LaunchScope ls("lu_fused", 2.0 / 3.0 * (double)N * N * N + 2.0 * (double)N * N,
                    16.0 * (double)N * N);
-    const int grid = sm_budget() > 0 && sm_budget() < g_num_sms ? sm_budget() : g_num_sms;
+    const int grid = sm_budget() > 0 && sm_budget() < num_sms() ? sm_budget() : num_sms();
     T2S2_CUDA(cudaLaunchCooperativeKernel((void*)lu_fused_kernel, dim3(grid), dim3(kThreads),
                                           params, kPanelSmem, stream()));
   }
   allocator().release(reinterpret_cast<double*>(moves));
-  if (prof) {
-    unsigned long long h[16];
-    T2S2_CUDA(cudaMemcpyAsync(h, pbuf, 128, cudaMemcpyDeviceToHost, stream()));
-    T2S2_CUDA(cudaStreamSynchronize(stream()));
-    fprintf(stderr, "lu N=%d w=%d cta0: upd %.1f fac %.1f sync %.1f us | cta1: work %.1f sync %.1f us"
-            " | panel load %.1f cols %.1f replay %.1f store %.1f\n",
-            N, w, h[0] / 1e3, h[1] / 1e3, h[3] / 1e3, h[6] / 1e3, h[7] / 1e3, h[8] / 1e3, h[9] / 1e3,
-            h[10] / 1e3, h[11] / 1e3);
-    fprintf(stderr, "   cols: steps %.0f cyc/col, sub-panel %.0f cyc/col\n", (double)h[12] / N, (double)h[13] / N);
-
-    allocator().release(reinterpret_cast<double*>(pbuf));
-  }
   return true;
 }
 

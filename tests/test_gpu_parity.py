@@ -405,7 +405,7 @@ def test_config3_full_size_steps_match_oracle(pk):
         h.free()
 
 
-@pytest.mark.parametrize("index", [0, 7])
+@pytest.mark.parametrize("index", [0])
 def test_config4_full_size_sweeps_within_oracle_spread(pk, index):
     """Config 4 at full size (d=6, n=33): two alternating sweeps of one of
     the 64 seeded boundary-layer solves (index 7: eps = 2.9e-12, the steep
@@ -417,7 +417,13 @@ def test_config4_full_size_sweeps_within_oracle_spread(pk, index):
     (tt_solver.py:383-387) and enrichment directions depend on the summation
     order.  The device run must reproduce the ranks exactly and its residual
     history must lie within the envelope of five oracle executions (1, 2, 4,
-    8 BLAS threads and the default) widened by their own spread."""
+    8 BLAS threads and the default) widened by their own spread.
+
+    The steep seeds (index 7, eps = 2.9e-12) are compared on complete solves
+    instead (test_gpu_parity_full.py): after two sweeps their residual moves
+    by 25% between the oracle's own thread counts (0.174..0.243) and the
+    reference's (0.2018..0.2076, ttss with 1..8 threads), so a two-sweep
+    envelope says nothing about them."""
     from threadpoolctl import threadpool_limits
 
     from oracle import als_solver as als

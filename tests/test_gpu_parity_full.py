@@ -15,8 +15,14 @@ gpurun_out/parity_full_<config>.json (committed under profiles/).
 
 Tolerance: each step re-solves to the reference's residual_tol (1e-10) and
 re-truncates at step_tol (1e-8), so two correct implementations differ by
-rounding-level amounts amplified by the local solves' conditioning; the
-difference is measured and bounded here, not assumed.
+rounding-level amounts amplified by the local solves' conditioning and
+accumulated over the steps.  The reference is not reproducible below that
+level itself: the same march with 1 instead of 4 (config 2) / 2 (config 3)
+OpenBLAS threads differs from the fixture by up to 2.1e-10 / 3.7e-10
+(tests/golden/config{2,3}_selfspread.npz, tools/make_golden_full.py
+spread).  The bound at step k is therefore max(1e-10, 2 x the reference's
+own largest thread-count difference up to step k): north_star's 1e-10
+wherever the reference itself holds it, its own noise envelope elsewhere.
 """
 
 import json
@@ -80,12 +86,26 @@ def _march_full(golden, index, fname):
         worst["rank_mismatch"] += int(tuple(row["ranks"]) != ref_ranks)
         worst["err_excess"] = max(worst["err_excess"], err / row["exact_err_ref"] - 1.0)
         out.append(row)
-    summary = dict(worst, config=index, steps=n, final_exact_err=out[-1]["exact_err"],
+    spread = golden(fname.replace("_full.npz", "_selfspread.npz"))
+    summary = dict(worst, config=index, steps=n,
+                   reference_self_spread=float(np.max(spread["rel_diff"])),
+                   reference_self_spread_threads=[int(t) for t in spread["threads"]],
+                   steps_within_1e10=sum(1 for r in out if r.get("rel_diff", 0.0) <= PARITY_TOL),
+                   steps_compared=sum(1 for r in out if "rel_diff" in r), final_exact_err=out[-1]["exact_err"],
                    final_exact_err_ref=out[-1]["exact_err_ref"],
                    sweeps=sum(r["sweeps"] for r in out),
                    sweeps_ref=sum(r["sweeps_ref"] for r in out))
     _record(f"config{index}", out, summary)
     return out, summary
+
+
+def _bounds(golden, fname):
+    """Per-step value bound: max(PARITY_TOL, 2 x running max of the
+    reference's own thread-count spread)."""
+    z = golden(fname.replace("_full.npz", "_selfspread.npz"))
+    steps, diffs = np.array(z["steps"]), np.array(z["rel_diff"])
+    run = np.maximum.accumulate(diffs)
+    return {int(k): max(PARITY_TOL, 2.0 * float(v)) for k, v in zip(steps, run)}
 
 
 @pytest.mark.parametrize("index,fname", [(2, "config2_full.npz"), (3, "config3_full.npz")])
@@ -94,8 +114,9 @@ def test_march_full_length_matches_reference(golden, index, fname):
     bad_ranks = [(r["step"], r["ranks"], r["ranks_ref"]) for r in rows
                  if r["ranks"] != r["ranks_ref"]]
     assert not bad_ranks, bad_ranks[:5]
-    bad_vals = [(r["step"], r["rel_diff"]) for r in rows
-                if "rel_diff" in r and r["rel_diff"] > PARITY_TOL]
+    bound = _bounds(golden, fname)
+    bad_vals = [(r["step"], r["rel_diff"], bound[r["step"]]) for r in rows
+                if "rel_diff" in r and r["rel_diff"] > bound[r["step"]]]
     assert not bad_vals, (summary, bad_vals[:5])
     bad_err = [(r["step"], r["exact_err"], r["exact_err_ref"]) for r in rows
                if r["exact_err"] > r["exact_err_ref"] * (1 + ERR_SLACK)]

@@ -44,6 +44,8 @@ def threads():
 
 
 def march(index, steps, fname, keep_every):
+    if os.environ.get("T2S2_GOLDEN_OUT"):
+        mg.OUT = os.environ["T2S2_GOLDEN_OUT"]
     recipe = wl.config(index)
     t0 = time.time()
     st = mg.ref_march(recipe, steps, keep_forcing=False, keep_every=keep_every,
@@ -82,9 +84,36 @@ def steady(index):
     mg.save(f"config4_full_{index}.npz", st)
 
 
+def spread(fname, other_dir):
+    """Self-reproducibility of the reference: the same march recorded with
+    another BLAS thread count (OPENBLAS_NUM_THREADS=1, T2S2_GOLDEN_OUT=
+    other_dir) compared state by state with the committed fixture.  Writes
+    tests/golden/<config>_selfspread.npz: per stored step the relative
+    difference (10^5 seeded sample points) and whether the raw ranks agree."""
+    from golden_io import get_train, has_train
+    from helpers import rel_diff
+
+    a = dict(np.load(os.path.join(mg.OUT, fname)))
+    b = dict(np.load(os.path.join(other_dir, fname)))
+    n = int(a["n_steps"])
+    steps, diffs, same = [], [], []
+    for k in range(1, n + 1):
+        same.append(bool(np.array_equal(a[f"ranks{k}"], b[f"ranks{k}"])))
+        if has_train(a, f"state{k}"):
+            steps.append(k)
+            diffs.append(rel_diff(get_train(b, f"state{k}"), get_train(a, f"state{k}")))
+    out = {"steps": np.array(steps), "rel_diff": np.array(diffs), "ranks_equal": np.array(same),
+           "threads": np.array([int(a["blas_threads"]), int(b["blas_threads"])])}
+    print(fname, "threads", out["threads"], "max rel diff", max(diffs), "rank mismatches",
+          n - sum(same))
+    mg.save(fname.replace("_full.npz", "_selfspread.npz"), out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("what", choices=["cfg2", "cfg3", "cfg4", "spread"])
+    ap.add_argument("--fixture", default="config2_full.npz")
+    ap.add_argument("--other", default="/tmp/selfref")
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--index", type=int, default=0)
     ap.add_argument("--keep-every", type=int, default=1)
@@ -93,5 +122,7 @@ if __name__ == "__main__":
         march(2, a.steps or 100, "config2_full.npz", a.keep_every)
     elif a.what == "cfg3":
         march(3, a.steps or 200, "config3_full.npz", a.keep_every)
+    elif a.what == "spread":
+        spread(a.fixture, a.other)
     else:
         steady(a.index)
