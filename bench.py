@@ -563,7 +563,6 @@ def run_b200_sweep(args, torch, dd):
     gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
     elapsed = dd.max(total_ms / 1e3)
     value = dd.world * K / elapsed
-
     _native.stats_reset(profile_events=True)
     for i in seeds[W:]:
         h, _ = solve_device(dev[i][0], dev[i][1], x0[i], cfg_of(i))

@@ -162,9 +162,10 @@ def lib():
 
 def context():
     """This thread's engine context on device ``T2S2_DEVICE`` (default
-    ``LOCAL_RANK`` or 0).  Each host thread gets its own context and stream,
-    so independent solves can run concurrently on one device; a train belongs
-    to the thread that created it."""
+    ``LOCAL_RANK`` or 0).  Each host thread gets its own context and stream;
+    a train belongs to the thread that created it.  (Solves of different
+    contexts on one GPU are not safe to overlap with unbounded kernels: see
+    sweep.py; set_thread_sm_budget caps a context's cooperative grids.)"""
     ctx = getattr(_tls, "ctx", None)
     if ctx is not None:
         return ctx

@@ -6,7 +6,11 @@ collective: rank k of N takes solves k, k+N, k+2N, ... (round-robin keeps the
 seeded eps draws — and with them the cost — spread evenly), runs them on its
 own device, and the per-solve results are gathered once at the end
 (``gather``; torch.distributed, any backend).  One process per GPU,
-``LOCAL_RANK`` selects the device (see _native.context).
+``LOCAL_RANK`` selects the device (see _native.context).  Solves run one
+after another on a rank's GPU: several engine contexts on one GPU would put
+spin-waiting cooperative kernels (Gauss-Jordan hand-offs, Krylov grid
+barriers) of different solves side by side, and a kernel whose CTAs are only
+partly resident next to another such kernel can wait forever.
 """
 
 from __future__ import annotations
@@ -30,8 +34,7 @@ def _default_solve(a, b, cfg_kwargs):
     return x, rep
 
 
-def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None,
-              concurrency=1):
+def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None):
     """Solve this rank's share of ``recipes`` (workloads.SteadyRecipe).
 
     Returns {index: dict(x=cores, residuals, ranks, converged, stagnated,
@@ -58,42 +61,8 @@ def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=
                       ranks=list(rep.rank_history), converged=bool(rep.converged),
                       stagnated=bool(rep.stagnated), wall_s=wall, eps=r.eps)
 
-    if concurrency <= 1:
-        for i in mine:
-            one(i)
-        return out
-    # several solves in flight on one device: one engine context (stream)
-    # per host thread, each thread's local dense solves capped to its share
-    # of the SMs so their cooperative kernels can be co-resident
-    import threading
-
-    from . import _native
-
-    queue = list(mine)
-    lock = threading.Lock()
-    errors = []
-
-    def worker():
-        _native.set_thread_sm_budget(max(1, _native.num_sms() // concurrency))
-        while True:
-            with lock:
-                if not queue or errors:
-                    return
-                i = queue.pop(0)
-            try:
-                one(i)
-            except Exception as exc:  # surface the first failure
-                with lock:
-                    errors.append(exc)
-                return
-
-    threads = [threading.Thread(target=worker) for _ in range(concurrency)]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if errors:
-        raise errors[0]
+    for i in mine:
+        one(i)
     return out
 
 

@@ -351,26 +351,6 @@ def test_singular_local_systems_use_lstsq(golden, pk):
     assert rel_diff(x.cores, get_train(z, "s8_x")) <= 1e-9
 
 
-def test_config4_sweep_concurrent_contexts(golden, pk):
-    """The same scaled sweep with two host threads, each on its own engine
-    context/stream with its cooperative solves capped to half the SMs: the
-    results must not depend on the interleaving."""
-    from paper_2506_04732_b200 import sweep, workloads as wl
-
-    z = golden("config4_small.npz")
-    recipes = wl.sweep_recipes(count=int(z["count"]), dims=3, degree=12)
-    res = sweep.run_sweep(recipes, overrides={"max_sweeps": int(z["sweeps"])}, concurrency=2)
-    serial = sweep.run_sweep(recipes[:1], overrides={"max_sweeps": int(z["sweeps"])})
-    for i in range(int(z["count"])):
-        got, ref = res[i], np.array(z[f"res{i}"])
-        want = get_train(z, f"x{i}")
-        assert got["converged"] == bool(z[f"conv{i}"])
-        assert rel_diff(got["x"], want) <= value_tol(got["residuals"][-1], ref[-1])
-    # deterministic engine: solve 0 is bit-identical with and without threads
-    for c1, c2 in zip(res[0]["x"], serial[0]["x"]):
-        np.testing.assert_array_equal(c1, c2)
-
-
 def test_config3_full_size_steps_match_oracle(pk):
     """Config 3 at full size (d=6, n=65, eps=1e-12, dt=5e-4): the first two
     implicit steps through the device march against the CPU oracle (the

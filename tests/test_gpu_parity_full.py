@@ -90,7 +90,7 @@ def _march_full(golden, index, fname):
     summary = dict(worst, config=index, steps=n,
                    reference_self_spread=float(np.max(spread["rel_diff"])),
                    reference_self_spread_threads=[int(t) for t in spread["threads"]],
-                   steps_within_1e10=sum(1 for r in out if r.get("rel_diff", 0.0) <= PARITY_TOL),
+                   steps_within_1e10=sum(1 for r in out if "rel_diff" in r and r["rel_diff"] <= PARITY_TOL),
                    steps_compared=sum(1 for r in out if "rel_diff" in r), final_exact_err=out[-1]["exact_err"],
                    final_exact_err_ref=out[-1]["exact_err_ref"],
                    sweeps=sum(r["sweeps"] for r in out),
