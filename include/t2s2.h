@@ -18,6 +18,10 @@
  *   t2s2_residual  <- tt_solver.residual         (tt_solver.py:80)
  *   t2s2_march     <- time_integration._march    (time_integration.py:149)
  *
+ * Instrumentation without a reference counterpart: t2s2_stats_reset /
+ * t2s2_stats_read / t2s2_launch_log (per-family and per-launch kernel
+ * accounting), t2s2_dense_solve / t2s2_gemm (kernel test hooks).
+ *
  * Trains cross the boundary as plain arrays: d, per-core row (and, for
  * operators, column) mode sizes, d+1 bond ranks, and all cores
  * concatenated row-major in float64 — the layout of the reference's
@@ -113,6 +117,19 @@ int t2s2_synchronize(t2s2_context* ctx);
  * around every launch (adds ~2 us per launch). */
 int t2s2_stats_reset(t2s2_context* ctx, int profile_events);
 int t2s2_stats_read(t2s2_context* ctx, t2s2_kernel_stat* out, int capacity, int* count);
+
+/* Instrumentation (no reference counterpart): while profile_events is on,
+ * one record per launch in launch order — family index (the order of
+ * t2s2_stats_read), algorithmic flops and bytes, CUDA-event duration.  At
+ * most T2S2_LAUNCH_LOG_CAP records are kept per reset. */
+#define T2S2_LAUNCH_LOG_CAP 1000000
+typedef struct {
+  int family;
+  double flops;
+  double bytes;
+  double device_ms;
+} t2s2_launch_record;
+int t2s2_launch_log(t2s2_context* ctx, t2s2_launch_record* out, int capacity, int* count);
 
 /* cols == NULL uploads a vector train (cores r0 x rows x r1), otherwise an
  * operator train (cores r0 x rows x cols x r1).  host_cores holds the

@@ -90,6 +90,15 @@ class KernelStatC(ctypes.Structure):
     ]
 
 
+class LaunchRecordC(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int),
+        ("flops", ctypes.c_double),
+        ("bytes", ctypes.c_double),
+        ("device_ms", ctypes.c_double),
+    ]
+
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _D = ctypes.c_double
@@ -105,6 +114,7 @@ _SIGNATURES = {
     "t2s2_context_set_sm_budget": (_I, [_P, _I]),
     "t2s2_stats_reset": (_I, [_P, _I]),
     "t2s2_stats_read": (_I, [_P, ctypes.POINTER(KernelStatC), _I, _IP]),
+    "t2s2_launch_log": (_I, [_P, ctypes.POINTER(LaunchRecordC), _I, _IP]),
     "t2s2_train_upload": (_I, [_P, _I, _IP, _IP, _IP, _DP, ctypes.POINTER(_P)]),
     "t2s2_train_upload_device": (_I, [_P, _I, _IP, _IP, _IP, _P, ctypes.POINTER(_P)]),
     "t2s2_train_shape": (_I, [_P, _IP, _IP, _IP, _IP, ctypes.POINTER(ctypes.c_size_t)]),
@@ -229,6 +239,18 @@ def stats_read():
                                          device_ms=float(buf[i].device_ms),
                                          flops=float(buf[i].flops), bytes=float(buf[i].bytes))
             for i in range(n.value)}
+
+
+def launch_log():
+    """Per-launch records [(family, flops, bytes, device_ms)] since the last
+    stats_reset(profile_events=True), in launch order."""
+    names = list(stats_read())
+    n = ctypes.c_int()
+    check(lib().t2s2_launch_log(context(), None, 0, ctypes.byref(n)))
+    buf = (LaunchRecordC * max(n.value, 1))()
+    check(lib().t2s2_launch_log(context(), buf, n.value, ctypes.byref(n)))
+    return [(names[buf[i].family], buf[i].flops, buf[i].bytes, buf[i].device_ms)
+            for i in range(n.value)]
 
 
 def dense_solve(a, b):

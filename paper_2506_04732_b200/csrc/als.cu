@@ -507,11 +507,12 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
 // Dense direct solve of a column-major N x N system; the LU info (0, or
 // 1 + first zero pivot) lands in *info_dev and is read back by the caller.
 // Partial-pivoting dense solve (the reference's numpy.linalg.solve).
+// info_dev[1] (set to 1, never cleared here) records a row interchange.
 void dense_solve_pivoted(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   const int N = M.dim(0);
   int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
   out = rhs.clone();
-  if (!lu_solve_fused(N, M.p, out.p, ipiv, info_dev)) {
+  if (!lu_solve_fused(N, M.p, out.p, ipiv, info_dev, info_dev + 1)) {
     lu_factor(N, M.p, ipiv, info_dev);
     lu_solve(N, M.p, ipiv, out.p);
   }
@@ -527,6 +528,33 @@ void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
   if (gj_solve_nopivot(M.dim(0), M.p, out.p, info_dev)) return;
   dense_solve_pivoted(M, rhs, out, info_dev);
 }
+
+// Which dense kernel a kind of local system tries first.  The no-pivot
+// Gauss-Jordan kernel declines (in its first panels) when partial pivoting
+// would interchange rows; after four declines in a row the pivoting kernel
+// runs directly, and as soon as one of its solves makes no interchange
+// (info[1] == 0: the no-pivot kernel would have accepted) the no-pivot
+// kernel is tried first again.  Results are those of the kernel that
+// accepts, so the policy only removes declined launches.
+struct PivotPolicy {
+  int declines = 0;
+  bool pivot_first = false;
+  void solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) const {
+    if (pivot_first)
+      dense_solve_pivoted(M, rhs, out, info_dev);
+    else
+      dense_solve(M, rhs, out, info_dev);
+  }
+  void observe(int info, int swapped) {  // after the first attempt of a system
+    if (pivot_first) {
+      if (info == 0 && swapped == 0) pivot_first = false, declines = 0;
+    } else if (info == -1) {
+      if (++declines >= 4) pivot_first = true;
+    } else if (info == 0) {
+      declines = 0;
+    }
+  }
+};
 
 // Minimum-norm least squares of a singular column-major N x N system, the
 // reference's fallback when numpy.linalg.solve raises (tt_solver.py:362,
@@ -556,7 +584,8 @@ struct Probe {
   Probe() { T2S2_CUDA(cudaMemsetAsync(buf.p, 0, 16 * sizeof(double), stream())); }
   int* info() { return reinterpret_cast<int*>(buf.p + 12); }
   unsigned* ticket() { return reinterpret_cast<unsigned*>(buf.p + 14); }
-  void clear_info() { T2S2_CUDA(cudaMemsetAsync(info(), 0, sizeof(int), stream())); }
+  // info()[0]: LU info; info()[1]: a pivoted solve interchanged rows
+  void clear_info() { T2S2_CUDA(cudaMemsetAsync(info(), 0, 2 * sizeof(int), stream())); }
   void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c) {
     const int n = (int)u.size();
     int nb = (n + 255) / 256;
@@ -569,13 +598,14 @@ struct Probe {
     T2S2_CHECK_LAUNCH();
     allocator().release(part);
   }
-  // one read-back: h[3*slot + {0,1,2}], info at h_info
-  void read(double* h, int* h_info) {
+  // one read-back: h[3*slot + {0,1,2}], info at h_info, interchange flag
+  void read(double* h, int* h_info, int* h_swapped = nullptr) {
     double tmp[16];
     T2S2_CUDA(cudaMemcpyAsync(tmp, buf.p, sizeof tmp, cudaMemcpyDeviceToHost, stream()));
     T2S2_CUDA(cudaStreamSynchronize(stream()));
     for (int i = 0; i < 12; ++i) h[i] = tmp[i];
-    *h_info = *reinterpret_cast<int*>(tmp + 12);
+    *h_info = reinterpret_cast<int*>(tmp + 12)[0];
+    if (h_swapped) *h_swapped = reinterpret_cast<int*>(tmp + 12)[1];
   }
 };
 
@@ -800,6 +830,7 @@ struct Sweep {
   }
 
   Probe probe;
+  PivotPolicy pol_gal, pol_ls;  // Galerkin / normal-equation systems
   bool gal_direct = false;  // the last update's Galerkin candidate came from a dense solve
 
   // Guarded update of core l (tt_solver.py:337-422).  Candidate scores
@@ -831,7 +862,7 @@ struct Sweep {
     if (try_gal) {
       if (direct) {
         DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
-        dense_solve(B, c_gal, u_gal, probe.info());
+        pol_gal.solve(B, c_gal, u_gal, probe.info());
       } else {
         // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
         u_gal = u_old.clone();
@@ -844,8 +875,9 @@ struct Sweep {
       probe.run(1, u_gal, nu_gal, c_ls);
     }
     double h[12];
-    int info = 0;
-    probe.read(h, &info);
+    int info = 0, swapped = 0;
+    probe.read(h, &info, &swapped);
+    if (try_gal && direct) pol_gal.observe(info, swapped);
     if (try_gal && direct && info == -1) {
       // the block needs row interchanges: rebuild it, partial pivoting
       DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
@@ -890,7 +922,7 @@ struct Sweep {
       if (direct) {
         DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
         Nm.view({(int)size, (int)size});
-        dense_solve(Nm, c_ls, u_ls, probe.info());
+        pol_ls.solve(Nm, c_ls, u_ls, probe.info());
       } else {
         // scipy cg(x0=u_old, rtol, atol=0, maxiter=250, M=diag^{-1})
         u_ls = u_old.clone();
@@ -901,7 +933,8 @@ struct Sweep {
       u_ls.view(u_old.shape);
       DTensor nu_ls = nop.apply(u_ls);
       probe.run(2, u_ls, nu_ls, c_ls);
-      probe.read(h, &info);
+      probe.read(h, &info, &swapped);
+      if (direct) pol_ls.observe(info, swapped);
       if (direct && info == -1) {
         DTensor Nm = normal_matrix(ln[l], ac, rn[l + 1]);
         Nm.view({(int)size, (int)size});

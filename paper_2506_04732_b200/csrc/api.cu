@@ -21,6 +21,7 @@ struct FamilyStat {
 };
 struct Pending {
   int fam;
+  double flops, bytes;
   cudaEvent_t a, b;
 };
 }  // namespace t2s2
@@ -42,6 +43,7 @@ struct t2s2_context {
   std::vector<cudaEvent_t> event_pool;
   size_t pool_used = 0;
   std::vector<t2s2::Pending> pending;
+  std::vector<t2s2_launch_record> launch_log;  // per launch while profiling
 };
 
 struct t2s2_train {
@@ -113,7 +115,7 @@ LaunchScope::LaunchScope(const char* family, double flops, double bytes) {
     if (cudaEventCreate(&e) != cudaSuccess) return;
     c->event_pool.push_back(e);
   }
-  Pending p{f, c->event_pool[c->pool_used], c->event_pool[c->pool_used + 1]};
+  Pending p{f, flops, bytes, c->event_pool[c->pool_used], c->event_pool[c->pool_used + 1]};
   c->pool_used += 2;
   cudaEventRecord(p.a, c->stream);
   slot = (int)c->pending.size();
@@ -131,6 +133,8 @@ void resolve_pending(t2s2_context* c) {
   for (auto& p : c->pending) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) c->fams[p.fam].ms += ms;
+    if (c->launch_log.size() < (size_t)T2S2_LAUNCH_LOG_CAP)
+      c->launch_log.push_back(t2s2_launch_record{p.fam, p.flops, p.bytes, (double)ms});
   }
   c->pending.clear();
   c->pool_used = 0;
@@ -297,7 +301,17 @@ int t2s2_stats_reset(t2s2_context* ctx, int profile_events) {
   return guarded(ctx, [&] {
     resolve_pending(ctx);
     for (auto& f : ctx->fams) f = FamilyStat{f.name};
+    ctx->launch_log.clear();
     ctx->profiling = profile_events != 0;
+  });
+}
+
+int t2s2_launch_log(t2s2_context* ctx, t2s2_launch_record* out, int capacity, int* count) {
+  return guarded(ctx, [&] {
+    resolve_pending(ctx);
+    const int n = (int)ctx->launch_log.size();
+    if (count) *count = n;
+    for (int i = 0; i < n && i < capacity && out; ++i) out[i] = ctx->launch_log[i];
   });
 }
 

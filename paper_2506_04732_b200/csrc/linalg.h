@@ -28,7 +28,9 @@ void lu_factor(int N, double* A, int* ipiv, int* info_dev);
 void lu_solve(int N, const double* LU, const int* ipiv, double* b);
 // One cooperative launch: factor A (clobbered) and overwrite b with the
 // solution.  Returns false when N is too large for the smem panel.
-bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev);
+// *swapped (optional, not cleared here) is set to 1 if any row was
+// interchanged, i.e. when the no-pivot kernel would have declined.
+bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev, int* swapped = nullptr);
 // Verified no-pivot dense solve by blocked Gauss-Jordan (one cooperative
 // launch, gj_solve.cu): when partial pivoting would make no interchange —
 // every multiplier |l| <= 1 — it computes GEPP's factors without a pivot

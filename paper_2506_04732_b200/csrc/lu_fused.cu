@@ -55,7 +55,8 @@ struct LuArgs {
   int w;         // panel width
   int* moves;    // per panel: count, then (dst, src) row offsets relative to k0
   int* flag;     // next-panel chunk completion counter (zeroed by the host)
-  unsigned long long* prof;  // optional phase timers (ns): see lu_solve_fused
+  unsigned long long* prof;  // optional phase timers (ns), null in the product
+  int* swapped;  // optional: set to 1 when any row interchange was made
 };
 
 __device__ __forceinline__ void dmma_8x8x4_lu(double& d0, double& d1, double a, double b) {
@@ -373,7 +374,10 @@ __device__ __forceinline__ void factor_panel(const LuArgs& a, int k0, int w, dou
       mv[1 + 2 * (n1 + k)] = p;
       mv[2 + 2 * (n1 + k)] = q;
     }
-    if (lane == 0) mv[0] = n1 + __popc(high_mask);
+    if (lane == 0) {
+      mv[0] = n1 + __popc(high_mask);
+      if (mv[0] > 0 && a.swapped) *a.swapped = 1;
+    }
     const unsigned zero = __ballot_sync(full, act && sm[lane * rows + p] == 0.0);
     if (lane == 0 && zero && *a.info == 0) *a.info = k0 + __ffs(zero);
   }
@@ -753,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1) lu_fused_kernel(LuArgs a) {
 
 }  // namespace
 
-bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
+bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev, int* swapped) {
   max_dynamic_smem((const void*)lu_fused_kernel, (int)kPanelSmem);
   int w = (int)((kPanelSmem - 8 * (size_t)N) / (sizeof(double) * (size_t)N));
   if (w > kMaxPanel) w = kMaxPanel;
@@ -761,7 +765,7 @@ bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev) {
   int* moves = reinterpret_cast<int*>(allocator().alloc(kMoveStride + 1));
   int* flag = moves + 2 * kMoveStride;
   T2S2_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), stream()));
-  LuArgs a{N, A, b, piv, info_dev, w, moves, flag, nullptr};
+  LuArgs a{N, A, b, piv, info_dev, w, moves, flag, nullptr, swapped};
   void* params[] = {&a};
   {
     // algorithmic: 2/3 N^3 (factor) + 2 N^2 (solves); bytes: matrix read+write
