@@ -39,6 +39,7 @@ pytestmark = pytest.mark.gpu
 
 PARITY_TOL = 1e-10       # north_star: full-grid relative agreement
 ERR_SLACK = 1e-6         # relative slack on the manufactured-solution error
+PLATEAU_FACTOR = 3.0     # config 4 plateau envelope (see the config-4 test)
 
 
 def _record(name, rows, summary):
@@ -121,3 +122,55 @@ def test_march_full_length_matches_reference(golden, index, fname):
     bad_err = [(r["step"], r["exact_err"], r["exact_err_ref"]) for r in rows
                if r["exact_err"] > r["exact_err_ref"] * (1 + ERR_SLACK)]
     assert not bad_err, bad_err[:5]
+
+
+# -- config 4: complete steady solves -------------------------------------------------
+
+
+def _solve_full(golden, index):
+    from helpers import sample_entries
+    from paper_2506_04732_b200 import _native, solver, tt, workloads as wl
+
+    _native.context()
+    z = golden(f"config4_full_{index}.npz")
+    r = wl.sweep_recipes()[index]
+    a, b, exact, _ = wl.steady_problem(r)
+    x0 = tt.TTVector(get_train(z, "x0"))
+    x, rep = solver.solve(a, b, x0=x0, cfg=solver.SolverConfig(**r.solver))
+    err = ot.tt_norm(ot.tt_add(x.cores, ot.tt_scale(exact.cores, -1.0))) / ot.tt_norm(exact.cores)
+    rng = np.random.default_rng(int(z["sample_idx_seed"]))
+    idx = np.column_stack([rng.integers(0, n, 10000) for n in x.mode_sizes])
+    xs, ref = sample_entries(x.cores, idx), np.array(z["x_samples"])
+    out = {
+        "index": index, "eps": float(z["eps"]),
+        "sweeps": len(rep.residual_history), "sweeps_ref": int(np.array(z["res"]).size),
+        "converged": rep.converged, "converged_ref": bool(z["conv"]),
+        "stagnated": rep.stagnated, "stagnated_ref": bool(z["stag"]),
+        "ranks": list(x.ranks), "ranks_ref": [int(v) for v in z["x_ranks"]],
+        "rank_history": rep.rank_history, "rank_history_ref": [int(v) for v in z["ranks"]],
+        "residuals": rep.residual_history, "residuals_ref": [float(v) for v in z["res"]],
+        "exact_err": float(err), "exact_err_ref": float(z["exact_err"]),
+        "sample_rel_diff": float(np.linalg.norm(xs - ref) / np.linalg.norm(ref)),
+        "wall_s": rep.wall_time, "wall_s_ref": float(z["wall"]),
+    }
+    _record(f"config4_{index}", [], out)
+    return out
+
+
+@pytest.mark.parametrize("index", [0, 2, 7])
+def test_config4_complete_solve_matches_reference(golden, index):
+    """A complete config-4 solve (d=6, n=33, 40 sweeps, rank cap 64) against
+    ttss's own complete solve of the same seed.  These solves do not
+    converge in the reference either: ranks reach the cap and the residual
+    decreases slowly to the sweep limit (a rank-capped plateau), where the
+    iterate is path dependent.  Checked: the same verdict and sweep count,
+    the rank history, and the plateau — final residual and
+    manufactured-solution error no worse than the reference's beyond the
+    reference's own thread-count spread (config4_selfspread)."""
+    o = _solve_full(golden, index)
+    assert (o["converged"], o["stagnated"]) == (o["converged_ref"], o["stagnated_ref"]), o
+    assert o["sweeps"] == o["sweeps_ref"], o
+    assert max(o["ranks"]) == max(o["ranks_ref"]) == 64
+    assert o["rank_history"] == o["rank_history_ref"], o
+    assert o["residuals"][-1] <= PLATEAU_FACTOR * o["residuals_ref"][-1], o
+    assert o["exact_err"] <= PLATEAU_FACTOR * o["exact_err_ref"], o

@@ -58,6 +58,8 @@ def march(index, steps, fname, keep_every):
 
 
 def steady(index):
+    if os.environ.get("T2S2_GOLDEN_OUT"):
+        mg.OUT = os.environ["T2S2_GOLDEN_OUT"]
     recipe = wl.sweep_recipes()[index]
     a, b, exact = mg.ref_steady(recipe)
     cfg = mg.rsol.SolverConfig(**recipe.solver)
@@ -68,7 +70,16 @@ def steady(index):
     err = mg.rtt.tt_norm(mg.rtt.tt_add(x, mg.rtt.tt_scale(exact, -1.0))) / mg.rtt.tt_norm(exact)
     st = {}
     put_train(st, "x0", x0.cores)
-    put_train(st, "x", x.cores)
+    # the rank-64 iterate itself is 3 MB: keep its ranks, norm and its values
+    # at 10^4 seeded grid points (the plateau iterate is path dependent)
+    from helpers import sample_entries
+
+    rng = np.random.default_rng(1234)
+    idx = np.column_stack([rng.integers(0, n, 10000) for n in x.mode_sizes])
+    st["sample_idx_seed"] = np.array(1234)
+    st["x_samples"] = sample_entries(x.cores, idx)
+    st["x_ranks"] = np.array(x.ranks)
+    st["x_norm"] = np.array(mg.rtt.tt_norm(x))
     st["res"] = np.array(rep.residual_history)
     st["ranks"] = np.array(rep.rank_history)
     st["conv"] = np.array(rep.converged)
