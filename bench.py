@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--workload", default="march", choices=["march", "sweep"])
     ap.add_argument("--sweep-sweeps", type=int, default=6,
                     help="ALS sweeps per config-4 solve (fixed budget)")
+    ap.add_argument("--sweep-partitions", type=int, default=4,
+                    help="run the timed solves on P disjoint SM partitions (green contexts)")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -512,6 +514,76 @@ def run_b200_march(args, torch, dd):
     }
 
 
+def partitioned_sweep(args, seeds, probs, recipes):
+    """The same solves on P disjoint SM partitions of this GPU (green
+    contexts), one host thread each pulling from a shared queue; returns the
+    batch makespan in seconds from the device's global timer (first start to
+    last end over all partitions)."""
+    import threading
+
+    from paper_2506_04732_b200 import _native
+    from paper_2506_04732_b200.solver import SolverConfig, _default_initial_guess, solve_device
+    from paper_2506_04732_b200.tt import to_device
+
+    P = args.sweep_partitions
+    sms = _native.sm_partitions(P)
+    queue = list(seeds)
+    lock = threading.Lock()
+    ready = threading.Barrier(P + 1)
+    go = threading.Event()
+    starts, ends, errors = [], [], []
+
+    def cfg_of(i):
+        return SolverConfig(**recipes[i].solver, max_sweeps=args.sweep_sweeps)
+
+    def worker(t):
+        mine = {}
+        try:
+            _native.use_partition(t)
+            for i in set(seeds):
+                a, b = probs[i][0], probs[i][1]
+                mine[i] = (to_device(a), to_device(b),
+                           to_device(_default_initial_guess(b, None, np.random.default_rng(0))))
+            i0 = seeds[0]  # warm-up: module load and shared-memory limits in this context
+            h, _ = solve_device(*mine[i0], SolverConfig(**recipes[i0].solver, max_sweeps=1))
+            h.free()
+            _native.synchronize()
+        except Exception as exc:
+            errors.append(exc)
+        ready.wait()
+        go.wait()
+        try:
+            if not errors:
+                t0 = _native.device_clock_ns()
+                while True:
+                    with lock:
+                        if not queue:
+                            break
+                        i = queue.pop(0)
+                    h, _ = solve_device(*mine[i], cfg_of(i))
+                    h.free()
+                t1 = _native.device_clock_ns()
+                with lock:
+                    starts.append(t0)
+                    ends.append(t1)
+        except Exception as exc:
+            errors.append(exc)
+        for hs in mine.values():
+            for h in hs:
+                h.free()
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(P)]
+    for th in threads:
+        th.start()
+    ready.wait()
+    go.set()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    return (max(ends) - min(starts)) * 1e-9, sms
+
+
 def run_b200_sweep(args, torch, dd):
     from paper_2506_04732_b200 import _native, workloads as wl
     from paper_2506_04732_b200.solver import SolverConfig, solve_device
@@ -563,6 +635,17 @@ def run_b200_sweep(args, torch, dd):
     gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
     elapsed = dd.max(total_ms / 1e3)
     value = dd.world * K / elapsed
+    serial = None
+    if args.sweep_partitions > 1:
+        # headline = the partitioned run; the one-stream run above is kept
+        l2_flush()
+        p_s, sms = partitioned_sweep(args, seeds[W:], probs, recipes)
+        p_s = dd.max(p_s)
+        serial = {"value": value, "ms_per_step": 1e3 * elapsed / K,
+                  "how": "one engine context on all 148 SMs, solves one after another, "
+                         "CUDA events per solve"}
+        elapsed = p_s
+        value = dd.world * K / elapsed
     _native.stats_reset(profile_events=True)
     for i in seeds[W:]:
         h, _ = solve_device(dev[i][0], dev[i][1], x0[i], cfg_of(i))
@@ -617,7 +700,11 @@ def run_b200_sweep(args, torch, dd):
             "l2": "256 MiB write between timed solves (not timed)",
             "rank0_timed": [{"seed": i, "residual": r, "max_rank": m} for i, r, m in reports],
             "sweeps_timed_rank0": sweeps,
+            "sm_partitions": (f"{args.sweep_partitions} green contexts of "
+                              f"{sms} SMs, one host thread each, shared queue; makespan from "
+                              "the device global timer" if args.sweep_partitions > 1 else None),
         }),
+        "serial": serial,
         "roofline": roof, "kernels": kernels, "gpu_launches": gpu_launches,
         "e2e": {"value": dd.world * K / e2e_elapsed, "unit": SWEEP["unit"],
                 "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K},

@@ -100,6 +100,19 @@ typedef struct {
 } t2s2_kernel_stat;
 
 int t2s2_context_create(int device, t2s2_context** out);
+/* SM partitions (no reference counterpart: B200 throughput feature for
+ * independent solves, BASELINE config 4).  t2s2_sm_partitions splits the
+ * device's SMs into `count` disjoint green contexts once per process and
+ * writes each partition's SM count to sms_out[count]; a context created on
+ * partition `part` runs all its kernels on those SMs only, so independent
+ * solves in different host threads cannot block each other's cooperative
+ * kernels. */
+int t2s2_sm_partitions(int device, int count, int* sms_out);
+int t2s2_context_create_on_partition(int device, int part, t2s2_context** out);
+/* Instrumentation: the device's global nanosecond timer, read by a kernel
+ * on the context's stream once its earlier work has run (blocking); one
+ * clock for all contexts and partitions of the device. */
+int t2s2_device_clock(t2s2_context* ctx, unsigned long long* out_ns);
 void t2s2_context_destroy(t2s2_context* ctx);
 const char* t2s2_last_error(const t2s2_context* ctx);
 /* Limit whole-GPU cooperative kernels (the local dense solves) to `sms`

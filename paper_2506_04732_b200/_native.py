@@ -107,6 +107,9 @@ _DP = ctypes.POINTER(ctypes.c_double)
 
 _SIGNATURES = {
     "t2s2_context_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "t2s2_sm_partitions": (_I, [_I, _I, _IP]),
+    "t2s2_context_create_on_partition": (_I, [_I, _I, ctypes.POINTER(_P)]),
+    "t2s2_device_clock": (_I, [_P, ctypes.POINTER(ctypes.c_ulonglong)]),
     "t2s2_context_destroy": (None, [_P]),
     "t2s2_last_error": (ctypes.c_char_p, [_P]),
     "t2s2_synchronize": (_I, [_P]),
@@ -180,17 +183,51 @@ def context():
     if ctx is not None:
         return ctx
     l = lib()
-    dev = int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    dev = device_index()
     h = _P()
-    rc = l.t2s2_context_create(dev, ctypes.byref(h))
+    part = getattr(_tls, "partition", None)
+    if part is None:
+        rc = l.t2s2_context_create(dev, ctypes.byref(h))
+    else:
+        rc = l.t2s2_context_create_on_partition(dev, int(part), ctypes.byref(h))
     if rc != T2S2_OK:
-        raise NativeUnavailable(f"t2s2_context_create(device={dev}) failed with code {rc}"
-                                " (no CUDA device?)")
+        raise NativeUnavailable(f"t2s2_context_create(device={dev}, partition={part}) failed "
+                                f"with code {rc} (no CUDA device?)")
     budget = getattr(_tls, "sm_budget", 0)
     if budget:
         l.t2s2_context_set_sm_budget(h, int(budget))
     _tls.ctx = h
     return h
+
+
+def device_index():
+    return int(os.environ.get("T2S2_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def sm_partitions(count):
+    """Split this process's device into `count` disjoint SM partitions
+    (green contexts; once per process).  Returns their SM counts."""
+    out = (ctypes.c_int * count)()
+    rc = lib().t2s2_sm_partitions(device_index(), int(count), out)
+    if rc != T2S2_OK:
+        raise NativeUnavailable(f"t2s2_sm_partitions({count}) failed with code {rc}")
+    return list(out)
+
+
+def use_partition(part):
+    """Bind this host thread's (future) engine context to SM partition
+    `part` of sm_partitions(); call before the thread's first engine call."""
+    if getattr(_tls, "ctx", None) is not None:
+        raise RuntimeError("this thread already has an engine context")
+    _tls.partition = int(part)
+
+
+def device_clock_ns():
+    """The device's global nanosecond timer, read on this thread's stream
+    after its queued work (blocking)."""
+    v = ctypes.c_ulonglong()
+    check(lib().t2s2_device_clock(context(), ctypes.byref(v)))
+    return int(v.value)
 
 
 def num_sms():

@@ -11,6 +11,7 @@
 #include "als.h"
 #include "blas.h"
 #include "linalg.h"
+#include "partition.h"
 #include "tt.h"
 
 namespace t2s2 {
@@ -28,6 +29,7 @@ struct Pending {
 
 struct t2s2_context {
   int device = 0;
+  void* cu_ctx = nullptr;  // green context of an SM partition (null: the primary context)
   int sms = 0;        // multiprocessor count of the device
   int sm_budget = 0;  // 0: all SMs
   std::unordered_map<const void*, int> smem_limit;  // kernel -> raised dynamic smem bytes
@@ -59,7 +61,10 @@ struct Bind {  // makes ctx current for the duration of an API call
   t2s2_context* prev;
   explicit Bind(t2s2_context* c) : prev(g_ctx) {
     g_ctx = c;
-    cudaSetDevice(c->device);
+    if (c->cu_ctx)
+      set_current_context(c->cu_ctx);
+    else
+      cudaSetDevice(c->device);
   }
   ~Bind() { g_ctx = prev; }
 };
@@ -67,6 +72,7 @@ struct Bind {  // makes ctx current for the duration of an API call
 
 Allocator& allocator() { return g_ctx->alloc; }
 int num_sms() { return g_ctx->sms; }
+bool on_partition() { return g_ctx->cu_ctx != nullptr; }
 
 void max_dynamic_smem(const void* kernel, int bytes) {
   auto it = g_ctx->smem_limit.find(kernel);
@@ -249,14 +255,21 @@ void fill_report(const SolveReport& r, t2s2_solve_report* out) {
 
 extern "C" {
 
-int t2s2_context_create(int device, t2s2_context** out) {
+namespace {
+int context_create(int device, int part, t2s2_context** out) {
   if (!out) return T2S2_ERR_ARG;
   auto ctx = std::make_unique<t2s2_context>();
   ctx->device = device;
   if (cudaSetDevice(device) != cudaSuccess) return T2S2_ERR_CUDA;
-  if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-      ctx->sms < 1)
+  if (part >= 0) {
+    // a green context: this context's kernels run on the partition's SMs only
+    if (!t2s2::partition_context(device, part, &ctx->cu_ctx, &ctx->sms)) return T2S2_ERR_VALUE;
+    if (!t2s2::set_current_context(ctx->cu_ctx)) return T2S2_ERR_CUDA;
+  } else if (cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device) !=
+                 cudaSuccess ||
+             ctx->sms < 1) {
     return T2S2_ERR_CUDA;
+  }
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
     return T2S2_ERR_CUDA;
   ctx->alloc.stream = ctx->stream;
@@ -269,10 +282,51 @@ int t2s2_context_create(int device, t2s2_context** out) {
   *out = ctx.release();
   return T2S2_OK;
 }
+}  // namespace
+
+int t2s2_context_create(int device, t2s2_context** out) { return context_create(device, -1, out); }
+
+int t2s2_sm_partitions(int device, int count, int* sms_out) {
+  try {
+    std::vector<int> sms;
+    t2s2::make_sm_partitions(device, count, sms);
+    for (int i = 0; i < count && sms_out; ++i) sms_out[i] = sms[i];
+    return T2S2_OK;
+  } catch (const t2s2::Error& e) {
+    return e.code;
+  }
+}
+
+int t2s2_context_create_on_partition(int device, int part, t2s2_context** out) {
+  return context_create(device, part, out);
+}
+
+namespace t2s2 {
+__global__ void device_clock_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  *out = t;
+}
+}  // namespace t2s2
+
+int t2s2_device_clock(t2s2_context* ctx, unsigned long long* out_ns) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(out_ns, kErrArg, "null output");
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(allocator().alloc(1));
+    t2s2::device_clock_kernel<<<1, 1, 0, stream()>>>(d);
+    T2S2_CHECK_LAUNCH();
+    T2S2_CUDA(cudaMemcpyAsync(out_ns, d, sizeof *out_ns, cudaMemcpyDeviceToHost, stream()));
+    T2S2_CUDA(cudaStreamSynchronize(stream()));
+    allocator().release(reinterpret_cast<double*>(d));
+  });
+}
 
 void t2s2_context_destroy(t2s2_context* ctx) {
   if (!ctx) return;
-  cudaSetDevice(ctx->device);
+  if (ctx->cu_ctx)
+    t2s2::set_current_context(ctx->cu_ctx);
+  else
+    cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   ctx->alloc.trim();
   cudaStreamSynchronize(ctx->stream);

@@ -39,10 +39,16 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 constexpr int kStages = 4;
-// dynamic shared memory of the GEMM program: the larger of the two tile rings
-constexpr int kGemmSmem = kStages * 8 * (32 * (32 + 4) * 2 > 16 * (64 + 4) * 2
-                                             ? 32 * (32 + 4) * 2
-                                             : 16 * (64 + 4) * 2);
+// dynamic shared memory of a tile ring: ST stages of a TK x (TM+4) A tile and
+// a TK x (TN+4) B tile
+constexpr int ring_bytes(int TM, int TN, int TK, int ST) { return ST * 8 * TK * (TM + 4 + TN + 4); }
+// the 32x32x32 and 64x64x16 rings (every program), and the 128x64x16 ring
+// (3 stages) of programs with a problem large enough for it
+constexpr int kGemmSmem = ring_bytes(32, 32, 32, kStages) > ring_bytes(64, 64, 16, kStages)
+                              ? ring_bytes(32, 32, 32, kStages)
+                              : ring_bytes(64, 64, 16, kStages);
+constexpr int kGemmSmemHuge = ring_bytes(128, 64, 16, 3) > kGemmSmem ? ring_bytes(128, 64, 16, 3)
+                                                                     : kGemmSmem;
 
 __device__ __forceinline__ void cp_async8(unsigned dst, const double* src, bool pred) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
@@ -65,7 +71,7 @@ __device__ __forceinline__ long long row_off(int i, int d, long long hi, long lo
 // general GEMM: A(i,k) = A[row(i) + k*ak], B(k,j) = B[k*bk + j*bj],
 // C(i,j) = C[crow(i) + j*cj] (row() two-level, see GemmProb).  Operand
 // tiles are fetched with consecutive threads on the contiguous index.
-template <int TM, int TN, int TK>
+template <int TM, int TN, int TK, int ST = kStages>
 __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz, double* smem) {
   constexpr int PA = TM * TK / 256, PB = TK * TN / 256;
   constexpr int LA = TM + 4, LB = TN + 4;  // +4: conflict-free DMMA fragment loads
@@ -109,10 +115,10 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
     bdst[t] = sbase + 8u * (unsigned)(SA + bkk[t] * LB + bj);
   }
   const int nk = (K + TK - 1) / TK;
-  auto issue = [&](int kt) {  // K-tile kt into ring slot kt % kStages (always commits a group)
+  auto issue = [&](int kt) {  // K-tile kt into ring slot kt % ST (always commits a group)
     if (kt < nk) {
       const int k0 = kt * TK;
-      const unsigned so = 8u * (unsigned)((kt % kStages) * SS);
+      const unsigned so = 8u * (unsigned)((kt % ST) * SS);
 #pragma unroll
       for (int t = 0; t < PA; ++t) {
         const bool ok = arow[t] && k0 + akk[t] < K;
@@ -132,12 +138,12 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
   const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * WN;
   double tc[MB][NB][2] = {};
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) issue(s);
+  for (int s = 0; s < ST - 1; ++s) issue(s);
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kStages - 2>();  // this thread's copies of K-tile kt landed
-    __syncthreads();               // everyone's did, and slot (kt - 1) % kStages is free
-    issue(kt + kStages - 1);
-    const double* As = smem + (kt % kStages) * SS;
+    cp_async_wait<ST - 2>();  // this thread's copies of K-tile kt landed
+    __syncthreads();          // everyone's did, and slot (kt - 1) % ST is free
+    issue(kt + ST - 1);
+    const double* As = smem + (kt % ST) * SS;
     const double* Bs = As + SA;
 #pragma unroll
     for (int kk = 0; kk < TK; kk += 4) {
@@ -187,6 +193,9 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
 // per GEMM.
 constexpr int kReduceTile = 4096;
 
+// HUGE: the instantiation that also has the 128x64 tile (more registers:
+// one CTA per SM), used only for programs containing such a problem.
+template <bool HUGE>
 __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
   extern __shared__ __align__(16) double gemm_smem[];
   cg::grid_group grid = cg::this_grid();
@@ -220,6 +229,10 @@ __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant
           }
         }
         __syncthreads();
+      } else if (HUGE && g.big == 2) {
+        const int tn = (g.N + 63) / 64, tm = (g.M + 127) / 128;
+        const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
+        gemm_tile<128, 64, 16, 3>(g, rem % tn, rem / tn, bz, gemm_smem);
       } else if (g.big) {
         const int tn = (g.N + 63) / 64, tm = (g.M + 63) / 64;
         const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
@@ -440,11 +453,14 @@ void GemmBatch::add_general(int stage, int M, int N, int K, const GemmOperand& a
   g.batch = batch;
   g.alpha = alpha;
   g.beta = beta;
-  // 64x64 tiles once a problem fills the GPU with them (more reuse per L2 byte)
+  // 64x64 tiles once a problem fills the GPU with them (more reuse per L2
+  // byte), 128x64 once it fills the GPU with those
   g.big = M >= 64 && N >= 64 && K >= 64 &&
           (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch >= 148;
-  g.tiles = g.big ? ceil_div(M, 64) * ceil_div(N, 64) * batch
-                  : ceil_div(M, 32) * ceil_div(N, 32) * batch;
+  if (g.big && M >= 128 && (long long)ceil_div(M, 128) * ceil_div(N, 64) * batch >= 148) g.big = 2;
+  g.tiles = g.big == 2 ? ceil_div(M, 128) * ceil_div(N, 64) * batch
+            : g.big    ? ceil_div(M, 64) * ceil_div(N, 64) * batch
+                       : ceil_div(M, 32) * ceil_div(N, 32) * batch;
   flops_ += 2.0 * M * N * (double)K * batch;
   // split-K for long contractions with too few output tiles to fill the GPU:
   // partial products at stage 2s, their deterministic sum at stage 2s+1
@@ -527,19 +543,27 @@ void GemmBatch::run() {
     // a stage cut by the problem limit continues in the next program
     prog.stage_first[prog.nstage] = prog.nprob;
     const int nsm = num_sms();
-    max_dynamic_smem((const void*)gemm_program_kernel, kGemmSmem);
-    const int occ = occupancy((const void*)gemm_program_kernel, 256, kGemmSmem);
+    bool huge = false;
+    for (int q = 0; q < prog.nprob; ++q) huge = huge || (prog.p[q].kind == 0 && prog.p[q].big == 2);
+    const int smem = huge ? kGemmSmemHuge : kGemmSmem;
+    const void* kern = huge ? (const void*)gemm_program_kernel<true>
+                            : (const void*)gemm_program_kernel<false>;
+    max_dynamic_smem(kern, smem);
+    const int occ = occupancy(kern, 256, smem);
     int grid = max_tiles < nsm * occ ? max_tiles : nsm * occ;
     if (sm_budget() > 0 && grid > sm_budget()) grid = sm_budget();
     if (grid < 1) grid = 1;
     {
       LaunchScope ls("gemm", flops_ * prog.nprob / (double)items_.size(), 0.0);
       if (prog.nstage == 1) {
-        gemm_program_kernel<<<grid, 256, kGemmSmem, stream()>>>(prog);
+        if (huge)
+          gemm_program_kernel<true><<<grid, 256, smem, stream()>>>(prog);
+        else
+          gemm_program_kernel<false><<<grid, 256, smem, stream()>>>(prog);
       } else {
         void* params[] = {&prog};
-        T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gemm_program_kernel, dim3(grid), dim3(256),
-                                              params, kGemmSmem, stream()));
+        T2S2_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(256), params, smem,
+                                              stream()));
       }
     }
     T2S2_CHECK_LAUNCH();

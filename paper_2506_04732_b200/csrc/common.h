@@ -113,7 +113,8 @@ struct LaunchScope {
 Allocator& allocator();  // the current context's allocator
 // Per-device launch properties, cached in the current context (one context
 // per host thread and device, so no shared mutable state between threads):
-int num_sms();                                          // multiprocessors of the device
+int num_sms();                                          // multiprocessors of the device / partition
+bool on_partition();                                    // the context runs on an SM partition
 void max_dynamic_smem(const void* kernel, int bytes);   // raise the kernel's dynamic smem limit
 int occupancy(const void* kernel, int threads, int smem);  // resident CTAs per SM (>= 1)
 int sm_budget();         // CTAs a whole-GPU cooperative kernel may use (context setting)

@@ -406,6 +406,12 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   // multi-CTA Arnoldi once each CTA gets >= 512 entries
   int G = n / 512;
   if (G > kCgMaxCtas) G = kCgMaxCtas;
+  // cooperative grid: no more CTAs than co-reside on this context's SMs (an
+  // SM partition has fewer than the device's 148)
+  {
+    const int cap = num_sms() * occupancy((const void*)gm_arnoldi_mc_kernel, kThreads, 0);
+    if (G > cap) G = cap;
+  }
   if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
   if (G < 1) G = 1;
   double* part = allocator().alloc((size_t)(kMaxRestart + 3) * kCgMaxCtas);
@@ -495,6 +501,15 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   T2S2_CUDA(cudaMemcpyAsync(st, &init, sizeof(CgState), cudaMemcpyHostToDevice, stream()));
   int G = (n + 2047) / 2048;
   if (G > kCgMaxCtas) G = kCgMaxCtas;
+  // cooperative grid: no more CTAs than co-reside on this context's SMs (an
+  // SM partition has fewer than the device's 148); the same G — and so the
+  // same reduction order — as on the whole GPU whenever it fits
+  {
+    int occ = occupancy((const void*)cg_step_kernel, kThreads, 0);
+    const int o2 = occupancy((const void*)cg_pre_kernel, kThreads, 0);
+    if (o2 < occ) occ = o2;
+    if (G > num_sms() * occ) G = num_sms() * occ;
+  }
   if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
   if (G < 1) G = 1;
   int it = 0;
@@ -516,7 +531,9 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   // T2S2_NO_GRAPH=1 runs the same iterations eagerly (tests check the
   // replay is bit-identical to it)
   static std::atomic<bool> graphs_ok{getenv("T2S2_NO_GRAPH") == nullptr};
-  if (graphs_ok && !profiling() && maxiter >= 2 * poll) {
+  // not on an SM partition: a replayed graph of cooperative kernels hangs in
+  // a green context (measured), the same iterations run eagerly there
+  if (graphs_ok && !profiling() && !on_partition() && maxiter >= 2 * poll) {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     const StatsMark before = stats_mark();

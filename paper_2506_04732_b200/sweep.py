@@ -6,11 +6,15 @@ collective: rank k of N takes solves k, k+N, k+2N, ... (round-robin keeps the
 seeded eps draws — and with them the cost — spread evenly), runs them on its
 own device, and the per-solve results are gathered once at the end
 (``gather``; torch.distributed, any backend).  One process per GPU,
-``LOCAL_RANK`` selects the device (see _native.context).  Solves run one
-after another on a rank's GPU: several engine contexts on one GPU would put
-spin-waiting cooperative kernels (Gauss-Jordan hand-offs, Krylov grid
-barriers) of different solves side by side, and a kernel whose CTAs are only
-partly resident next to another such kernel can wait forever.
+``LOCAL_RANK`` selects the device (see _native.context).
+
+Within a GPU, ``partitions=P`` runs P solves at a time, one host thread each,
+on P disjoint SM partitions (green contexts, csrc/partition.cu): a single
+solve leaves most SMs idle through its latency-bound stretches, and the
+partitions keep the solves' spin-waiting cooperative kernels (Gauss-Jordan
+hand-offs, Krylov grid barriers) on separate SMs — two such kernels sharing
+SMs can each be partly resident and wait on each other forever, so plain
+concurrent streams are not used.
 """
 
 from __future__ import annotations
@@ -34,7 +38,8 @@ def _default_solve(a, b, cfg_kwargs):
     return x, rep
 
 
-def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None):
+def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=None,
+              partitions=1):
     """Solve this rank's share of ``recipes`` (workloads.SteadyRecipe).
 
     Returns {index: dict(x=cores, residuals, ranks, converged, stagnated,
@@ -61,8 +66,40 @@ def run_sweep(recipes, rank=0, world=1, solve_fn=None, build_fn=None, overrides=
                       ranks=list(rep.rank_history), converged=bool(rep.converged),
                       stagnated=bool(rep.stagnated), wall_s=wall, eps=r.eps)
 
-    for i in mine:
-        one(i)
+    if partitions <= 1:
+        for i in mine:
+            one(i)
+        return out
+    import threading
+
+    from . import _native
+
+    _native.sm_partitions(partitions)
+    queue = list(mine)
+    lock = threading.Lock()
+    errors = []
+
+    def worker(t):
+        _native.use_partition(t)
+        while True:
+            with lock:
+                if not queue or errors:
+                    return
+                i = queue.pop(0)
+            try:
+                one(i)
+            except Exception as exc:  # surface the first failure
+                with lock:
+                    errors.append(exc)
+                return
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(partitions)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
     return out
 
 

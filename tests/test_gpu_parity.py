@@ -253,7 +253,9 @@ def test_dense_local_solve_late_interchange(pk):
     (0, 0, 37, 29, 13), (1, 0, 64, 65, 70), (0, 1, 130, 64, 132), (1, 1, 33, 40, 9),
     (0, 0, 2112, 64, 1024),  # split-K with a reduce stage
     (0, 1, 200, 48, 600),    # split-K, transposed B
-    (0, 0, 1024, 2112, 64),  # 64x64 tiles
+    (0, 0, 1024, 2112, 64),  # 128x64 tiles (fills the GPU with them)
+    (1, 0, 1000, 1030, 70),  # 128x64 tiles, ragged edges, transposed A
+    (0, 0, 512, 1100, 64),   # 64x64 tiles
 ])
 def test_gemm_program_against_torch(pk, ta, tb, m, n, k):
     """The GEMM-program kernel behind every contraction (DMMA tiles, operand
@@ -349,6 +351,28 @@ def test_singular_local_systems_use_lstsq(golden, pk):
     assert rep.stagnated and not rep.converged
     np.testing.assert_allclose(rep.residual_history[-1], ref[-1], rtol=1e-9)
     assert rel_diff(x.cores, get_train(z, "s8_x")) <= 1e-9
+
+
+def test_config4_sweep_on_sm_partitions(golden, pk):
+    """The scaled sweep on two disjoint SM partitions (green contexts), one
+    host thread and engine context each: every solve converges to the
+    reference's solution, and the engine is deterministic, so a solve's
+    result does not depend on the partition (or its SM count) it ran on."""
+    from paper_2506_04732_b200 import sweep, workloads as wl
+
+    z = golden("config4_small.npz")
+    recipes = wl.sweep_recipes(count=int(z["count"]), dims=3, degree=12)
+    ov = {"max_sweeps": int(z["sweeps"])}
+    res = sweep.run_sweep(recipes, overrides=ov, partitions=2)
+    serial = sweep.run_sweep(recipes[:1], overrides=ov)
+    for i in range(int(z["count"])):
+        got, ref = res[i], np.array(z[f"res{i}"])
+        want = get_train(z, f"x{i}")
+        assert got["converged"] == bool(z[f"conv{i}"])
+        assert rel_diff(got["x"], want) <= value_tol(got["residuals"][-1], ref[-1])
+    assert res[0]["residuals"] == serial[0]["residuals"]
+    for c1, c2 in zip(res[0]["x"], serial[0]["x"]):
+        np.testing.assert_array_equal(c1, c2)
 
 
 def test_config3_full_size_steps_match_oracle(pk):
