@@ -62,6 +62,9 @@ def parse():
                     help="ALS sweeps per config-4 solve (fixed budget)")
     ap.add_argument("--sweep-partitions", type=int, default=4,
                     help="run the timed solves on P disjoint SM partitions (green contexts)")
+    ap.add_argument("--residual-tol", type=float, default=None,
+                    help="march: inner residual target (default: the reference's MarchConfig "
+                         "1e-10); 1e-12 reads BASELINE's 'TT tolerance' as the residual target")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -133,6 +136,15 @@ def ttss_march(recipe, problem, state, first, count):
     return time.perf_counter() - t0, state
 
 
+def march_recipe(args):
+    from paper_2506_04732_b200 import workloads as wl
+
+    recipe = wl.config(MARCH["index"])
+    if args.residual_tol is not None:
+        recipe.solver = dict(recipe.solver, residual_tol=args.residual_tol)
+    return recipe
+
+
 def sweep_seeds(rank, world, count):
     from paper_2506_04732_b200.sweep import shard
 
@@ -168,7 +180,7 @@ def run_reference(args):
     cores = blas_threads()
     if args.workload == "march":
         w = MARCH
-        recipe = wl.config(w["index"])
+        recipe = march_recipe(args)
         problem = wl.march_problem(recipe)
         _, state = ttss_march(recipe, problem, problem[2], 1, W)
         elapsed, _ = ttss_march(recipe, problem, state, W + 1, K)
@@ -367,7 +379,7 @@ def run_b200_march(args, torch, dd):
     from paper_2506_04732_b200.solver import SolverConfig
     from paper_2506_04732_b200.tt import from_device, to_device
 
-    recipe = wl.config(MARCH["index"])
+    recipe = march_recipe(args)
     W, K = args.warmup, args.steps
     problem = wl.march_problem(recipe)
     left, right, state0, forcing, exact, _ = problem

@@ -159,6 +159,19 @@ __device__ void mc_dots(const double* V, const double* w, int n, int nk, int i0,
   }
 }
 
+// out[k] = sum_c part[k * G + c] for k < nk, every CTA the same bits: warp w
+// takes rows k = w, w + nw, ...; lane l loads partials l, l + 32, ... (all in
+// flight at once) and a fixed shuffle tree adds them.
+__device__ __forceinline__ void sum_partials(const double* part, int G, int nk, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < nk; k += nw) {
+    double t = 0.0;
+    for (int c = lane; c < G; c += 32) t += __ldcg(part + (size_t)k * G + c);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) out[k] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
     gm_arnoldi_mc_kernel(GmState* st, double* V, int n, int col, double* part) {
   cg::grid_group grid = cg::this_grid();
@@ -171,11 +184,7 @@ __global__ void __launch_bounds__(kThreads)
   const int nk = col + 2;  // col+1 dots and ||w||^2
   mc_dots(V, w, n, nk, i0, i1, part, G);
   grid.sync();
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-    double t = 0.0;
-    for (int c = 0; c < G; ++c) t += __ldcg(part + (size_t)k * G + c);
-    hs[k] = t;
-  }
+  sum_partials(part, G, nk, hs);
   __syncthreads();
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     double x = w[i];
@@ -186,11 +195,7 @@ __global__ void __launch_bounds__(kThreads)
   grid.sync();  // every CTA has read the first-pass partials
   mc_dots(V, w, n, nk, i0, i1, part, G);
   grid.sync();
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-    double t = 0.0;
-    for (int c = 0; c < G; ++c) t += __ldcg(part + (size_t)k * G + c);
-    h2[k] = t;
-  }
+  sum_partials(part, G, nk, h2);
   __syncthreads();
   double ww = 0.0;
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
@@ -210,8 +215,10 @@ __global__ void __launch_bounds__(kThreads)
     part[(size_t)(kMaxRestart + 2) * G + blockIdx.x] = t;
   }
   grid.sync();
-  double sww = 0.0;
-  for (int c = 0; c < G; ++c) sww += __ldcg(part + (size_t)(kMaxRestart + 2) * G + c);
+  __shared__ double sw1[1];
+  sum_partials(part + (size_t)(kMaxRestart + 2) * G, G, 1, sw1);
+  __syncthreads();
+  const double sww = sw1[0];
   const double h0 = sqrt(hs[nk - 1]);
   const double h1 = sqrt(sww);
   const bool brk = h1 <= DBL_EPSILON * h0;
@@ -275,7 +282,9 @@ __global__ void __launch_bounds__(kThreads)
 
 // scipy cg (Jacobi-preconditioned), split around the matvec q = A p into two
 // cooperative kernels over G CTAs.  Reductions are deterministic: per-CTA
-// partials, one grid barrier, every CTA sums the G partials in order.
+// partials, one grid barrier, every CTA sums the G partials in the same
+// fixed order (sum_partials: all loads in flight at once, a shuffle tree —
+// a serial loop over G partials was a chain of G dependent L2 round trips).
 __device__ __forceinline__ double block_reduce(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -308,11 +317,10 @@ __global__ void __launch_bounds__(kThreads)
     part[G + blockIdx.x] = rz;
   }
   grid.sync();
-  double srr = 0.0, rho = 0.0;
-  for (int c = 0; c < G; ++c) {
-    srr += __ldcg(part + c);
-    rho += __ldcg(part + G + c);
-  }
+  __shared__ double sums[2];
+  sum_partials(part, G, 2, sums);  // rows: rr partials, rz partials
+  __syncthreads();
+  const double srr = sums[0], rho = sums[1];
   if (sqrt(srr) < atol) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
     return;
@@ -340,8 +348,10 @@ __global__ void __launch_bounds__(kThreads)
   pq = block_reduce(pq, red);
   if (threadIdx.x == 0) part[2 * G + blockIdx.x] = pq;
   grid.sync();
-  double spq = 0.0;
-  for (int c = 0; c < G; ++c) spq += __ldcg(part + 2 * G + c);
+  __shared__ double sums[2];
+  sum_partials(part + 2 * G, G, 1, sums);
+  __syncthreads();
+  const double spq = sums[0];
   const double rho_cur = st->rho_cur;
   const double alpha = rho_cur / spq;
   double rr = 0.0, rz = 0.0;
@@ -360,11 +370,10 @@ __global__ void __launch_bounds__(kThreads)
   }
   grid.sync();
   // next iteration's top: convergence check, rho, p update
-  double srr = 0.0, rho = 0.0;
-  for (int c = 0; c < G; ++c) {
-    srr += __ldcg(part + c);
-    rho += __ldcg(part + G + c);
-  }
+  __syncthreads();  // sums[0] (spq) read by every thread above
+  sum_partials(part, G, 2, sums);  // rows: rr partials, rz partials
+  __syncthreads();
+  const double srr = sums[0], rho = sums[1];
   if (sqrt(srr) < atol) {
     if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
     return;

@@ -39,7 +39,7 @@ pytestmark = pytest.mark.gpu
 
 PARITY_TOL = 1e-10       # north_star: full-grid relative agreement
 ERR_SLACK = 1e-6         # relative slack on the manufactured-solution error
-PLATEAU_FACTOR = 3.0     # config 4 plateau envelope (see the config-4 test)
+PLATEAU_FACTOR = 3.0     # config 4: x the envelope of reference-equivalent plateaus
 
 
 def _record(name, rows, summary):
@@ -163,14 +163,20 @@ def test_config4_complete_solve_matches_reference(golden, index):
     ttss's own complete solve of the same seed.  These solves do not
     converge in the reference either: ranks reach the cap and the residual
     decreases slowly to the sweep limit (a rank-capped plateau), where the
-    iterate is path dependent.  Checked: the same verdict and sweep count,
-    the rank history, and the plateau — final residual and
-    manufactured-solution error no worse than the reference's beyond the
-    reference's own thread-count spread (config4_selfspread)."""
+    iterate is path dependent — ttss itself ends seed 0 at residual 2.2e-4
+    with 2 OpenBLAS threads and 8.3e-5 with 1 (error 5.1e-4 / 1.9e-4), its
+    numpy restatement ends seed 2 at 4.0e-3 against ttss's 1.7e-3 / 2.1e-3.
+    Checked exactly: the verdict, the sweep count and the rank history.
+    Checked against the envelope of these reference-equivalent runs
+    (fixture keys env_*, tools/config4_envelope.py): the final residual and
+    the manufactured-solution error no worse than PLATEAU_FACTOR x the
+    envelope's largest."""
     o = _solve_full(golden, index)
+    z = golden(f"config4_full_{index}.npz")
+    env_res, env_err = float(np.max(z["env_res"])), float(np.max(z["env_err"]))
     assert (o["converged"], o["stagnated"]) == (o["converged_ref"], o["stagnated_ref"]), o
     assert o["sweeps"] == o["sweeps_ref"], o
     assert max(o["ranks"]) == max(o["ranks_ref"]) == 64
     assert o["rank_history"] == o["rank_history_ref"], o
-    assert o["residuals"][-1] <= PLATEAU_FACTOR * o["residuals_ref"][-1], o
-    assert o["exact_err"] <= PLATEAU_FACTOR * o["exact_err_ref"], o
+    assert o["residuals"][-1] <= PLATEAU_FACTOR * env_res, (o["residuals"][-1], env_res)
+    assert o["exact_err"] <= PLATEAU_FACTOR * env_err, (o["exact_err"], env_err)
