@@ -27,7 +27,8 @@ __all__ = [
     "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libt2s2.so")
+LIB_PATH = os.environ.get("T2S2_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "lib", "libt2s2.so")
 MAX_SWEEPS = 1024
 
 T2S2_OK = 0

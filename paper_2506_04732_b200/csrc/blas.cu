@@ -42,13 +42,15 @@ constexpr int kStages = 4;
 // dynamic shared memory of a tile ring: ST stages of a TK x (TM+4) A tile and
 // a TK x (TN+4) B tile
 constexpr int ring_bytes(int TM, int TN, int TK, int ST) { return ST * 8 * TK * (TM + 4 + TN + 4); }
-// the 32x32x32 and 64x64x16 rings (every program), and the 128x64x16 ring
-// (3 stages) of programs with a problem large enough for it
+// the 32x32x32 and 64x64x16 rings (every program), and the 64x136x16 ring
+// of programs with a problem whose N is 65..136 (see add_general)
 constexpr int kGemmSmem = ring_bytes(32, 32, 32, kStages) > ring_bytes(64, 64, 16, kStages)
                               ? ring_bytes(32, 32, 32, kStages)
                               : ring_bytes(64, 64, 16, kStages);
-constexpr int kGemmSmemHuge = ring_bytes(128, 64, 16, 3) > kGemmSmem ? ring_bytes(128, 64, 16, 3)
-                                                                     : kGemmSmem;
+constexpr int kWideN = 136;  // 17 DMMA columns
+constexpr int kGemmSmemWide = ring_bytes(64, kWideN, 16, kStages) > kGemmSmem
+                                  ? ring_bytes(64, kWideN, 16, kStages)
+                                  : kGemmSmem;
 
 __device__ __forceinline__ void cp_async8(unsigned dst, const double* src, bool pred) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
@@ -71,9 +73,11 @@ __device__ __forceinline__ long long row_off(int i, int d, long long hi, long lo
 // general GEMM: A(i,k) = A[row(i) + k*ak], B(k,j) = B[k*bk + j*bj],
 // C(i,j) = C[crow(i) + j*cj] (row() two-level, see GemmProb).  Operand
 // tiles are fetched with consecutive threads on the contiguous index.
-template <int TM, int TN, int TK, int ST = kStages>
+// WGM x WGN warps tile the output (4 x 2 by default; 8 x 1 for the wide
+// tile, one warp per 8 rows across all 136 columns).
+template <int TM, int TN, int TK, int ST = kStages, int WGM = 4, int WGN = 2>
 __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int bz, double* smem) {
-  constexpr int PA = TM * TK / 256, PB = TK * TN / 256;
+  constexpr int PA = (TM * TK + 255) / 256, PB = (TK * TN + 255) / 256;
   constexpr int LA = TM + 4, LB = TN + 4;  // +4: conflict-free DMMA fragment loads
   constexpr int SA = TK * LA, SS = TK * (LA + LB);  // per stage: A tile then B tile
   const double* A = g.A + bz * g.sA;
@@ -89,10 +93,11 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
   long long aoff[PA];
   int akk[PA];
   unsigned adst[PA];
-  bool arow[PA];
+  bool arow[PA], aval[PA];
 #pragma unroll
   for (int t = 0; t < PA; ++t) {
     const int e = tid + t * 256;
+    aval[t] = e < TM * TK;  // tiles that are not a multiple of 256 elements
     const int ai = a_ifast ? e % TM : e / TK;
     akk[t] = a_ifast ? e / TM : e % TK;
     const int gi = row0 + ai;
@@ -104,9 +109,11 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
   bool bcol[PB];
   long long boff[PB];
   unsigned bdst[PB];
+  bool bval[PB];
 #pragma unroll
   for (int t = 0; t < PB; ++t) {
     const int e = tid + t * 256;
+    bval[t] = e < TK * TN;
     const int bj = b_jfast ? e % TN : e / TK;
     bkk[t] = b_jfast ? e / TN : e % TK;
     const int gj = col0 + bj;
@@ -121,11 +128,13 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
       const unsigned so = 8u * (unsigned)((kt % ST) * SS);
 #pragma unroll
       for (int t = 0; t < PA; ++t) {
+        if (!aval[t]) continue;
         const bool ok = arow[t] && k0 + akk[t] < K;
         cp_async8(adst[t] + so, ok ? A + aoff[t] + (long long)k0 * g.ak : A, ok);
       }
 #pragma unroll
       for (int t = 0; t < PB; ++t) {
+        if (!bval[t]) continue;
         const bool ok = bcol[t] && k0 + bkk[t] < K;
         cp_async8(bdst[t] + so, ok ? B + boff[t] + (long long)k0 * g.bk : B, ok);
       }
@@ -133,9 +142,9 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
     cp_async_commit();
   };
   // 8 warps on a 4 x 2 grid of (TM/4) x (TN/2) warp tiles of 8x8 DMMA blocks
-  constexpr int WM = TM / 4, WN = TN / 2, MB = WM / 8, NB = WN / 8;
+  constexpr int WM = TM / WGM, WN = TN / WGN, MB = WM / 8, NB = WN / 8;
   const int lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp >> 1) * WM, wn0 = (warp & 1) * WN;
+  const int wm0 = (warp / WGN) * WM, wn0 = (warp % WGN) * WN;
   double tc[MB][NB][2] = {};
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) issue(s);
@@ -193,10 +202,12 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
 // per GEMM.
 constexpr int kReduceTile = 4096;
 
-// HUGE: the instantiation that also has the 128x64 tile (more registers:
-// one CTA per SM), used only for programs containing such a problem.
-template <bool HUGE>
-__global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
+// WIDE: the instantiation that also has the 64x136 tile (a larger
+// shared-memory ring), used only for programs containing such a problem.
+// Two CTAs per SM for both (<= 128 registers): the other stages of a
+// program with a wide problem run in the same instantiation.
+template <bool WIDE>
+__global__ void __launch_bounds__(256, 2) gemm_program_kernel(const __grid_constant__ GemmProgram prog) {
   extern __shared__ __align__(16) double gemm_smem[];
   cg::grid_group grid = cg::this_grid();
   if (prog.guard && *prog.guard == 0) return;  // uniform over the grid: flag set by an earlier kernel
@@ -229,10 +240,9 @@ __global__ void __launch_bounds__(256) gemm_program_kernel(const __grid_constant
           }
         }
         __syncthreads();
-      } else if (HUGE && g.big == 2) {
-        const int tn = (g.N + 63) / 64, tm = (g.M + 127) / 128;
-        const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
-        gemm_tile<128, 64, 16, 3>(g, rem % tn, rem / tn, bz, gemm_smem);
+      } else if (WIDE && g.big == 2) {
+        const int tm = (g.M + 63) / 64;
+        gemm_tile<64, kWideN, 16, kStages, 8, 1>(g, 0, tt % tm, tt / tm, gemm_smem);
       } else if (g.big) {
         const int tn = (g.N + 63) / 64, tm = (g.M + 63) / 64;
         const int bz = tt / (tm * tn), rem = tt - bz * tm * tn;
@@ -454,11 +464,13 @@ void GemmBatch::add_general(int stage, int M, int N, int K, const GemmOperand& a
   g.alpha = alpha;
   g.beta = beta;
   // 64x64 tiles once a problem fills the GPU with them (more reuse per L2
-  // byte), 128x64 once it fills the GPU with those
+  // byte); for 64 < N <= 136 — the operator-core stages of a config-4
+  // matvec, N = n * rA = 132 — one 64 x 136 tile covers all columns (64-wide
+  // tiles would compute 192 columns for 132)
   g.big = M >= 64 && N >= 64 && K >= 64 &&
           (long long)ceil_div(M, 64) * ceil_div(N, 64) * batch >= 148;
-  if (g.big && M >= 128 && (long long)ceil_div(M, 128) * ceil_div(N, 64) * batch >= 148) g.big = 2;
-  g.tiles = g.big == 2 ? ceil_div(M, 128) * ceil_div(N, 64) * batch
+  if (g.big && N > 64 && N <= kWideN) g.big = 2;
+  g.tiles = g.big == 2 ? ceil_div(M, 64) * batch
             : g.big    ? ceil_div(M, 64) * ceil_div(N, 64) * batch
                        : ceil_div(M, 32) * ceil_div(N, 32) * batch;
   flops_ += 2.0 * M * N * (double)K * batch;
@@ -543,10 +555,10 @@ void GemmBatch::run() {
     // a stage cut by the problem limit continues in the next program
     prog.stage_first[prog.nstage] = prog.nprob;
     const int nsm = num_sms();
-    bool huge = false;
-    for (int q = 0; q < prog.nprob; ++q) huge = huge || (prog.p[q].kind == 0 && prog.p[q].big == 2);
-    const int smem = huge ? kGemmSmemHuge : kGemmSmem;
-    const void* kern = huge ? (const void*)gemm_program_kernel<true>
+    bool wide = false;
+    for (int q = 0; q < prog.nprob; ++q) wide = wide || (prog.p[q].kind == 0 && prog.p[q].big == 2);
+    const int smem = wide ? kGemmSmemWide : kGemmSmem;
+    const void* kern = wide ? (const void*)gemm_program_kernel<true>
                             : (const void*)gemm_program_kernel<false>;
     max_dynamic_smem(kern, smem);
     const int occ = occupancy(kern, 256, smem);
@@ -556,7 +568,7 @@ void GemmBatch::run() {
     {
       LaunchScope ls("gemm", flops_ * prog.nprob / (double)items_.size(), 0.0);
       if (prog.nstage == 1) {
-        if (huge)
+        if (wide)
           gemm_program_kernel<true><<<grid, 256, smem, stream()>>>(prog);
         else
           gemm_program_kernel<false><<<grid, 256, smem, stream()>>>(prog);

@@ -35,7 +35,7 @@ struct GemmProb {
   long long ahi, alo, ak, bk, bj, chi, clo, cj;
   int ad, cd;
   int M, N, K, batch, tiles;
-  int big;   // 2: 128x64x16 tiles, 1: 64x64x16, 0: 32x32x32
+  int big;   // 2: 64x136x16 tiles (65 <= N <= 136), 1: 64x64x16, 0: 32x32x32
   int kind;  // 0 GEMM; 1 split-K reduction: C = alpha sum_j A[j] + beta C (A: batch x M x N)
   double alpha, beta;
   const double* rs;  // optional epilogue scales (beta == 0 only): C(i,j) = alpha acc rs[i] cs[j]

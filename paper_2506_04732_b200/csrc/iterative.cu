@@ -159,15 +159,29 @@ __device__ void mc_dots(const double* V, const double* w, int n, int nk, int i0,
   }
 }
 
-// out[k] = sum_c part[k * G + c] for k < nk, every CTA the same bits: warp w
-// takes rows k = w, w + nw, ...; lane l loads partials l, l + 32, ... (all in
-// flight at once) and a fixed shuffle tree adds them.
+// out[k] = sum_c part[k * G + c] for k < nk, added in the order c = 0, 1,
+// ..., G - 1 (every CTA the same bits, and the bits of a plain serial loop),
+// but without a chain of G dependent L2 round trips: warp w takes rows
+// k = w, w + nw, ...; its lanes load the row's partials at once (lane l holds
+// c = l, l + 32, ...) and the sum walks them through shuffles in order.
+constexpr int kMaxPartialsPerLane = (kCgMaxCtas + 31) / 32;
 __device__ __forceinline__ void sum_partials(const double* part, int G, int nk, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = warp; k < nk; k += nw) {
+    double v[kMaxPartialsPerLane];
+#pragma unroll
+    for (int j = 0; j < kMaxPartialsPerLane; ++j) {
+      const int c = lane + 32 * j;
+      v[j] = c < G ? __ldcg(part + (size_t)k * G + c) : 0.0;
+    }
     double t = 0.0;
-    for (int c = lane; c < G; c += 32) t += __ldcg(part + (size_t)k * G + c);
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+#pragma unroll
+    for (int j = 0; j < kMaxPartialsPerLane; ++j)
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) {
+        const double x = __shfl_sync(0xffffffffu, v[j], l);
+        if (32 * j + l < G) t += x;
+      }
     if (lane == 0) out[k] = t;
   }
 }
@@ -282,9 +296,8 @@ __global__ void __launch_bounds__(kThreads)
 
 // scipy cg (Jacobi-preconditioned), split around the matvec q = A p into two
 // cooperative kernels over G CTAs.  Reductions are deterministic: per-CTA
-// partials, one grid barrier, every CTA sums the G partials in the same
-// fixed order (sum_partials: all loads in flight at once, a shuffle tree —
-// a serial loop over G partials was a chain of G dependent L2 round trips).
+// partials, one grid barrier, every CTA sums the G partials in CTA order
+// (sum_partials: the loads in flight at once, the adds in order).
 __device__ __forceinline__ double block_reduce(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

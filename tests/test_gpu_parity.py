@@ -253,9 +253,9 @@ def test_dense_local_solve_late_interchange(pk):
     (0, 0, 37, 29, 13), (1, 0, 64, 65, 70), (0, 1, 130, 64, 132), (1, 1, 33, 40, 9),
     (0, 0, 2112, 64, 1024),  # split-K with a reduce stage
     (0, 1, 200, 48, 600),    # split-K, transposed B
-    (0, 0, 1024, 2112, 64),  # 128x64 tiles (fills the GPU with them)
-    (1, 0, 1000, 1030, 70),  # 128x64 tiles, ragged edges, transposed A
-    (0, 0, 512, 1100, 64),   # 64x64 tiles
+    (0, 0, 1024, 2112, 64),  # 64x64 tiles
+    (0, 0, 16384, 132, 132),  # 64x136 tiles (the config-4 operator-core stage)
+    (1, 0, 9500, 71, 70),     # 64x136 tiles, ragged, transposed A
 ])
 def test_gemm_program_against_torch(pk, ta, tb, m, n, k):
     """The GEMM-program kernel behind every contraction (DMMA tiles, operand

@@ -11,6 +11,7 @@ from paper_2506_04732_b200 import _native  # noqa: E402
 
 shapes = [  # (name, M, N, K)
     ("stage1 x.a1.a2 x n.w x z", 1024, 2112, 64),
+    ("stage2/3 operator core (x.a.w) x m.A x a.n", 16384, 132, 132),
     ("stage4 x.m x y x A1.A2.w", 2112, 64, 1024),
     ("stage2-like 132 x 64 x 132 (one batch entry)", 132, 64, 132),
     ("square 2048", 2048, 2048, 2048),

@@ -32,3 +32,19 @@ tot = sum(v["device_ms"] for v in st.values()) or 1.0
 for name, v in sorted(st.items(), key=lambda kv: -kv[1]["device_ms"] if prof else -kv[1]["launches"]):
     print(f"    {name:16s} n={v['launches']:8d} ms={v['device_ms']:10.2f} ({100 * v['device_ms'] / tot:4.1f}%)"
           f" gflop={v['flops'] / 1e9:10.3f} tflops={v['flops'] / max(v['device_ms'], 1e-9) / 1e9:6.2f}")
+if prof and len(sys.argv) > 4:
+    # the GEMM programs grouped by algorithmic flops (one group ~ one program shape)
+    import collections
+
+    groups = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for fam, fl, by, ms in _native.launch_log():
+        if fam == "gemm":
+            g = groups[round(fl / 1e3)]
+            g[0] += 1
+            g[1] += ms
+            g[2] = fl
+    tot = sum(v[1] for v in groups.values())
+    print("  GEMM programs by flop count (top 12 by time):")
+    for key, (n, ms, fl) in sorted(groups.items(), key=lambda kv: -kv[1][1])[:12]:
+        print(f"    {fl / 1e6:10.2f} MFLOP x{n:6d}  {ms:9.1f} ms ({100 * ms / tot:4.1f}%)  "
+              f"{1e3 * ms / n:7.1f} us/launch  {fl / (ms / n) / 1e9:6.2f} TF")
