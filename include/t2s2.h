@@ -144,6 +144,15 @@ typedef struct {
 } t2s2_launch_record;
 int t2s2_launch_log(t2s2_context* ctx, t2s2_launch_record* out, int capacity, int* count);
 
+/* Instrumentation (no reference counterpart): the device->host reads that
+ * steer the host (ranks, candidate scores, residuals, solver flags).
+ * mode 1 records the values every such read returns, mode 2 hands the
+ * recorded values back to an IDENTICAL run without synchronising (the host
+ * then runs ahead of the device; a run that asks for a different read
+ * fails with T2S2_ERR_ARG), mode 0 switches both off.  *count = reads
+ * recorded.  Used to measure what the synchronising reads cost. */
+int t2s2_read_trace(t2s2_context* ctx, int mode, int* count);
+
 /* cols == NULL uploads a vector train (cores r0 x rows x r1), otherwise an
  * operator train (cores r0 x rows x cols x r1).  host_cores holds the
  * concatenated cores; device_cores (second form) is a device pointer. */

@@ -119,6 +119,7 @@ _SIGNATURES = {
     "t2s2_stats_reset": (_I, [_P, _I]),
     "t2s2_stats_read": (_I, [_P, ctypes.POINTER(KernelStatC), _I, _IP]),
     "t2s2_launch_log": (_I, [_P, ctypes.POINTER(LaunchRecordC), _I, _IP]),
+    "t2s2_read_trace": (_I, [_P, _I, _IP]),
     "t2s2_train_upload": (_I, [_P, _I, _IP, _IP, _IP, _DP, ctypes.POINTER(_P)]),
     "t2s2_train_upload_device": (_I, [_P, _I, _IP, _IP, _IP, _P, ctypes.POINTER(_P)]),
     "t2s2_train_shape": (_I, [_P, _IP, _IP, _IP, _IP, ctypes.POINTER(ctypes.c_size_t)]),
@@ -265,6 +266,14 @@ def check(rc, step=None):
 
 def stats_reset(profile_events=False):
     check(lib().t2s2_stats_reset(context(), 1 if profile_events else 0))
+
+
+def read_trace(mode):
+    """0 off, 1 record, 2 replay the recorded host reads (see t2s2.h); returns
+    the number of reads recorded."""
+    n = ctypes.c_int()
+    check(lib().t2s2_read_trace(context(), int(mode), ctypes.byref(n)))
+    return n.value
 
 
 def stats_read():

@@ -214,8 +214,7 @@ bool all_finite(const DTensor& t) {
   }
   T2S2_CHECK_LAUNCH();
   int h = 0;
-  T2S2_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  host_read(&h, flag, sizeof(int));
   allocator().release(reinterpret_cast<double*>(flag));
   return h == 0;
 }
@@ -601,8 +600,7 @@ struct Probe {
   // one read-back: h[3*slot + {0,1,2}], info at h_info, interchange flag
   void read(double* h, int* h_info, int* h_swapped = nullptr) {
     double tmp[16];
-    T2S2_CUDA(cudaMemcpyAsync(tmp, buf.p, sizeof tmp, cudaMemcpyDeviceToHost, stream()));
-    T2S2_CUDA(cudaStreamSynchronize(stream()));
+    host_read(tmp, buf.p, sizeof tmp);
     for (int i = 0; i < 12; ++i) h[i] = tmp[i];
     *h_info = reinterpret_cast<int*>(tmp + 12)[0];
     if (h_swapped) *h_swapped = reinterpret_cast<int*>(tmp + 12)[1];
@@ -1133,7 +1131,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       }
     }
   }
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  if (!replaying_reads()) T2S2_CUDA(cudaStreamSynchronize(stream()));
   rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   Train out;
   out.rows = rhs.rows;

@@ -46,6 +46,10 @@ struct t2s2_context {
   size_t pool_used = 0;
   std::vector<t2s2::Pending> pending;
   std::vector<t2s2_launch_record> launch_log;  // per launch while profiling
+  // host_read trace: 0 off, 1 record, 2 replay
+  int trace_mode = 0;
+  std::vector<std::vector<unsigned char>> trace;
+  size_t trace_pos = 0;
 };
 
 struct t2s2_train {
@@ -148,6 +152,24 @@ void resolve_pending(t2s2_context* c) {
 }  // namespace
 cudaStream_t stream() { return g_ctx->stream; }
 bool profiling() { return g_ctx->profiling; }
+
+bool replaying_reads() { return g_ctx->trace_mode == 2; }
+
+void host_read(void* host, const void* dev, size_t bytes) {
+  t2s2_context* c = g_ctx;
+  if (c->trace_mode == 2) {
+    T2S2_REQUIRE(c->trace_pos < c->trace.size() && c->trace[c->trace_pos].size() == bytes, kErrArg,
+                 "host_read replay: the run differs from the recorded one");
+    std::memcpy(host, c->trace[c->trace_pos++].data(), bytes);
+    return;
+  }
+  if (bytes) T2S2_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  T2S2_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->trace_mode == 1) {
+    const unsigned char* b = static_cast<const unsigned char*>(host);
+    c->trace.emplace_back(b, b + bytes);
+  }
+}
 
 StatsMark stats_mark() {
   StatsMark m;
@@ -357,6 +379,17 @@ int t2s2_stats_reset(t2s2_context* ctx, int profile_events) {
     for (auto& f : ctx->fams) f = FamilyStat{f.name};
     ctx->launch_log.clear();
     ctx->profiling = profile_events != 0;
+  });
+}
+
+int t2s2_read_trace(t2s2_context* ctx, int mode, int* count) {
+  return guarded(ctx, [&] {
+    T2S2_REQUIRE(mode >= 0 && mode <= 2, kErrArg, "mode: 0 off, 1 record, 2 replay");
+    if (mode == 1) ctx->trace.clear();
+    if (mode == 0 && count) *count = (int)ctx->trace.size();
+    ctx->trace_pos = 0;
+    ctx->trace_mode = mode;
+    if (mode != 0 && count) *count = (int)ctx->trace.size();
   });
 }
 

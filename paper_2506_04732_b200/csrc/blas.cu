@@ -830,8 +830,7 @@ void ddot_dev(const double* x, const double* y, size_t n, double* out) {
 
 double scalar_to_host(const double* d) {
   double h = 0.0;
-  T2S2_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  host_read(&h, d, sizeof(double));
   return h;
 }
 
@@ -845,10 +844,7 @@ double ddot(const double* x, const double* y, size_t n) {
 
 double dnrm2(const double* x, size_t n) { return std::sqrt(ddot(x, x, n)); }
 
-void to_host(double* h, const double* d, size_t n) {
-  if (n) T2S2_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
-}
+void to_host(double* h, const double* d, size_t n) { host_read(h, d, n * sizeof(double)); }
 
 void to_device(double* d, const double* h, size_t n) {
   if (n) T2S2_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, stream()));

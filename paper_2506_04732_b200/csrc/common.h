@@ -121,6 +121,14 @@ int sm_budget();         // CTAs a whole-GPU cooperative kernel may use (context
 cudaStream_t stream();   // the current context's stream
 bool profiling();        // per-launch CUDA-event timing switched on (t2s2_stats_reset)
 
+// Every device->host read that steers the host (ranks, candidate scores,
+// residuals, solver flags) goes through host_read: copy + synchronise.  A
+// context can record the values of a run and hand them back, without
+// synchronising, to an identical run (t2s2_read_trace): the measurement of
+// what the synchronising reads cost.
+void host_read(void* host, const void* dev, size_t bytes);
+bool replaying_reads();  // host_read returns recorded values, nothing synchronises
+
 // Launch statistics of a captured CUDA graph: mark before and after the
 // capture, then stats_replay(before, after, -1) once (captured launches did
 // not run) and stats_replay(before, after, +1) per graph launch.

@@ -403,8 +403,7 @@ __global__ void __launch_bounds__(kThreads)
 template <class T>
 T read_state(const T* d) {
   T h;
-  T2S2_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, stream()));
-  T2S2_CUDA(cudaStreamSynchronize(stream()));
+  host_read(&h, d, sizeof(T));
   return h;
 }
 
