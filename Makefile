@@ -5,7 +5,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC -Xcompiler -g -Xptxas -v --expt-relaxed-constexpr
 SRC := $(wildcard paper_2506_04732_b200/csrc/*.cu)
-HDR := $(wildcard paper_2506_04732_b200/csrc/*.h) include/t2s2.h
+HDR := $(wildcard paper_2506_04732_b200/csrc/*.h) $(wildcard paper_2506_04732_b200/csrc/*.cuh) include/t2s2.h
 LIB := paper_2506_04732_b200/lib/libt2s2.so
 OBJ := $(patsubst paper_2506_04732_b200/csrc/%.cu,build/%.o,$(SRC))
 

@@ -149,8 +149,10 @@ int t2s2_launch_log(t2s2_context* ctx, t2s2_launch_record* out, int capacity, in
  * mode 1 records the values every such read returns, mode 2 hands the
  * recorded values back to an IDENTICAL run without synchronising (the host
  * then runs ahead of the device; a run that asks for a different read
- * fails with T2S2_ERR_ARG), mode 0 switches both off.  *count = reads
- * recorded.  Used to measure what the synchronising reads cost. */
+ * fails with T2S2_ERR_ARG), mode 3 runs normally and reports (stderr) the
+ * first read whose value differs from the recorded run (a determinism
+ * check), mode 0 switches everything off.  *count = reads recorded.  Used to
+ * measure what the synchronising reads cost. */
 int t2s2_read_trace(t2s2_context* ctx, int mode, int* count);
 
 /* cols == NULL uploads a vector train (cores r0 x rows x r1), otherwise an

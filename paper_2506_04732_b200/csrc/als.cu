@@ -691,6 +691,7 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
   DTensor U, s, Vt;
   svd_thin(m, r1, u.p, U, s, Vt);
+  trace_buffer("split_forward s", s.p, s.size());
   const int kk = s.dim(0);
   SplitSync sync(s, cfg, d);
   const bool enrich = cfg.enrichment_rank > 0 && grad;
@@ -735,6 +736,7 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), cols = n * r1;
   DTensor U, s, Vt;
   svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
+  trace_buffer("split_backward s", s.p, s.size());
   const int kk = s.dim(0);
   SplitSync sync(s, cfg, d);
   const bool enrich = cfg.enrichment_rank > 0 && grad;
@@ -869,6 +871,7 @@ struct Sweep {
               inner_rtol, 40, 10);
       }
       u_gal.view(u_old.shape);
+      trace_buffer("update u_gal", u_gal.p, u_gal.size());
       nu_gal = nop.apply(u_gal);
       probe.run(1, u_gal, nu_gal, c_ls);
     }
@@ -925,10 +928,11 @@ struct Sweep {
         // scipy cg(x0=u_old, rtol, atol=0, maxiter=250, M=diag^{-1})
         u_ls = u_old.clone();
         DTensor dg = normal_diagonal(ln[l], ac, rn[l + 1]);
-        pcg([&](const double* in, double* out, const int* g) { nop(in, out, g); }, (int)size, c_ls.p, u_ls.p, dg.p,
-            inner_rtol, 250);
+        pcg([&](GemmBatch& gb, const double* in, double* out) { nop.add(gb, 0, in, out); }, (int)size, c_ls.p,
+            u_ls.p, dg.p, inner_rtol, 250);
       }
       u_ls.view(u_old.shape);
+      trace_buffer("update u_ls", u_ls.p, u_ls.size());
       DTensor nu_ls = nop.apply(u_ls);
       probe.run(2, u_ls, nu_ls, c_ls);
       probe.read(h, &info, &swapped);

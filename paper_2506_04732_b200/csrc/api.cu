@@ -50,6 +50,7 @@ struct t2s2_context {
   int trace_mode = 0;
   std::vector<std::vector<unsigned char>> trace;
   size_t trace_pos = 0;
+  int trace_diff = -1;  // mode 3: index of the first differing read
 };
 
 struct t2s2_train {
@@ -136,6 +137,30 @@ LaunchScope::~LaunchScope() {
   if (slot >= 0) cudaEventRecord(g_ctx->pending[slot].b, g_ctx->stream);
 }
 
+void trace_buffer(const char* tag, const double* dev, size_t n) {
+  t2s2_context* c = g_ctx;
+  if (c->trace_mode != 1 && c->trace_mode != 3) return;
+  std::vector<double> h(n);
+  const int before = c->trace_diff;
+  host_read(h.data(), dev, n * sizeof(double));
+  if (c->trace_mode == 3 && before < 0 && c->trace_diff >= 0)
+    fprintf(stderr, "   ^ buffer '%s' (%zu doubles)\n", tag, n);
+}
+
+void amend_work(const char* family, double flops, double bytes) {
+  t2s2_context* c = g_ctx;
+  auto it = c->fam_index.find(family);
+  if (it == c->fam_index.end()) return;
+  c->fams[it->second].flops += flops;
+  c->fams[it->second].bytes += bytes;
+  for (size_t k = c->pending.size(); k-- > 0;)
+    if (c->pending[k].fam == it->second) {
+      c->pending[k].flops += flops;
+      c->pending[k].bytes += bytes;
+      break;
+    }
+}
+
 namespace {
 void resolve_pending(t2s2_context* c) {
   if (c->pending.empty()) return;
@@ -168,25 +193,22 @@ void host_read(void* host, const void* dev, size_t bytes) {
   if (c->trace_mode == 1) {
     const unsigned char* b = static_cast<const unsigned char*>(host);
     c->trace.emplace_back(b, b + bytes);
-  }
-}
-
-StatsMark stats_mark() {
-  StatsMark m;
-  for (const FamilyStat& f : g_ctx->fams) {
-    m.launches.push_back(f.launches);
-    m.flops.push_back(f.flops);
-    m.bytes.push_back(f.bytes);
-  }
-  return m;
-}
-
-void stats_replay(const StatsMark& before, const StatsMark& after, int times) {
-  for (size_t f = 0; f < after.launches.size() && f < g_ctx->fams.size(); ++f) {
-    const bool old = f < before.launches.size();
-    g_ctx->fams[f].launches += times * (after.launches[f] - (old ? before.launches[f] : 0));
-    g_ctx->fams[f].flops += times * (after.flops[f] - (old ? before.flops[f] : 0.0));
-    g_ctx->fams[f].bytes += times * (after.bytes[f] - (old ? before.bytes[f] : 0.0));
+  } else if (c->trace_mode == 3) {
+    // compare with the recorded run: report the first read that differs
+    const size_t k = c->trace_pos++;
+    if (k < c->trace.size() && c->trace_diff < 0 &&
+        (c->trace[k].size() != bytes || std::memcmp(c->trace[k].data(), host, bytes) != 0)) {
+      c->trace_diff = (int)k;
+      fprintf(stderr, "host_read compare: read %zu (%zu bytes, recorded %zu) differs\n", k, bytes,
+              c->trace[k].size());
+      const size_t nd = bytes / 8 < c->trace[k].size() / 8 ? bytes / 8 : c->trace[k].size() / 8;
+      for (size_t i = 0; i < nd && i < 24; ++i) {
+        double a, b;
+        std::memcpy(&a, c->trace[k].data() + 8 * i, 8);
+        std::memcpy(&b, static_cast<const unsigned char*>(host) + 8 * i, 8);
+        if (std::memcmp(&a, &b, 8) != 0) fprintf(stderr, "   [%zu] recorded %.17g now %.17g\n", i, a, b);
+      }
+    }
   }
 }
 
@@ -384,7 +406,8 @@ int t2s2_stats_reset(t2s2_context* ctx, int profile_events) {
 
 int t2s2_read_trace(t2s2_context* ctx, int mode, int* count) {
   return guarded(ctx, [&] {
-    T2S2_REQUIRE(mode >= 0 && mode <= 2, kErrArg, "mode: 0 off, 1 record, 2 replay");
+    T2S2_REQUIRE(mode >= 0 && mode <= 3, kErrArg, "mode: 0 off, 1 record, 2 replay, 3 compare");
+    ctx->trace_diff = -1;
     if (mode == 1) ctx->trace.clear();
     if (mode == 0 && count) *count = (int)ctx->trace.size();
     ctx->trace_pos = 0;

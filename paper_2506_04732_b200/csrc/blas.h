@@ -74,6 +74,12 @@ class GemmBatch {
   void scale_last(const double* rs, const double* cs);
   void run();
   void set_guard(const int* g) { guard_ = g; }
+  // The added problems as ONE program for a kernel that runs it inside its
+  // own loop (gemm_device.cuh; the Krylov solvers): false when they do not
+  // fit one program.  wide: the program needs the 64x136 instantiation;
+  // max_tiles: the largest stage.  The scratch of temp() lives until the
+  // batch is destroyed.
+  bool build_program(GemmProgram& prog, bool& wide, int& max_tiles, double& flops);
 
  private:
   const int* guard_ = nullptr;
@@ -85,6 +91,9 @@ class GemmBatch {
   std::vector<DTensor> temps_;
   double flops_ = 0.0;
 };
+
+// dynamic shared memory of a kernel running programs (gemm_device.cuh)
+int gemm_program_smem(bool wide);
 
 DTensor permute(const DTensor& a, const std::vector<int>& perm);
 

@@ -59,11 +59,6 @@ struct Allocator {
   cudaStream_t stream = nullptr;
   std::unordered_map<size_t, std::vector<double*>> free_lists;
   std::unordered_map<double*, size_t> live;
-  // set while a CUDA graph is being captured on the stream: a cache miss
-  // then throws instead of calling cudaMallocAsync (a graph-owned
-  // allocation would leak into the free lists), and the caller falls back
-  // to eager launches
-  bool capturing = false;
   static size_t size_class(size_t n) {
     size_t c = 32;
     while (c < n) c <<= 1;
@@ -78,7 +73,6 @@ struct Allocator {
       p = fl.back();
       fl.pop_back();
     } else {
-      T2S2_REQUIRE(!capturing, kErrCuda, "allocator cache miss during graph capture");
       void* v = nullptr;
       T2S2_CUDA(cudaMallocAsync(&v, c * sizeof(double), stream));
       p = static_cast<double*>(v);
@@ -110,6 +104,10 @@ struct LaunchScope {
   ~LaunchScope();
 };
 
+// Work of the most recent launch of a family that was not known when it was
+// enqueued (a device-side loop): added to the family and to that launch's record.
+void amend_work(const char* family, double flops, double bytes);
+
 Allocator& allocator();  // the current context's allocator
 // Per-device launch properties, cached in the current context (one context
 // per host thread and device, so no shared mutable state between threads):
@@ -128,16 +126,9 @@ bool profiling();        // per-launch CUDA-event timing switched on (t2s2_stats
 // what the synchronising reads cost.
 void host_read(void* host, const void* dev, size_t bytes);
 bool replaying_reads();  // host_read returns recorded values, nothing synchronises
-
-// Launch statistics of a captured CUDA graph: mark before and after the
-// capture, then stats_replay(before, after, -1) once (captured launches did
-// not run) and stats_replay(before, after, +1) per graph launch.
-struct StatsMark {
-  std::vector<long long> launches;
-  std::vector<double> flops, bytes;
-};
-StatsMark stats_mark();
-void stats_replay(const StatsMark& before, const StatsMark& after, int times);
+// Determinism probe: while a trace is recorded (mode 1) or compared (mode 3)
+// the tagged device buffer joins the trace like a host read; otherwise a no-op.
+void trace_buffer(const char* tag, const double* dev, size_t n);
 
 // A dense row-major device array with a host-known shape.  Owns its
 // buffer (move-only).

@@ -75,7 +75,8 @@ struct GjArgs {
   double* inv;    // npan * kInv
   double* wbuf;   // 3 x (kP x (N+1)), column-major ld kP (phase p: buffer p % 3)
   int* info;      // 0, or -1: a multiplier exceeded 1 / zero pivot
-  unsigned* sync; // [0] arrivals, [1 + p] finished feeder tasks of phase p (zeroed by the host)
+  unsigned* sync; // [0] tile-worker arrivals, [1] diagonal blocks published by CTA 0,
+                  // [2 + p] finished feeder tasks of phase p (zeroed by the host)
   unsigned long long* prof;
 };
 
@@ -101,10 +102,14 @@ __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// Phase hand-off without a grid-wide barrier: every CTA adds one arrival per
-// phase (CTA 0 after factoring the next diagonal block, the others after
-// their tile tasks); a CTA waits for a count of arrivals, or — CTA 0 — only
-// for the tile tasks that produce its next diagonal block.  Release: the
+// Phase hand-off without a grid-wide barrier, two counters: the tile workers
+// add one arrival per phase after their tile tasks, CTA 0 counts the diagonal
+// blocks it has published.  A tile worker starts phase p once every worker
+// has finished phase p - 1 AND D_p^{-1} is published; CTA 0 waits only for
+// the tile tasks that produce its next diagonal block.  (One shared counter
+// is not enough: CTA 0 runs a phase ahead, and its early arrival would stand
+// in for a tile worker that has not finished — the other workers would start
+// on rows and columns that are still being updated.)  Release: the
 // CTA's stores, a CTA barrier, one thread's fence and atomic; acquire: one
 // thread's ld.acquire spin, then a CTA barrier (loads use ld.global.cg).
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -653,8 +658,9 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     a.prof[cta * 4 + (slot)] += tq - tp;       \
     tp = tq;                                   \
   }
-  unsigned* arrivals = a.sync;
-  unsigned* feed = a.sync + 1;  // feed[p]: finished feeder tasks of phase p
+  unsigned* arrivals = a.sync;   // tile workers: G - 1 per phase with a next diagonal block, G in the last
+  unsigned* published = a.sync + 1;  // D_0^{-1} .. published by CTA 0
+  unsigned* feed = a.sync + 2;   // feed[p]: finished feeder tasks of phase p
   if (cta == 0) {
     // *info = 0 before the first hand-off; every check that can set it runs
     // after that
@@ -666,7 +672,7 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       if (r < kb && c < kb) s.dg[c * 33 + r] = __ldcg(a.A + (size_t)c * N + r);
     }
     gj_diag(a, 0, kb, s);
-    cta_signal(arrivals);  // arrival 1: D_0^{-1} published
+    cta_signal(published);  // D_0^{-1}
   }
   TileRegs R;
   // The tile tasks of phase p that produce the next diagonal block of phase
@@ -696,10 +702,14 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
         gj_diag(a, p + 1, ph.kb2, s);
         if (pr) a.prof[9] += gtimer() - td;
       }
-      cta_signal(arrivals);
+      cta_signal(published);  // D_{p+1}^{-1} (also when skipped)
     } else {
-      // all arrivals of the earlier phases (CTA 0's: D_p^{-1} published)
-      if (G > 1) cta_wait(arrivals, 1u + (unsigned)G * (unsigned)p, a.info, false);
+      // every tile worker has finished the earlier phases (all of them had a
+      // next diagonal block: G - 1 workers each) and D_p^{-1} is published
+      if (G > 1) {
+        cta_wait(arrivals, (unsigned)(G - 1) * (unsigned)p, a.info, false);
+        cta_wait(published, (unsigned)p + 1u, a.info, false);
+      }
       const bool live = __ldcg(a.info) == 0;
       if (has_diag && G == 1 && live) {
         special_tile(a, ph, s);
@@ -756,7 +766,8 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
   // last panel's rows, which are in its row-panel buffer (a single panel
   // never ran a tile phase: x = D^{-1} b)
   if (cta == 0) {
-    if (G > 1) cta_wait(arrivals, 1u + (unsigned)G * (unsigned)npan, a.info, false);
+    // the last phase has no next diagonal block: all G CTAs were tile workers
+    if (G > 1) cta_wait(arrivals, (unsigned)(G - 1) * (unsigned)(npan - 1) + (unsigned)G, a.info, false);
     if (__ldcg(a.info) == 0) {
       const int p = npan - 1, k0 = p * kP, kb = N - k0;
       if (npan > 1) {
@@ -802,8 +813,8 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   const int npan = (N + kP - 1) / kP;
   double* inv = allocator().alloc((size_t)npan * kInv);
   double* wbuf = allocator().alloc((size_t)3 * kP * (N + 1));
-  unsigned* sync = reinterpret_cast<unsigned*>(allocator().alloc((size_t)(npan + 2) / 2 + 1));
-  T2S2_CUDA(cudaMemsetAsync(sync, 0, sizeof(unsigned) * (size_t)(npan + 2), stream()));
+  unsigned* sync = reinterpret_cast<unsigned*>(allocator().alloc((size_t)(npan + 3) / 2 + 1));
+  T2S2_CUDA(cudaMemsetAsync(sync, 0, sizeof(unsigned) * (size_t)(npan + 3), stream()));
   GjArgs a{N, A, b, inv, wbuf, info_dev, sync, nullptr};  // *info zeroed by the kernel
   void* params[] = {&a};
   {

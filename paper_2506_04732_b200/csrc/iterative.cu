@@ -1,10 +1,11 @@
 // Device GMRES(restart) and Jacobi-PCG (see iterative.h).
-#include <atomic>
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 
 #include "blas.h"
+#include "gemm_device.cuh"
 #include "iterative.h"
 
 #include <cooperative_groups.h>
@@ -26,11 +27,6 @@ struct GmState {
   int active;
   int breakdown;
   int restart;
-};
-
-struct CgState {
-  double rho_prev, rho_cur;
-  int active;
 };
 
 constexpr int kCgMaxCtas = 148;
@@ -176,12 +172,11 @@ __device__ __forceinline__ void sum_partials(const double* part, int G, int nk, 
     }
     double t = 0.0;
 #pragma unroll
-    for (int j = 0; j < kMaxPartialsPerLane; ++j)
-#pragma unroll 8
-      for (int l = 0; l < 32; ++l) {
-        const double x = __shfl_sync(0xffffffffu, v[j], l);
-        if (32 * j + l < G) t += x;
-      }
+    for (int j = 0; j < kMaxPartialsPerLane; ++j) {
+      // only the lanes that hold a partial are walked (G is uniform)
+      const int m = G - 32 * j < 32 ? G - 32 * j : 32;
+      for (int l = 0; l < m; ++l) t += __shfl_sync(0xffffffffu, v[j], l);
+    }
     if (lane == 0) out[k] = t;
   }
 }
@@ -294,10 +289,38 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// scipy cg (Jacobi-preconditioned), split around the matvec q = A p into two
-// cooperative kernels over G CTAs.  Reductions are deterministic: per-CTA
-// partials, one grid barrier, every CTA sums the G partials in CTA order
-// (sum_partials: the loads in flight at once, the adds in order).
+// scipy cg (Jacobi-preconditioned) as ONE cooperative kernel for the whole
+// iteration loop: the matvec q = A p is a GEMM program run inside the loop
+// (gemm_device.cuh, a grid barrier between its stages), the vector updates
+// and the three sums of an iteration run on the first a.G CTAs, and every CTA
+// decides convergence from the same sums, so the loop ends grid-wide without
+// the host.  Reductions are deterministic: per-CTA partials, one grid
+// barrier, every CTA sums the G partials in CTA order (sum_partials: the
+// loads in flight at once, the adds in order).  With an empty program the
+// kernel runs the vector part of ONE iteration after a matvec launched
+// before it (operators whose matvec does not fit one program).
+struct CgState {
+  double rho_cur;
+  int active;
+  int iters;  // iterations performed so far
+};
+
+struct PcgArgs {
+  CgState* st;
+  const double* q;  // A p
+  double* x;
+  double* r;
+  const double* diag;
+  double* p;
+  double* part;  // 3 * G partials
+  int n, G;
+  double atol;
+  int top;         // start with the top of iteration 0 (rho, p from the initial residual)
+  int it0, count;  // then iterations it0 .. it0 + count - 1
+};
+
+constexpr int kPcgThreads = 256;  // the GEMM programs' CTA
+
 __device__ __forceinline__ double block_reduce(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -309,94 +332,116 @@ __device__ __forceinline__ double block_reduce(double v, double* red) {
   return t;
 }
 
-// top of iteration: ||r|| < atol -> stop; rho = r.(r/diag); p = r/diag + beta p
-__global__ void __launch_bounds__(kThreads)
-    cg_pre_kernel(CgState* st, const double* r, const double* diag, double* p, int n, double atol,
-                  int iteration, double* part) {
-  cg::grid_group grid = cg::this_grid();
+template <bool WIDE>
+__global__ void __launch_bounds__(kPcgThreads, 2)
+    pcg_kernel(const __grid_constant__ GemmProgram prog, const PcgArgs a) {
+  extern __shared__ __align__(16) double gemm_smem[];
   __shared__ double red[32];
-  if (!st->active) return;
-  const int G = gridDim.x, gt = blockIdx.x * blockDim.x + threadIdx.x, gs = G * blockDim.x;
-  double rr = 0.0, rz = 0.0;
-  for (int i = gt; i < n; i += gs) {
-    const double ri = r[i];
-    rr = fma(ri, ri, rr);
-    rz = fma(ri, ri / diag[i], rz);
-  }
-  rr = block_reduce(rr, red);
-  rz = block_reduce(rz, red);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = rr;
-    part[G + blockIdx.x] = rz;
-  }
-  grid.sync();
   __shared__ double sums[2];
-  sum_partials(part, G, 2, sums);  // rows: rr partials, rz partials
-  __syncthreads();
-  const double srr = sums[0], rho = sums[1];
-  if (sqrt(srr) < atol) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
-    return;
-  }
-  const double beta = iteration > 0 ? rho / st->rho_prev : 0.0;
-  for (int i = gt; i < n; i += gs) {
-    const double z = r[i] / diag[i];
-    p[i] = iteration > 0 ? fma(p[i], beta, z) : z;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_cur = rho;
-}
-
-// After q = A p: alpha = rho / p.q, x += alpha p, r -= alpha q — fused
-// with the next iteration's top (||r|| < atol -> stop, rho, p update): one
-// launch per iteration besides the matvec.
-__global__ void __launch_bounds__(kThreads)
-    cg_step_kernel(CgState* st, const double* q, double* x, double* r, const double* diag,
-                   double* p, int n, double atol, int iteration, double* part) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[32];
-  if (!st->active) return;
-  const int G = gridDim.x, gt = blockIdx.x * blockDim.x + threadIdx.x, gs = G * blockDim.x;
-  double pq = 0.0;
-  for (int i = gt; i < n; i += gs) pq = fma(p[i], q[i], pq);
-  pq = block_reduce(pq, red);
-  if (threadIdx.x == 0) part[2 * G + blockIdx.x] = pq;
-  grid.sync();
-  __shared__ double sums[2];
-  sum_partials(part + 2 * G, G, 1, sums);
-  __syncthreads();
-  const double spq = sums[0];
-  const double rho_cur = st->rho_cur;
-  const double alpha = rho_cur / spq;
-  double rr = 0.0, rz = 0.0;
-  for (int i = gt; i < n; i += gs) {
-    x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, q[i], r[i]);
-    r[i] = ri;
-    rr = fma(ri, ri, rr);
-    rz = fma(ri, ri / diag[i], rz);
+  CgState* st = a.st;
+  if (!st->active) return;  // uniform: written only after a grid barrier of this launch
+  const int G = a.G, n = a.n;
+  const bool vec = (int)blockIdx.x < G;  // this CTA takes part in the vector phases
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = G * blockDim.x;
+  const double* q = a.q;
+  const double* diag = a.diag;
+  double *x = a.x, *r = a.r, *p = a.p, *part = a.part;
+  double rho_cur;
+  if (a.top) {
+    // top of iteration 0: ||r|| < atol -> stop; rho = r.(r/diag); p = r/diag
+    if (vec) {
+      double rr = 0.0, rz = 0.0;
+      for (int i = gt; i < n; i += gs) {
+        const double ri = r[i];
+        rr = fma(ri, ri, rr);
+        rz = fma(ri, ri / diag[i], rz);
+      }
+      rr = block_reduce(rr, red);
+      rz = block_reduce(rz, red);
+      if (threadIdx.x == 0) {
+        part[blockIdx.x] = rr;
+        part[G + blockIdx.x] = rz;
+      }
+    }
+    grid.sync();
+    sum_partials(part, G, 2, sums);  // rows: rr partials, rz partials
+    __syncthreads();
+    const double srr = sums[0];
+    rho_cur = sums[1];
+    if (sqrt(srr) < a.atol) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
+      return;
+    }
+    if (vec)
+      for (int i = gt; i < n; i += gs) p[i] = r[i] / diag[i];
+    if (a.count == 0) {
+      // the matvec runs outside: this launch was the top of iteration 0 only
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->rho_cur = rho_cur;
+      return;
+    }
+    grid.sync();  // p complete before the first matvec
+  } else {
+    rho_cur = st->rho_cur;
   }
-  rr = block_reduce(rr, red);
-  rz = block_reduce(rz, red);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = rr;
-    part[G + blockIdx.x] = rz;
+  int it = a.it0;
+  bool done = false;
+  for (; it < a.it0 + a.count; ++it) {
+    if (prog.nstage > 0) {
+      gemm_device::gemm_program_run<WIDE>(prog, gemm_smem, grid);  // q = A p
+      grid.sync();
+    }
+    // alpha = rho / p.q
+    if (vec) {
+      double pq = 0.0;
+      for (int i = gt; i < n; i += gs) pq = fma(p[i], q[i], pq);
+      pq = block_reduce(pq, red);
+      if (threadIdx.x == 0) part[2 * G + blockIdx.x] = pq;
+    }
+    grid.sync();
+    __syncthreads();  // sums[] of the previous phase read by every thread
+    sum_partials(part + 2 * G, G, 1, sums);
+    __syncthreads();
+    const double alpha = rho_cur / sums[0];
+    // x += alpha p, r -= alpha q, and the next iteration's top
+    if (vec) {
+      double rr = 0.0, rz = 0.0;
+      for (int i = gt; i < n; i += gs) {
+        x[i] = fma(alpha, p[i], x[i]);
+        const double ri = fma(-alpha, q[i], r[i]);
+        r[i] = ri;
+        rr = fma(ri, ri, rr);
+        rz = fma(ri, ri / diag[i], rz);
+      }
+      rr = block_reduce(rr, red);
+      rz = block_reduce(rz, red);
+      if (threadIdx.x == 0) {
+        part[blockIdx.x] = rr;
+        part[G + blockIdx.x] = rz;
+      }
+    }
+    grid.sync();
+    __syncthreads();  // sums[0] (p.q) read by every thread above
+    sum_partials(part, G, 2, sums);
+    __syncthreads();
+    const double srr = sums[0], rho = sums[1];
+    if (sqrt(srr) < a.atol) {
+      done = true;
+      ++it;
+      break;
+    }
+    const double beta = rho / rho_cur;
+    if (vec)
+      for (int i = gt; i < n; i += gs) p[i] = fma(p[i], beta, r[i] / diag[i]);
+    rho_cur = rho;
+    // p complete before the next matvec of this launch reads it (the launch
+    // boundary orders it otherwise)
+    if (prog.nstage > 0 && it + 1 < a.it0 + a.count) grid.sync();
   }
-  grid.sync();
-  // next iteration's top: convergence check, rho, p update
-  __syncthreads();  // sums[0] (spq) read by every thread above
-  sum_partials(part, G, 2, sums);  // rows: rr partials, rz partials
-  __syncthreads();
-  const double srr = sums[0], rho = sums[1];
-  if (sqrt(srr) < atol) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->active = 0;
-    return;
-  }
-  const double beta = rho / rho_cur;  // rho_prev of the next iteration = this rho_cur
-  for (int i = gt; i < n; i += gs) p[i] = fma(p[i], beta, r[i] / diag[i]);
-  grid.sync();  // every CTA has read rho_cur
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->rho_prev = rho_cur;
-    st->rho_cur = rho;
+    st->rho_cur = rho_cur;
+    st->iters = it;
+    if (done) st->active = 0;
   }
 }
 
@@ -503,7 +548,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   return inner;
 }
 
-int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, double rtol,
+int pcg(const ProgramBuilder& A, int n, const double* b, double* x, const double* diag, double rtol,
         int maxiter) {
   const double bnrm2 = dnrm2(b, n);
   const double atol = rtol * bnrm2;
@@ -516,100 +561,74 @@ int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, 
   double* q = allocator().alloc(n);
   double* part = allocator().alloc(3 * kCgMaxCtas);
   CgState* st = reinterpret_cast<CgState*>(allocator().alloc(sizeof(CgState) / sizeof(double) + 1));
-  A(x, r, nullptr);
+  auto apply = [&](const double* in, double* out) {
+    GemmBatch gb;
+    A(gb, in, out);
+    gb.run();
+  };
+  apply(x, r);
   daxpby(1.0, b, -1.0, r, n);
-  CgState init{0.0, 0.0, 1};
+  CgState init{0.0, 1, 0};
   T2S2_CUDA(cudaMemcpyAsync(st, &init, sizeof(CgState), cudaMemcpyHostToDevice, stream()));
-  int G = (n + 2047) / 2048;
-  if (G > kCgMaxCtas) G = kCgMaxCtas;
+  // the matvec q = A p as one program inside the kernel; T2S2_PCG_EXTERNAL_MATVEC=1
+  // (tests: same bits either way) launches it separately as operators
+  // beyond one program do
+  GemmBatch gbq;
+  A(gbq, p, q);
+  GemmProgram prog{};
+  bool wide = false;
+  int max_tiles = 0;
+  double mv_flops = 0.0;
+  static const bool external = getenv("T2S2_PCG_EXTERNAL_MATVEC") != nullptr;
+  const bool fused = !external && gbq.build_program(prog, wide, max_tiles, mv_flops);
+  if (!fused) prog = GemmProgram{};
+  const void* kern = wide ? (const void*)pcg_kernel<true> : (const void*)pcg_kernel<false>;
+  const int smem = gemm_program_smem(wide);
+  max_dynamic_smem(kern, smem);
   // cooperative grid: no more CTAs than co-reside on this context's SMs (an
-  // SM partition has fewer than the device's 148); the same G — and so the
-  // same reduction order — as on the whole GPU whenever it fits
-  {
-    int occ = occupancy((const void*)cg_step_kernel, kThreads, 0);
-    const int o2 = occupancy((const void*)cg_pre_kernel, kThreads, 0);
-    if (o2 < occ) occ = o2;
-    if (G > num_sms() * occ) G = num_sms() * occ;
-  }
-  if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
+  // SM partition has fewer than the device's 148); the vector phases run on
+  // the first G CTAs — the same G, and so the same reduction order, with and
+  // without the program
+  int cap = num_sms() * occupancy(kern, kPcgThreads, smem);
+  if (sm_budget() > 0 && cap > sm_budget()) cap = sm_budget();
+  int G = (n + 1023) / 1024;
+  if (G > kCgMaxCtas) G = kCgMaxCtas;
+  if (G > cap) G = cap;
   if (G < 1) G = 1;
+  int grid = fused && max_tiles > G ? max_tiles : G;
+  if (grid > cap) grid = cap;
+  PcgArgs a{st, q, x, r, diag, p, part, n, G, atol, 1, 0, maxiter};
+  auto launch = [&](int top, int it0, int count) {
+    a.top = top;
+    a.it0 = it0;
+    a.count = count;
+    void* params[] = {&prog, &a};
+    LaunchScope ls("cg", 0.0, 0.0);
+    T2S2_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kPcgThreads), params, smem, stream()));
+  };
   int it = 0;
-  double at = atol;
-  constexpr int poll = 20;  // iterations per captured graph / host poll
-  {
-    LaunchScope ls("cg", 6.0 * n, 40.0 * n);
-    int itv = 0;
-    void* params[] = {&st, &r, &diag, &p, &n, &at, &itv, &part};
-    T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_pre_kernel, dim3(G), dim3(kThreads), params,
-                                          0, stream()));
-  }
-  // One CUDA graph holds `poll` whole iterations (matvec program + update;
-  // every pointer is fixed for this solve and the kernels read their state
-  // from the device), captured once and replayed between host polls: the
-  // host no longer builds and launches two cooperative kernels per
-  // iteration.  Iterations after convergence are device no-ops, as without
-  // the graph.  The remainder below a multiple of `poll` runs eagerly.
-  // T2S2_NO_GRAPH=1 runs the same iterations eagerly (tests check the
-  // replay is bit-identical to it)
-  static std::atomic<bool> graphs_ok{getenv("T2S2_NO_GRAPH") == nullptr};
-  // not on an SM partition: a replayed graph of cooperative kernels hangs in
-  // a green context (measured), the same iterations run eagerly there
-  if (graphs_ok && !profiling() && !on_partition() && maxiter >= 2 * poll) {
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    const StatsMark before = stats_mark();
-    bool captured = false;
-    T2S2_CUDA(cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal));
-    allocator().capturing = true;
-    try {
-      for (int k = 0; k < poll; ++k) {
-        A(p, q, &st->active);
-        int itv = k;
-        void* params[] = {&st, &q, &x, &r, &diag, &p, &n, &at, &itv, &part};
-        LaunchScope ls("cg", 12.0 * n, 88.0 * n);
-        T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_step_kernel, dim3(G), dim3(kThreads),
-                                              params, 0, stream()));
-      }
-      captured = true;
-    } catch (const Error&) {
-    }
-    allocator().capturing = false;
-    const cudaError_t ec = cudaStreamEndCapture(stream(), &graph);
-    if (captured && ec == cudaSuccess && graph &&
-        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
-      const StatsMark after = stats_mark();
-      stats_replay(before, after, -1);
-      for (; it + poll <= maxiter; it += poll) {
-        if (it > 0 && !read_flag(&st->active)) break;
-        T2S2_CUDA(cudaGraphLaunch(exec, stream()));
-        stats_replay(before, after, 1);
-      }
-    } else {
-      // an allocator cache miss aborted this capture: eager launches this
-      // time; a capture that completed but cannot be instantiated means
-      // graphs are unsupported here: eager from now on
-      if (captured) graphs_ok = false;
-      const StatsMark after = stats_mark();
-      stats_replay(before, after, -1);
-      (void)cudaGetLastError();
-    }
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-  }
-  for (; it < maxiter; ++it) {
-    if (it > 0 && it % poll == 0 && !read_flag(&st->active)) break;
-    A(p, q, &st->active);  // skipped on the device once converged
-    {
-      // this iteration's update and the next one's top (convergence, p)
-      LaunchScope ls("cg", 12.0 * n, 88.0 * n);
-      int itv = it;
-      void* params[] = {&st, &q, &x, &r, &diag, &p, &n, &at, &itv, &part};
-      T2S2_CUDA(cudaLaunchCooperativeKernel((void*)cg_step_kernel, dim3(G), dim3(kThreads), params,
-                                            0, stream()));
-    }
+  if (fused) {
+    launch(1, 0, maxiter);
     T2S2_CHECK_LAUNCH();
+    const CgState h = read_state<CgState>(st);
+    it = h.iters;
+    // the work of the iterations performed (known only now)
+    amend_work("cg", it * (mv_flops + 12.0 * n) + 6.0 * n, it * 88.0 * n + 40.0 * n);
+  } else {
+    constexpr int poll = 20;  // iterations between host polls of the convergence flag
+    launch(1, 0, 0);          // top of iteration 0
+    for (; it < maxiter; ++it) {
+      if (it > 0 && it % poll == 0 && !read_flag(&st->active)) break;
+      GemmBatch gb;  // skipped on the device once converged
+      gb.set_guard(&st->active);
+      A(gb, p, q);
+      gb.run();
+      launch(0, it, 1);
+      T2S2_CHECK_LAUNCH();
+    }
+    it = read_state<CgState>(st).iters;
+    amend_work("cg", it * 12.0 * n + 6.0 * n, it * 88.0 * n + 40.0 * n);
   }
-  T2S2_CUDA(cudaStreamSynchronize(stream()));  // init lives on the host stack
   allocator().release(r);
   allocator().release(p);
   allocator().release(q);

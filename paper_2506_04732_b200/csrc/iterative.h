@@ -5,12 +5,13 @@
 // The Krylov recurrences follow scipy 1.18's pure-Python implementations
 // (modified Gram-Schmidt Arnoldi with LAPACK-style Givens rotations and the
 // gh-8400 inner-tolerance control; textbook PCG), with every vector and
-// scalar resident on the device.  The host only polls a convergence flag
-// every few iterations.
+// scalar resident on the device.  GMRES: the host polls a convergence flag
+// every few iterations; PCG: the loop runs on the device.
 #pragma once
 
 #include <functional>
 
+#include "blas.h"
 #include "common.h"
 
 namespace t2s2 {
@@ -26,8 +27,12 @@ using MatVec = std::function<void(const double* in, double* out, const int* guar
 int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int restart,
           int maxiter);
 
-// Preconditioner M = diag^{-1}.
-int pcg(const MatVec& A, int n, const double* b, double* x, const double* diag, double rtol,
+// Adds the problems of out = A in to a GEMM batch (stages from 0).
+using ProgramBuilder = std::function<void(GemmBatch& gb, const double* in, double* out)>;
+
+// Preconditioner M = diag^{-1}.  The whole iteration loop is one cooperative
+// kernel with the matvec program inside it.
+int pcg(const ProgramBuilder& A, int n, const double* b, double* x, const double* diag, double rtol,
         int maxiter);
 
 }  // namespace t2s2

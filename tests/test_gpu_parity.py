@@ -208,7 +208,7 @@ def test_dense_local_solve_kernel(pk, n):
     assert np.linalg.norm(a @ x - b) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(x)
 
 
-@pytest.mark.parametrize("n", [7, 64, 65, 300, 1000])
+@pytest.mark.parametrize("n", [7, 64, 65, 300, 1000, 1953, 2000, 2500])
 def test_dense_local_solve_without_interchanges(pk, n):
     """Column diagonally dominant matrices: partial pivoting makes no
     interchange, so the verified no-pivot kernel alone must solve them, to
@@ -489,17 +489,28 @@ def test_norm_and_round_wide_cores(pk, rank):
         assert np.linalg.norm(ot.tt_full(r.cores) - ot.tt_full(ro)) <= 1e-9 * np.linalg.norm(ot.tt_full(ro))
 
 
-@pytest.mark.parametrize("n", [264, 1601, 1848])
-def test_dense_local_solve_deterministic(pk, n):
+@pytest.mark.parametrize("n,budget", [(264, 0), (1601, 0), (1848, 0), (1953, 0), (2000, 0), (1200, 24),
+                                      (1952, 64)])
+def test_dense_local_solve_deterministic(pk, n, budget):
     """The Gauss-Jordan solve hands panels between CTAs and warps without
     grid barriers (arrival counts, named barriers): repeated solves of one
-    system must be bit-identical (N = 1601: a one-row last panel)."""
+    system must be bit-identical and accurate (N = 1601: a one-row last
+    panel).  Long tile phases — N >= 1953 on 148 CTAs, or fewer CTAs (an SM
+    budget) — are the case where CTA 0 finishes a phase ahead of the tile
+    workers: its arrival must not stand in for theirs (a shared arrival
+    counter did, giving errors of 1e-6 that changed from run to run)."""
     from paper_2506_04732_b200 import _native
 
     rng = np.random.default_rng(7 + n)
     a = rng.standard_normal((n, n))
     a += np.diag(np.abs(a).sum(0))
     b = rng.standard_normal(n)
-    ref = _native.dense_solve(a, b)
-    for _ in range(8):
-        assert np.array_equal(_native.dense_solve(a, b), ref)
+    want = np.linalg.solve(a, b)
+    _native.set_thread_sm_budget(budget)
+    try:
+        ref = _native.dense_solve(a, b)
+        for _ in range(8):
+            assert np.array_equal(_native.dense_solve(a, b), ref)
+    finally:
+        _native.set_thread_sm_budget(0)
+    assert np.linalg.norm(ref - want) <= 1e-13 * np.linalg.norm(want)
