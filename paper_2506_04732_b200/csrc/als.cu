@@ -426,9 +426,8 @@ struct NormalOp {  // (A^T A)-projected block (_ls_matvec / _LsApply)
     const int q = o.rA * o.rA * rw;
     gb.add(s0 + 3, false, true, rx * o.nn, ry, q, t3.p, q, 0, pnr.p, q, 0, out, ry, 0);
   }
-  void operator()(const double* u, double* out, const int* guard = nullptr) {
+  void operator()(const double* u, double* out) {
     GemmBatch gb;
-    gb.set_guard(guard);
     add(gb, 0, u, out);
     gb.run();
   }
@@ -447,14 +446,12 @@ struct GalerkinOp {  // Galerkin block (_gal_matvec)
   GalerkinOp(const DTensor& l, const DTensor& a, const DTensor& ag, const DTensor& r)
       : pal(l), acg(ag), par(r), o(a), rx(l.dim(0)), rX(l.dim(2)), ry(r.dim(0)), rY(r.dim(2)),
         t1({rx, o.ra, o.nn, rY}), t2({rx, o.nm, o.rA, rY}) {}
-  void operator()(const double* u, double* out, const int* guard = nullptr) {
-    GemmBatch gb;
-    gb.set_guard(guard);
+  // 3 stages from 0; the scratch is shared, so one application per batch
+  void add(GemmBatch& gb, const double* u, double* out) {
     gb.add(0, false, false, rx * o.ra, o.nn * rY, rX, pal.p, rX, 0, u, o.nn * rY, 0, t1.p, o.nn * rY, 0);
     gb.add(1, false, false, o.nm * o.rA, rY, o.ra * o.nn, acg.p, o.ra * o.nn, 0, t1.p, rY,
            (long long)o.ra * o.nn * rY, t2.p, rY, (long long)o.nm * o.rA * rY, rx);
     gb.add(2, false, true, rx * o.nm, ry, o.rA * rY, t2.p, o.rA * rY, 0, par.p, o.rA * rY, 0, out, ry, 0);
-    gb.run();
   }
 };
 
@@ -867,8 +864,8 @@ struct Sweep {
         // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
         u_gal = u_old.clone();
         GalerkinOp gop(la[l], ac, acg[l], ra[l + 1]);
-        gmres([&](const double* in, double* out, const int* g) { gop(in, out, g); }, (int)size, c_gal.p, u_gal.p,
-              inner_rtol, 40, 10);
+        gmres([&](GemmBatch& gb, const double* in, double* out) { gop.add(gb, in, out); }, (int)size, c_gal.p,
+              u_gal.p, inner_rtol, 40, 10);
       }
       u_gal.view(u_old.shape);
       trace_buffer("update u_gal", u_gal.p, u_gal.size());

@@ -91,11 +91,9 @@ __global__ void __launch_bounds__(kThreads)
 
 __global__ void gm_set_restart(GmState* st, int restart) { st->restart = restart; }
 
-// Arnoldi step for column col (w = A v_col already in V[col+1]).
-__global__ void __launch_bounds__(kThreads)
-    gm_arnoldi_kernel(GmState* st, double* V, int n, int col, int restart) {
-  __shared__ double red[33];
-  if (!st->active) return;
+// Arnoldi step for column col (w = A v_col already in V[col+1]) on one CTA:
+// modified Gram-Schmidt as scipy's loop (small systems).
+__device__ void gm_arnoldi_cta(GmState* st, double* V, int n, int col, int restart, double* red) {
   double* w = V + (size_t)(col + 1) * n;
   const double h0 = sqrt(cta_dot(w, w, n, red));
   for (int k = 0; k <= col; ++k) {
@@ -181,17 +179,19 @@ __device__ __forceinline__ void sum_partials(const double* part, int G, int nk, 
   }
 }
 
-__global__ void __launch_bounds__(kThreads)
-    gm_arnoldi_mc_kernel(GmState* st, double* V, int n, int col, double* part) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double hs[kMaxRestart + 2], h2[kMaxRestart + 2];
-  if (!st->active) return;
-  const int G = gridDim.x;
-  const int chunk = (n + G - 1) / G, i0 = blockIdx.x * chunk;
+struct ArnoldiSmem {
+  double hs[kMaxRestart + 2], h2[kMaxRestart + 2], red[33], sw1[1];
+};
+__device__ void gm_arnoldi_grid(GmState* st, double* V, int n, int col, double* part, int G,
+                                cg::grid_group& grid, ArnoldiSmem& sm) {
+  double* hs = sm.hs;
+  double* h2 = sm.h2;
+  const bool vec = (int)blockIdx.x < G;  // CTAs beyond G only join the barriers and the sums
+  const int chunk = (n + G - 1) / G, i0 = vec ? blockIdx.x * chunk : n;
   const int i1 = i0 + chunk < n ? i0 + chunk : n;
   double* w = V + (size_t)(col + 1) * n;
   const int nk = col + 2;  // col+1 dots and ||w||^2
-  mc_dots(V, w, n, nk, i0, i1, part, G);
+  if (vec) mc_dots(V, w, n, nk, i0, i1, part, G);
   grid.sync();
   sum_partials(part, G, nk, hs);
   __syncthreads();
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   grid.sync();  // every CTA has read the first-pass partials
-  mc_dots(V, w, n, nk, i0, i1, part, G);
+  if (vec) mc_dots(V, w, n, nk, i0, i1, part, G);
   grid.sync();
   sum_partials(part, G, nk, h2);
   __syncthreads();
@@ -214,20 +214,19 @@ __global__ void __launch_bounds__(kThreads)
     ww = fma(x, x, ww);
   }
   for (int o = 16; o > 0; o >>= 1) ww += __shfl_xor_sync(0xffffffffu, ww, o);
-  __shared__ double red[32];
+  double* red = sm.red;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) red[warp] = ww;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && vec) {
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
     part[(size_t)(kMaxRestart + 2) * G + blockIdx.x] = t;
   }
   grid.sync();
-  __shared__ double sw1[1];
-  sum_partials(part + (size_t)(kMaxRestart + 2) * G, G, 1, sw1);
+  sum_partials(part + (size_t)(kMaxRestart + 2) * G, G, 1, sm.sw1);
   __syncthreads();
-  const double sww = sw1[0];
+  const double sww = sm.sw1[0];
   const double h0 = sqrt(hs[nk - 1]);
   const double h1 = sqrt(sww);
   const bool brk = h1 <= DBL_EPSILON * h0;
@@ -445,6 +444,64 @@ __global__ void __launch_bounds__(kPcgThreads, 2)
   }
 }
 
+// The column loop of one GMRES cycle as ONE cooperative kernel: for each
+// column the matvec V[col + 1] = A V[col] (the GEMM program, built for column
+// 0 and shifted by col * n in a shared-memory copy), then the Arnoldi step —
+// CGS2 over the first a.G CTAs, or scipy's modified Gram-Schmidt on CTA 0 for
+// small systems — whose state update (Givens rotation, convergence) ends the
+// loop grid-wide through st->active.  With an empty program the kernel runs
+// the Arnoldi step of ONE column after a matvec launched before it.
+struct GmresArgs {
+  GmState* st;
+  double* V;
+  double* part;
+  int n, G, restart;
+  int col0, ncol;  // columns col0 .. col0 + ncol - 1
+};
+
+template <bool WIDE>
+__global__ void __launch_bounds__(kPcgThreads, 2)
+    gmres_cols_kernel(const __grid_constant__ GemmProgram prog, const GmresArgs a) {
+  extern __shared__ __align__(16) double gemm_smem[];
+  __shared__ GemmProgram sp;
+  __shared__ ArnoldiSmem sm;
+  cg::grid_group grid = cg::this_grid();
+  GmState* st = a.st;
+  if (!st->active) return;  // uniform: written only after a grid barrier of this launch
+  static_assert(sizeof(GemmProgram) % 8 == 0, "GemmProgram copied in 8-byte words");
+  if (prog.nstage > 0) {
+    const long long* src = reinterpret_cast<const long long*>(&prog);
+    long long* dst = reinterpret_cast<long long*>(&sp);
+    for (int i = threadIdx.x; i < (int)(sizeof(GemmProgram) / 8); i += blockDim.x) dst[i] = src[i];
+  }
+  const double* lo = a.V;                      // the program reads V[0] and writes V[1]:
+  const double* hi = a.V + 2 * (size_t)a.n;    // operands in [lo, hi) move with the column
+  for (int col = a.col0; col < a.col0 + a.ncol; ++col) {
+    if (prog.nstage > 0) {
+      __syncthreads();
+      if ((int)threadIdx.x < prog.nprob) {
+        const GemmProb& g = prog.p[threadIdx.x];
+        const size_t off = (size_t)col * a.n;
+        GemmProb& t = sp.p[threadIdx.x];
+        t.A = (g.A >= lo && g.A < hi) ? g.A + off : g.A;
+        t.B = (g.B >= lo && g.B < hi) ? g.B + off : g.B;
+        t.C = (g.C >= lo && g.C < hi) ? g.C + off : g.C;
+      }
+      __syncthreads();
+      gemm_device::gemm_program_run<WIDE>(sp, gemm_smem, grid);
+      grid.sync();
+    }
+    if (a.G > 1)
+      gm_arnoldi_grid(st, a.V, a.n, col, a.part, a.G, grid, sm);
+    else if (blockIdx.x == 0)
+      gm_arnoldi_cta(st, a.V, a.n, col, a.restart, sm.red);
+    if (col + 1 < a.col0 + a.ncol) {
+      grid.sync();  // CTA 0's state update is visible
+      if (!__ldcg(&st->active)) break;
+    }
+  }
+}
+
 template <class T>
 T read_state(const T* d) {
   T h;
@@ -456,7 +513,7 @@ int read_flag(const int* d) { return read_state<int>(d); }
 
 }  // namespace
 
-int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int restart,
+int gmres(const ProgramBuilder& A, int n, const double* b, double* x, double rtol, int restart,
           int maxiter) {
   const double bnrm2 = dnrm2(b, n);
   const double atol = rtol * bnrm2;  // scipy: max(atol=0, rtol*||b||)
@@ -469,35 +526,61 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
   double* V = allocator().alloc((size_t)(restart + 1) * n);
   double* r = allocator().alloc(n);
   GmState* st = reinterpret_cast<GmState*>(allocator().alloc(sizeof(GmState) / sizeof(double) + 1));
-  // multi-CTA Arnoldi once each CTA gets >= 512 entries
-  int G = n / 512;
-  if (G > kCgMaxCtas) G = kCgMaxCtas;
-  // cooperative grid: no more CTAs than co-reside on this context's SMs (an
-  // SM partition has fewer than the device's 148)
-  {
-    const int cap = num_sms() * occupancy((const void*)gm_arnoldi_mc_kernel, kThreads, 0);
-    if (G > cap) G = cap;
-  }
-  if (sm_budget() > 0 && G > sm_budget()) G = sm_budget();
-  if (G < 1) G = 1;
   double* part = allocator().alloc((size_t)(kMaxRestart + 3) * kCgMaxCtas);
+  auto release = [&]() {
+    allocator().release(V);
+    allocator().release(r);
+    allocator().release(part);
+    allocator().release(reinterpret_cast<double*>(st));
+  };
   auto residual = [&]() {  // r = b - A x, returns ||r||
-    A(x, r, nullptr);
+    GemmBatch gb;
+    A(gb, x, r);
+    gb.run();
     daxpby(1.0, b, -1.0, r, n);
     return dnrm2(r, n);
   };
   double rnorm = residual();
   int inner = 0;
-  // host polls of the device convergence flag (each one drains the stream);
-  // iterations past convergence are no-ops on the device (guarded)
-  constexpr int poll = 16;  // host convergence poll interval (iterations)
   if (rnorm < atol) {
-    allocator().release(V);
-    allocator().release(r);
-    allocator().release(part);
-    allocator().release(reinterpret_cast<double*>(st));
+    release();
     return 0;
   }
+  // the matvec V[1] = A V[0] as one program inside the column kernel, which
+  // shifts it from column to column; T2S2_KRYLOV_EXTERNAL_MATVEC=1 (tests: same
+  // bits either way) launches it separately as operators beyond one program do
+  GemmBatch gbq;
+  A(gbq, V, V + n);
+  GemmProgram prog{};
+  bool wide = false;
+  int max_tiles = 0;
+  double mv_flops = 0.0;
+  static const bool external = getenv("T2S2_KRYLOV_EXTERNAL_MATVEC") != nullptr;
+  const bool fused = !external && gbq.build_program(prog, wide, max_tiles, mv_flops);
+  if (!fused) prog = GemmProgram{};
+  const void* kern = wide ? (const void*)gmres_cols_kernel<true> : (const void*)gmres_cols_kernel<false>;
+  const int smem = gemm_program_smem(wide);
+  max_dynamic_smem(kern, smem);
+  // cooperative grid: no more CTAs than co-reside on this context's SMs (an
+  // SM partition has fewer than the device's 148); multi-CTA Arnoldi (CGS2)
+  // once each CTA gets >= 512 entries, on the first G CTAs of the grid
+  int cap = num_sms() * occupancy(kern, kPcgThreads, smem);
+  if (sm_budget() > 0 && cap > sm_budget()) cap = sm_budget();
+  int G = n / 512;
+  if (G > kCgMaxCtas) G = kCgMaxCtas;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  int grid = fused && max_tiles > G ? max_tiles : G;
+  if (grid > cap) grid = cap;
+  GmresArgs ga{st, V, part, n, G, restart, 0, restart};
+  auto launch = [&](int col0, int ncol) {
+    ga.col0 = col0;
+    ga.ncol = ncol;
+    void* params[] = {&prog, &ga};
+    LaunchScope ls("gmres", 0.0, 0.0);
+    T2S2_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kPcgThreads), params, smem, stream()));
+  };
+  constexpr int poll = 16;  // external matvec: host poll interval of the convergence flag
   double ptol_max_factor = 1.0;
   double ptol = bnrm2 * std::fmin(ptol_max_factor, atol / bnrm2);
   for (int it = 0; it < maxiter; ++it) {
@@ -507,22 +590,19 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
       gm_set_restart<<<1, 1, 0, stream()>>>(st, restart);
     }
     T2S2_CHECK_LAUNCH();
-    for (int col = 0; col < restart; ++col) {
-      if (col > 0 && col % poll == 0 && !read_flag(&st->active)) break;
-      A(V + (size_t)col * n, V + (size_t)(col + 1) * n, &st->active);  // skipped once converged
-      {
-        LaunchScope ls("gmres", 8.0 * n * (col + 2), 32.0 * n * (col + 2));
-        if (G > 1) {
-          int c = col;
-          int nn = n;
-          void* params[] = {&st, &V, &nn, &c, &part};
-          T2S2_CUDA(cudaLaunchCooperativeKernel((void*)gm_arnoldi_mc_kernel, dim3(G),
-                                                dim3(kThreads), params, 0, stream()));
-        } else {
-          gm_arnoldi_kernel<<<1, kThreads, 0, stream()>>>(st, V, n, col, restart);
-        }
-      }
+    if (fused) {
+      launch(0, restart);
       T2S2_CHECK_LAUNCH();
+    } else {
+      for (int col = 0; col < restart; ++col) {
+        if (col > 0 && col % poll == 0 && !read_flag(&st->active)) break;
+        GemmBatch gb;  // skipped on the device once converged
+        gb.set_guard(&st->active);
+        A(gb, V + (size_t)col * n, V + (size_t)(col + 1) * n);
+        gb.run();
+        launch(col, 1);
+        T2S2_CHECK_LAUNCH();
+      }
     }
     {
       LaunchScope ls("gmres", 2.0*n*restart, 8.0*n*restart);
@@ -530,7 +610,12 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
     }
     T2S2_CHECK_LAUNCH();
     GmState h = read_state<GmState>(st);
-    inner += h.col_final + 1;
+    const int cols = h.col_final + 1;
+    inner += cols;
+    // the work of the columns performed (known only now): matvecs inside the
+    // kernel, and 8 n flops per basis vector and column for CGS2
+    amend_work("gmres", (fused ? cols * mv_flops : 0.0) + 4.0 * n * cols * (cols + 3.0),
+               16.0 * n * cols * (cols + 3.0));
     const double presid = h.presid;
     rnorm = residual();
     if (rnorm <= atol) break;
@@ -541,10 +626,7 @@ int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int r
       ptol_max_factor = std::fmin(1.0, 1.5 * ptol_max_factor);
     ptol = presid * std::fmin(ptol_max_factor, atol / rnorm);
   }
-  allocator().release(V);
-  allocator().release(r);
-  allocator().release(part);
-  allocator().release(reinterpret_cast<double*>(st));
+  release();
   return inner;
 }
 
@@ -570,7 +652,7 @@ int pcg(const ProgramBuilder& A, int n, const double* b, double* x, const double
   daxpby(1.0, b, -1.0, r, n);
   CgState init{0.0, 1, 0};
   T2S2_CUDA(cudaMemcpyAsync(st, &init, sizeof(CgState), cudaMemcpyHostToDevice, stream()));
-  // the matvec q = A p as one program inside the kernel; T2S2_PCG_EXTERNAL_MATVEC=1
+  // the matvec q = A p as one program inside the kernel; T2S2_KRYLOV_EXTERNAL_MATVEC=1
   // (tests: same bits either way) launches it separately as operators
   // beyond one program do
   GemmBatch gbq;
@@ -579,7 +661,7 @@ int pcg(const ProgramBuilder& A, int n, const double* b, double* x, const double
   bool wide = false;
   int max_tiles = 0;
   double mv_flops = 0.0;
-  static const bool external = getenv("T2S2_PCG_EXTERNAL_MATVEC") != nullptr;
+  static const bool external = getenv("T2S2_KRYLOV_EXTERNAL_MATVEC") != nullptr;
   const bool fused = !external && gbq.build_program(prog, wide, max_tiles, mv_flops);
   if (!fused) prog = GemmProgram{};
   const void* kern = wide ? (const void*)pcg_kernel<true> : (const void*)pcg_kernel<false>;

@@ -5,8 +5,7 @@
 // The Krylov recurrences follow scipy 1.18's pure-Python implementations
 // (modified Gram-Schmidt Arnoldi with LAPACK-style Givens rotations and the
 // gh-8400 inner-tolerance control; textbook PCG), with every vector and
-// scalar resident on the device.  GMRES: the host polls a convergence flag
-// every few iterations; PCG: the loop runs on the device.
+// scalar resident on the device; the iteration loops run on the device.
 #pragma once
 
 #include <functional>
@@ -16,19 +15,18 @@
 
 namespace t2s2 {
 
-// out = A in.  guard (device int, may be null): when it reads 0 on the
-// device the application is skipped (a Krylov loop that converged between
-// two host polls does not pay for its trailing matvecs).
-using MatVec = std::function<void(const double* in, double* out, const int* guard)>;
+// Adds the problems of out = A in to a GEMM batch (stages from 0).  The
+// solvers run the matvec as a program inside their own kernels; an operator
+// whose matvec does not fit one program gets it as a separate launch per
+// iteration, skipped on the device once the loop has converged.
+using ProgramBuilder = std::function<void(GemmBatch& gb, const double* in, double* out)>;
 
 // x (device, length n) is the initial guess and receives the result.
 // rtol relative to ||b|| (scipy's atol = rtol * ||b||).  Returns inner
-// iterations performed.
-int gmres(const MatVec& A, int n, const double* b, double* x, double rtol, int restart,
+// iterations performed.  One cooperative kernel per restart cycle (the
+// column loop with matvec and Arnoldi step); the host runs the restart logic.
+int gmres(const ProgramBuilder& A, int n, const double* b, double* x, double rtol, int restart,
           int maxiter);
-
-// Adds the problems of out = A in to a GEMM batch (stages from 0).
-using ProgramBuilder = std::function<void(GemmBatch& gb, const double* in, double* out)>;
 
 // Preconditioner M = diag^{-1}.  The whole iteration loop is one cooperative
 // kernel with the matvec program inside it.

@@ -66,6 +66,15 @@ def main(first=4, count=20):
                      "total_ms": float(np.sum(v))})
         print(f"  {name:12s} N={n:5d} x{len(v):4d} avg {1e3 * np.mean(v):8.1f} us "
               f"total {np.sum(v):8.3f} ms")
+    # GEMM programs by duration class
+    g = [ms for name, fl, by, ms in recs if name == "gemm"]
+    if g:
+        g = np.array(g) * 1e3
+        print("gemm programs by event-timed duration (us): count, total ms")
+        edges = [0, 6, 8, 10, 15, 20, 30, 50, 100, 1e9]
+        for lo, hi in zip(edges[:-1], edges[1:]):
+            m = (g >= lo) & (g < hi)
+            print(f"  [{lo:5.0f}, {hi:5.0f})  x{int(m.sum()):5d}  {g[m].sum() / 1e3:8.3f} ms")
     out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "solve_sizes.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     json.dump({"steps": count, "first": first, "families": dict(fam), "solves": rows},
