@@ -1,4 +1,4 @@
-"""Determinism stress test of the dense local solve (development helper):
+"""Determinism stress test of the no-pivot Gauss-Jordan solve (diagonally dominant systems; DET_SIZES="1953 2000" are the sizes that exposed the hand-off race fixed in round 2):
 the same systems solved repeatedly must give bit-identical results."""
 import os
 import sys
