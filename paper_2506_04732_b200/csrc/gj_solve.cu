@@ -658,6 +658,14 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
     a.prof[cta * 4 + (slot)] += tq - tp;       \
     tp = tq;                                   \
   }
+#ifdef GJ_TIMELINE
+  // development timeline (tools/micro/gj_timeline.cu): globaltimer stamps of a few CTAs per phase
+  const int tl_slot = cta == 0 ? 0 : cta == 1 ? 1 : cta == 5 ? 2 : cta == G / 2 ? 3 : cta == G - 1 ? 4 : -1;
+#define GJ_TL(k) \
+  if (a.prof && tid == 0 && tl_slot >= 0) a.prof[((size_t)tl_slot * 128 + p) * 4 + (k)] = gtimer();
+#else
+#define GJ_TL(k)
+#endif
   unsigned* arrivals = a.sync;   // tile workers: G - 1 per phase with a next diagonal block, G in the last
   unsigned* published = a.sync + 1;  // D_0^{-1} .. published by CTA 0
   unsigned* feed = a.sync + 2;   // feed[p]: finished feeder tasks of phase p
@@ -695,21 +703,28 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       // wait only for the feeders of phase p - 1, then the next diagonal
       // block: W of its columns, multipliers checked, updated block kept in
       // shared memory, factored
+      GJ_TL(0)
       if (p > 0) cta_wait(feed + (p - 1), (unsigned)nfeed(Phase(N, p - 1)), a.info, true);
+      GJ_TL(1)
       if (__ldcg(a.info) == 0) {
         special_tile(a, ph, s);
+        GJ_TL(2)
         unsigned long long td = pr ? gtimer() : 0;
         gj_diag(a, p + 1, ph.kb2, s);
         if (pr) a.prof[9] += gtimer() - td;
       }
+      GJ_TL(3)
       cta_signal(published);  // D_{p+1}^{-1} (also when skipped)
     } else {
       // every tile worker has finished the earlier phases (all of them had a
       // next diagonal block: G - 1 workers each) and D_p^{-1} is published
+      GJ_TL(0)
       if (G > 1) {
         cta_wait(arrivals, (unsigned)(G - 1) * (unsigned)p, a.info, false);
+        GJ_TL(1)
         cta_wait(published, (unsigned)p + 1u, a.info, false);
       }
+      GJ_TL(2)
       const bool live = __ldcg(a.info) == 0;
       if (has_diag && G == 1 && live) {
         special_tile(a, ph, s);
@@ -758,6 +773,7 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
         }
       }
       __syncthreads();
+      GJ_TL(3)
       if (G > 1) cta_signal(arrivals);
     }
     GJ_PHASE(0)
