@@ -11,6 +11,9 @@ from paper_2506_04732_b200 import _native  # noqa: E402
 if os.environ.get('T2S2_LIB'):
     _native.load_library(os.environ['T2S2_LIB'])
 
+if os.environ.get('BUDGET'):
+    _native.context()
+    _native.set_thread_sm_budget(int(os.environ['BUDGET']))
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 rng = np.random.default_rng(3)
 for n in [int(x) for x in os.environ.get('DET_SIZES', '66 264 792 1188 1848').split()]:
