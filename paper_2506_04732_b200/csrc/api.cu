@@ -2,6 +2,7 @@
 // upload/download and the hot-path entry points.
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -46,6 +47,12 @@ struct t2s2_context {
   size_t pool_used = 0;
   std::vector<t2s2::Pending> pending;
   std::vector<t2s2_launch_record> launch_log;  // per launch while profiling
+  // pinned staging buffer of host_read: a device->host copy into pinned
+  // memory is one DMA, into pageable memory a staged copy with a driver-side
+  // wait (measured per read in DESIGN.md section 8)
+  void* pinned = nullptr;
+  static constexpr size_t kPinnedBytes = 64 * 1024;
+  unsigned read_ticket = 0;  // last ticket published into the word after the staging buffer
   // host_read trace: 0 off, 1 record, 2 replay
   int trace_mode = 0;
   std::vector<std::vector<unsigned char>> trace;
@@ -186,6 +193,19 @@ bool profiling() { return g_ctx->profiling; }
 
 bool replaying_reads() { return g_ctx->trace_mode == 2; }
 
+// A steering read without the copy engine: one small kernel copies the words
+// into mapped pinned host memory and then raises a ticket the host spins on
+// (system-scope fence between data and ticket).  The host-visible latency is
+// the kernel's launch slot plus a PCIe posted write instead of a copy-engine
+// transfer and a stream synchronisation.
+__global__ void publish_kernel(const unsigned* __restrict__ src, unsigned* dst, int n_words,
+                               volatile unsigned* ticket, unsigned value) {
+  for (int i = threadIdx.x; i < n_words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = value;
+}
+
 void host_read(void* host, const void* dev, size_t bytes) {
   t2s2_context* c = g_ctx;
   if (c->trace_mode == 2) {
@@ -194,8 +214,37 @@ void host_read(void* host, const void* dev, size_t bytes) {
     std::memcpy(host, c->trace[c->trace_pos++].data(), bytes);
     return;
   }
-  if (bytes) T2S2_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
-  T2S2_CUDA(cudaStreamSynchronize(c->stream));
+  if (bytes && bytes <= t2s2_context::kPinnedBytes && bytes % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(dev) % 4 == 0) {
+    if (!c->pinned) {
+      T2S2_CUDA(cudaHostAlloc(&c->pinned, t2s2_context::kPinnedBytes + 64, cudaHostAllocMapped));
+      std::memset(c->pinned, 0, t2s2_context::kPinnedBytes + 64);
+    }
+    volatile unsigned* ticket =
+        reinterpret_cast<volatile unsigned*>(static_cast<char*>(c->pinned) + t2s2_context::kPinnedBytes);
+    const unsigned value = ++c->read_ticket;
+    const int words = (int)(bytes / 4);
+    {
+      LaunchScope ls("host_read", 0.0, 2.0 * bytes);
+      publish_kernel<<<1, words < 256 ? 32 * ((words + 31) / 32) : 256, 0, c->stream>>>(
+          static_cast<const unsigned*>(dev), static_cast<unsigned*>(c->pinned), words, ticket, value);
+    }
+    T2S2_CHECK_LAUNCH();
+    // spin on the ticket; a faulted or finished stream without the ticket is an error
+    for (unsigned long long spins = 0; *ticket != value; ++spins) {
+      if ((spins & 0xfffff) == 0xfffff) {
+        const cudaError_t q = cudaStreamQuery(c->stream);
+        if (q != cudaErrorNotReady && *ticket != value) {
+          T2S2_CUDA(q);
+          T2S2_REQUIRE(*ticket == value, kErrCuda, "host_read: the stream drained without the ticket");
+        }
+      }
+    }
+    std::memcpy(host, c->pinned, bytes);
+  } else {
+    if (bytes) T2S2_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    T2S2_CUDA(cudaStreamSynchronize(c->stream));
+  }
   if (c->trace_mode == 1) {
     const unsigned char* b = static_cast<const unsigned char*>(host);
     c->trace.emplace_back(b, b + bytes);
@@ -381,6 +430,7 @@ void t2s2_context_destroy(t2s2_context* ctx) {
   ctx->alloc.trim();
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

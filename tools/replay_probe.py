@@ -45,8 +45,11 @@ for k in range(steps):
         nxt, _, _, _ = timed(k, state)
         state = nxt
         continue
-    _native.read_trace(1)
-    a, row, ms_sync, host_sync = timed(k, state)
+    _native.read_trace(1)  # record (the determinism probes' buffers join the trace: not timed)
+    r, _, _, _ = timed(k, state)
+    r.free()
+    _native.read_trace(0)
+    a, row, ms_sync, host_sync = timed(k, state)  # the plain, synchronising run
     nreads = _native.read_trace(2)
     b, _, ms_free, host_free = timed(k, state)
     _native.read_trace(0)
@@ -54,7 +57,7 @@ for k in range(steps):
     same = all(np.array_equal(x, y) for x, y in zip(ca, cb))
     tot[0] += ms_sync
     tot[1] += ms_free
-    print(f"step {k+1}: sweeps {row[4]} reads {nreads}  synchronising {ms_sync:7.2f} ms  "
+    print(f"step {k+1}: sweeps {row[4]} trace entries {nreads}  synchronising {ms_sync:7.2f} ms  "
           f"read-free {ms_free:7.2f} ms (host enqueue {host_free:6.2f} ms)  identical {same}", flush=True)
     state = a
 print(f"steps {first}..{steps}: synchronising {tot[0]:.1f} ms, read-free {tot[1]:.1f} ms, ratio {tot[0]/tot[1]:.3f}")
