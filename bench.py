@@ -20,6 +20,10 @@ solves/s, weak scaling.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload march|sweep]
 
+Defaults: 3 warm-up steps, then steps 4..23 of the config-2 march timed
+(--steps 97: the whole 100-step march); 16 solves after 1 warm-up solve for
+the sweep.
+
 --impl b200 (default): the CUDA engine through its C ABI.  One JSON line with
 value (inputs resident in HBM), e2e (public API with pinned host buffers:
 per-step H2D of the step's inputs, D2H of its result), the roofline of the
@@ -54,8 +58,10 @@ SWEEP = dict(metric="steady_solves_per_s", unit="solves/s", index=4)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps; default 20 (march: steps 4..23; --steps 97 times the rest "
+                         "of BASELINE config 2's 100-step march), 16 solves (sweep)")
+    ap.add_argument("--warmup", type=int, default=None, help="default 3 (march), 1 (sweep)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="march", choices=["march", "sweep"])
     ap.add_argument("--sweep-sweeps", type=int, default=6,
@@ -67,7 +73,12 @@ def parse():
                          "1e-10); 1e-12 reads BASELINE's 'TT tolerance' as the residual target")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.warmup is None:
+        args.warmup = 3 if args.workload == "march" else 1
+    if args.steps is None:
+        args.steps = 20 if args.workload == "march" else 16
+    return args
 
 
 def march_config(recipe, extra=None):
