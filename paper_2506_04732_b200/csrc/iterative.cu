@@ -91,15 +91,72 @@ __global__ void __launch_bounds__(kThreads)
 
 __global__ void gm_set_restart(GmState* st, int restart) { st->restart = restart; }
 
+// CTA 0's copy of the cycle's rotations and right-hand side (GmState gc, gs,
+// S) and the Hessenberg column being finished.  The column update is a
+// chain of dependent reads of what the previous iteration wrote: run against
+// global memory every link was an L2 round trip (~20 us for column 40,
+// most of the Arnoldi step); here it runs in shared memory and global memory
+// only receives the results.
+struct RotSmem {
+  double gc[kMaxRestart], gs[kMaxRestart], S[kMaxRestart + 1], hc[kMaxRestart + 2];
+};
+
+// thread 0 of CTA 0: load the rotations of the columns before col0
+__device__ void rot_load(const GmState* st, RotSmem& r, int col0) {
+  for (int k = threadIdx.x; k < col0; k += blockDim.x) {
+    r.gc[k] = st->gc[k];
+    r.gs[k] = st->gs[k];
+  }
+  for (int k = threadIdx.x; k <= col0; k += blockDim.x) r.S[k] = st->S[k];
+  __syncthreads();
+}
+
+// one thread: r.hc[0..col] = the new column's projections, h1 = ||w|| after
+// orthogonalisation; previous rotations applied, the new one formed (LAPACK
+// dlartg), S advanced, convergence / breakdown / last column recorded
+__device__ void finish_column(GmState* st, RotSmem& r, int col, double h1, bool brk, int restart) {
+  double* hc = r.hc;
+  hc[col + 1] = brk ? 0.0 : h1;
+  for (int k = 0; k < col; ++k) {
+    const double c = r.gc[k], s = r.gs[k];
+    const double n0 = hc[k], n1 = hc[k + 1];
+    hc[k] = c * n0 + s * n1;
+    hc[k + 1] = -s * n0 + c * n1;
+  }
+  double c, s, mag;
+  lartg(hc[col], hc[col + 1], c, s, mag);
+  r.gc[col] = c;
+  r.gs[col] = s;
+  hc[col] = mag;
+  hc[col + 1] = 0.0;
+  const double t = -s * r.S[col];
+  r.S[col] = c * r.S[col];
+  r.S[col + 1] = t;
+  // results to global memory (stores only)
+  double* gh = st->h[col];
+  for (int k = 0; k <= col + 1; ++k) gh[k] = hc[k];
+  st->gc[col] = c;
+  st->gs[col] = s;
+  st->S[col] = r.S[col];
+  st->S[col + 1] = t;
+  st->presid = fabs(t);
+  if (brk) st->breakdown = 1;
+  if (fabs(t) <= st->ptol || brk || col == restart - 1) {
+    st->active = 0;
+    st->col_final = col;
+  }
+}
+
 // Arnoldi step for column col (w = A v_col already in V[col+1]) on one CTA:
 // modified Gram-Schmidt as scipy's loop (small systems).
-__device__ void gm_arnoldi_cta(GmState* st, double* V, int n, int col, int restart, double* red) {
+__device__ void gm_arnoldi_cta(GmState* st, double* V, int n, int col, int restart, double* red,
+                               RotSmem& rot) {
   double* w = V + (size_t)(col + 1) * n;
   const double h0 = sqrt(cta_dot(w, w, n, red));
   for (int k = 0; k <= col; ++k) {
     const double* vk = V + (size_t)k * n;
     const double t = cta_dot(vk, w, n, red);
-    if (threadIdx.x == 0) st->h[col][k] = t;
+    if (threadIdx.x == 0) rot.hc[k] = t;
     for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = fma(-t, vk[i], w[i]);
     __syncthreads();
   }
@@ -109,31 +166,7 @@ __device__ void gm_arnoldi_cta(GmState* st, double* V, int n, int col, int resta
     const double inv = 1.0 / h1;
     for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] *= inv;
   }
-  if (threadIdx.x == 0) {
-    double* hc = st->h[col];
-    hc[col + 1] = brk ? 0.0 : h1;
-    if (brk) st->breakdown = 1;
-    for (int k = 0; k < col; ++k) {
-      const double c = st->gc[k], s = st->gs[k];
-      const double n0 = hc[k], n1 = hc[k + 1];
-      hc[k] = c * n0 + s * n1;
-      hc[k + 1] = -s * n0 + c * n1;
-    }
-    double c, s, mag;
-    lartg(hc[col], hc[col + 1], c, s, mag);
-    st->gc[col] = c;
-    st->gs[col] = s;
-    hc[col] = mag;
-    hc[col + 1] = 0.0;
-    const double t = -s * st->S[col];
-    st->S[col] = c * st->S[col];
-    st->S[col + 1] = t;
-    st->presid = fabs(t);
-    if (st->presid <= st->ptol || brk || col == restart - 1) {
-      st->active = 0;
-      st->col_final = col;
-    }
-  }
+  if (threadIdx.x == 0) finish_column(st, rot, col, h1, brk, restart);
 }
 
 // Arnoldi step over G CTAs (cooperative): classical Gram-Schmidt applied
@@ -141,41 +174,52 @@ __device__ void gm_arnoldi_cta(GmState* st, double* V, int n, int col, int resta
 // precision) so the column costs three grid barriers instead of one CTA-wide
 // reduction per basis vector.  Dots: per-CTA partials (warp per basis
 // vector), every CTA sums them in the same order.
-__device__ void mc_dots(const double* V, const double* w, int n, int nk, int i0, int i1,
-                        double* part, int G) {
+// vb(k): this CTA's chunk (len entries) of basis vector k; wl: its chunk of w.
+template <class BasisChunk>
+__device__ void mc_dots(const BasisChunk& vb, const double* wl, int len, int nk, double* part, int G) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = warp; k < nk; k += nw) {
-    const double* v = k < nk - 1 ? V + (size_t)k * n : w;  // last: ||w||^2
+    const double* v = k < nk - 1 ? vb(k) : wl;  // last: ||w||^2
     double acc = 0.0;
-    for (int i = i0 + lane; i < i1; i += 32) acc = fma(v[i], w[i], acc);
+    for (int j = lane; j < len; j += 32) acc = fma(v[j], wl[j], acc);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) part[(size_t)k * G + blockIdx.x] = acc;
   }
 }
 
-// out[k] = sum_c part[k * G + c] for k < nk, added in the order c = 0, 1,
-// ..., G - 1 (every CTA the same bits, and the bits of a plain serial loop),
-// but without a chain of G dependent L2 round trips: warp w takes rows
-// k = w, w + nw, ...; its lanes load the row's partials at once (lane l holds
-// c = l, l + 32, ...) and the sum walks them through shuffles in order.
+// out[k] = sum_c part[k * G + c] for k < nk in a fixed order (every CTA the
+// same bits): warp w takes rows k = w, w + nw, ...; lane l adds the partials
+// c = l, l + 32, ... in that order, then the lanes combine by a butterfly.
+// All loads of a warp's rows are issued before the first sum, so a call
+// costs one L2 round trip plus five shuffle steps per row (an ordered walk
+// over G partials per row made the Arnoldi step of a 40-column cycle spend
+// more time summing than orthogonalising).
 constexpr int kMaxPartialsPerLane = (kCgMaxCtas + 31) / 32;
+constexpr int kMaxRowsPerWarp = (kMaxRestart + 2 + 7) / 8;  // 8 warps per CTA
 __device__ __forceinline__ void sum_partials(const double* part, int G, int nk, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = warp; k < nk; k += nw) {
-    double v[kMaxPartialsPerLane];
+  double v[kMaxRowsPerWarp];
 #pragma unroll
-    for (int j = 0; j < kMaxPartialsPerLane; ++j) {
-      const int c = lane + 32 * j;
-      v[j] = c < G ? __ldcg(part + (size_t)k * G + c) : 0.0;
-    }
+  for (int r = 0; r < kMaxRowsPerWarp; ++r) {
+    const int k = warp + r * nw;
     double t = 0.0;
+    if (k < nk) {
 #pragma unroll
-    for (int j = 0; j < kMaxPartialsPerLane; ++j) {
-      // only the lanes that hold a partial are walked (G is uniform)
-      const int m = G - 32 * j < 32 ? G - 32 * j : 32;
-      for (int l = 0; l < m; ++l) t += __shfl_sync(0xffffffffu, v[j], l);
+      for (int j = 0; j < kMaxPartialsPerLane; ++j) {
+        const int c = lane + 32 * j;
+        if (c < G) t += __ldcg(part + (size_t)k * G + c);
+      }
     }
-    if (lane == 0) out[k] = t;
+    v[r] = t;
+  }
+#pragma unroll
+  for (int r = 0; r < kMaxRowsPerWarp; ++r) {
+    const int k = warp + r * nw;
+    if (k < nk) {  // uniform over the warp
+      double t = v[r];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) out[k] = t;
+    }
   }
 }
 
@@ -183,35 +227,51 @@ struct ArnoldiSmem {
   double hs[kMaxRestart + 2], h2[kMaxRestart + 2], red[33], sw1[1];
 };
 __device__ void gm_arnoldi_grid(GmState* st, double* V, int n, int col, double* part, int G,
-                                cg::grid_group& grid, ArnoldiSmem& sm) {
+                                cg::grid_group& grid, ArnoldiSmem& sm, RotSmem& rot, double* Vs, int stride) {
+  // Vs (may be null): this CTA's chunk of every basis vector, resident in
+  // shared memory for the whole cycle (slot k at Vs + k * stride, slots
+  // 0..col loaded, slot col + 1 receives w): the dots and updates of CGS2
+  // then read shared memory instead of col + 1 rows of V from L2, twice.
   double* hs = sm.hs;
   double* h2 = sm.h2;
-  const bool vec = (int)blockIdx.x < G;  // CTAs beyond G only join the barriers and the sums
+  const bool vec = (int)blockIdx.x < G;  // CTAs beyond G only join the barriers
   const int chunk = (n + G - 1) / G, i0 = vec ? blockIdx.x * chunk : n;
   const int i1 = i0 + chunk < n ? i0 + chunk : n;
+  const int len = i1 > i0 ? i1 - i0 : 0;
   double* w = V + (size_t)(col + 1) * n;
-  const int nk = col + 2;  // col+1 dots and ||w||^2
-  if (vec) mc_dots(V, w, n, nk, i0, i1, part, G);
-  grid.sync();
-  sum_partials(part, G, nk, hs);
-  __syncthreads();
-  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    double x = w[i];
-    for (int k = 0; k <= col; ++k) x = fma(-hs[k], V[(size_t)k * n + i], x);
-    w[i] = x;
+  double* wl = Vs ? Vs + (size_t)(col + 1) * stride : w + i0;  // this CTA's chunk of w
+  auto vb = [&](int k) -> const double* { return Vs ? Vs + (size_t)k * stride : V + (size_t)k * n + i0; };
+  if (Vs && vec) {
+    for (int j = threadIdx.x; j < len; j += blockDim.x) wl[j] = __ldcg(w + i0 + j);
+    __syncthreads();
   }
-  __syncthreads();
-  grid.sync();  // every CTA has read the first-pass partials
-  if (vec) mc_dots(V, w, n, nk, i0, i1, part, G);
+  const int nk = col + 2;  // col+1 dots and ||w||^2
+  // two partial buffers: the second pass may write while a slow CTA still sums the first
+  double* part2 = part + (size_t)(kMaxRestart + 3) * kCgMaxCtas;
+  if (vec) mc_dots(vb, wl, len, nk, part, G);
   grid.sync();
-  sum_partials(part, G, nk, h2);
-  __syncthreads();
+  if (vec) {
+    sum_partials(part, G, nk, hs);
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double x = wl[j];
+      for (int k = 0; k <= col; ++k) x = fma(-hs[k], vb(k)[j], x);
+      wl[j] = x;
+    }
+    __syncthreads();
+    mc_dots(vb, wl, len, nk, part2, G);
+  }
+  grid.sync();
   double ww = 0.0;
-  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    double x = w[i];
-    for (int k = 0; k <= col; ++k) x = fma(-h2[k], V[(size_t)k * n + i], x);
-    w[i] = x;
-    ww = fma(x, x, ww);
+  if (vec) {
+    sum_partials(part2, G, nk, h2);
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) {
+      double x = wl[j];
+      for (int k = 0; k <= col; ++k) x = fma(-h2[k], vb(k)[j], x);
+      wl[j] = x;
+      ww = fma(x, x, ww);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) ww += __shfl_xor_sync(0xffffffffu, ww, o);
   double* red = sm.red;
@@ -224,6 +284,7 @@ __device__ void gm_arnoldi_grid(GmState* st, double* V, int n, int col, double* 
     part[(size_t)(kMaxRestart + 2) * G + blockIdx.x] = t;
   }
   grid.sync();
+  if (!vec) return;
   sum_partials(part + (size_t)(kMaxRestart + 2) * G, G, 1, sm.sw1);
   __syncthreads();
   const double sww = sm.sw1[0];
@@ -232,33 +293,15 @@ __device__ void gm_arnoldi_grid(GmState* st, double* V, int n, int col, double* 
   const bool brk = h1 <= DBL_EPSILON * h0;
   if (!brk) {
     const double inv = 1.0 / h1;
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) w[i] *= inv;
+    for (int j = threadIdx.x; j < len; j += blockDim.x) wl[j] *= inv;
+  }
+  if (Vs) {  // the next matvec and the final update read V from global memory
+    __syncthreads();
+    for (int j = threadIdx.x; j < len; j += blockDim.x) w[i0 + j] = wl[j];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double* hc = st->h[col];
-    for (int k = 0; k <= col; ++k) hc[k] = hs[k] + h2[k];
-    hc[col + 1] = brk ? 0.0 : h1;
-    if (brk) st->breakdown = 1;
-    for (int k = 0; k < col; ++k) {
-      const double c = st->gc[k], sn = st->gs[k];
-      const double n0 = hc[k], n1 = hc[k + 1];
-      hc[k] = c * n0 + sn * n1;
-      hc[k + 1] = -sn * n0 + c * n1;
-    }
-    double c, sn, mag;
-    lartg(hc[col], hc[col + 1], c, sn, mag);
-    st->gc[col] = c;
-    st->gs[col] = sn;
-    hc[col] = mag;
-    hc[col + 1] = 0.0;
-    const double t = -sn * st->S[col];
-    st->S[col] = c * st->S[col];
-    st->S[col + 1] = t;
-    st->presid = fabs(t);
-    if (st->presid <= st->ptol || brk || col == st->restart - 1) {
-      st->active = 0;
-      st->col_final = col;
-    }
+    for (int k = 0; k <= col; ++k) rot.hc[k] = hs[k] + h2[k];
+    finish_column(st, rot, col, h1, brk, st->restart);
   }
 }
 
@@ -457,6 +500,10 @@ struct GmresArgs {
   double* part;
   int n, G, restart;
   int col0, ncol;  // columns col0 .. col0 + ncol - 1
+  // resident basis: each vector CTA keeps its chunk of V[0..restart] in
+  // shared memory behind the GEMM ring (vs_off doubles in), stride doubles
+  // per vector; stride == 0: the basis is read from global memory
+  int vs_off, stride;
 };
 
 template <bool WIDE>
@@ -465,6 +512,7 @@ __global__ void __launch_bounds__(kPcgThreads, 2)
   extern __shared__ __align__(16) double gemm_smem[];
   __shared__ GemmProgram sp;
   __shared__ ArnoldiSmem sm;
+  __shared__ RotSmem rot;
   cg::grid_group grid = cg::this_grid();
   GmState* st = a.st;
   if (!st->active) return;  // uniform: written only after a grid barrier of this launch
@@ -476,6 +524,16 @@ __global__ void __launch_bounds__(kPcgThreads, 2)
   }
   const double* lo = a.V;                      // the program reads V[0] and writes V[1]:
   const double* hi = a.V + 2 * (size_t)a.n;    // operands in [lo, hi) move with the column
+  if (blockIdx.x == 0) rot_load(st, rot, a.col0);
+  double* Vs = a.stride > 0 ? gemm_smem + a.vs_off : nullptr;
+  if (Vs && (int)blockIdx.x < a.G) {
+    // this CTA's chunk of the basis vectors that exist already
+    const int chunk = (a.n + a.G - 1) / a.G, i0 = blockIdx.x * chunk;
+    const int len = (i0 + chunk < a.n ? i0 + chunk : a.n) - i0;
+    for (int k = 0; k <= a.col0; ++k)
+      for (int j = threadIdx.x; j < len; j += blockDim.x)
+        Vs[(size_t)k * a.stride + j] = __ldcg(a.V + (size_t)k * a.n + i0 + j);
+  }
   for (int col = a.col0; col < a.col0 + a.ncol; ++col) {
     if (prog.nstage > 0) {
       __syncthreads();
@@ -492,9 +550,9 @@ __global__ void __launch_bounds__(kPcgThreads, 2)
       grid.sync();
     }
     if (a.G > 1)
-      gm_arnoldi_grid(st, a.V, a.n, col, a.part, a.G, grid, sm);
+      gm_arnoldi_grid(st, a.V, a.n, col, a.part, a.G, grid, sm, rot, Vs, a.stride);
     else if (blockIdx.x == 0)
-      gm_arnoldi_cta(st, a.V, a.n, col, a.restart, sm.red);
+      gm_arnoldi_cta(st, a.V, a.n, col, a.restart, sm.red, rot);
     if (col + 1 < a.col0 + a.ncol) {
       grid.sync();  // CTA 0's state update is visible
       if (!__ldcg(&st->active)) break;
@@ -526,7 +584,7 @@ int gmres(const ProgramBuilder& A, int n, const double* b, double* x, double rto
   double* V = allocator().alloc((size_t)(restart + 1) * n);
   double* r = allocator().alloc(n);
   GmState* st = reinterpret_cast<GmState*>(allocator().alloc(sizeof(GmState) / sizeof(double) + 1));
-  double* part = allocator().alloc((size_t)(kMaxRestart + 3) * kCgMaxCtas);
+  double* part = allocator().alloc((size_t)2 * (kMaxRestart + 3) * kCgMaxCtas);  // two CGS2 passes
   auto release = [&]() {
     allocator().release(V);
     allocator().release(r);
@@ -559,20 +617,46 @@ int gmres(const ProgramBuilder& A, int n, const double* b, double* x, double rto
   const bool fused = !external && gbq.build_program(prog, wide, max_tiles, mv_flops);
   if (!fused) prog = GemmProgram{};
   const void* kern = wide ? (const void*)gmres_cols_kernel<true> : (const void*)gmres_cols_kernel<false>;
-  const int smem = gemm_program_smem(wide);
+  const int ring = gemm_program_smem(wide);
+  // Vector CTAs.  Below 1024 unknowns one CTA runs scipy's modified
+  // Gram-Schmidt.  Otherwise CGS2 over G CTAs, each with a chunk of at most
+  // kResidentChunk entries of every basis vector resident in shared memory
+  // when G such CTAs co-reside on this context's SMs (an SM partition has
+  // fewer than the device's 148); larger systems read the basis from global
+  // memory in chunks of >= 512.  The chunking is the same whether the matvec
+  // runs inside the kernel or not (same bits), residency needs the loop kernel.
+  constexpr int kResidentChunk = 320;
+  int G = 1, stride = 0, smem = ring;
+  if (n >= 1024) {
+    const int g_res = (n + kResidentChunk - 1) / kResidentChunk;
+    const int st_res = ((n + g_res - 1) / g_res + 1) & ~1;
+    const int smem_res = ring + (restart + 1) * st_res * (int)sizeof(double);
+    max_dynamic_smem(kern, smem_res);
+    int cap_res = num_sms() * occupancy(kern, kPcgThreads, smem_res);
+    if (sm_budget() > 0 && cap_res > sm_budget()) cap_res = sm_budget();
+    if (g_res <= kCgMaxCtas && g_res <= cap_res) {
+      G = g_res;
+      // not on an SM partition: a green context refuses the cooperative launch
+      // with this much dynamic shared memory ("too many blocks", measured with
+      // 12 CTAs of 177 KB on 72 SMs); the basis is read from global memory there
+      if (fused && !on_partition()) {
+        stride = st_res;
+        smem = smem_res;
+      }
+    } else {
+      G = n / 512;
+      if (G > kCgMaxCtas) G = kCgMaxCtas;
+    }
+  }
   max_dynamic_smem(kern, smem);
-  // cooperative grid: no more CTAs than co-reside on this context's SMs (an
-  // SM partition has fewer than the device's 148); multi-CTA Arnoldi (CGS2)
-  // once each CTA gets >= 512 entries, on the first G CTAs of the grid
+  // cooperative grid: no more CTAs than co-reside on this context's SMs
   int cap = num_sms() * occupancy(kern, kPcgThreads, smem);
   if (sm_budget() > 0 && cap > sm_budget()) cap = sm_budget();
-  int G = n / 512;
-  if (G > kCgMaxCtas) G = kCgMaxCtas;
   if (G > cap) G = cap;
   if (G < 1) G = 1;
   int grid = fused && max_tiles > G ? max_tiles : G;
   if (grid > cap) grid = cap;
-  GmresArgs ga{st, V, part, n, G, restart, 0, restart};
+  GmresArgs ga{st, V, part, n, G, restart, 0, restart, ring / (int)sizeof(double), stride};
   auto launch = [&](int col0, int ncol) {
     ga.col0 = col0;
     ga.ncol = ncol;

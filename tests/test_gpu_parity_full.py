@@ -17,9 +17,10 @@ Tolerance: each step re-solves to the reference's residual_tol (1e-10) and
 re-truncates at step_tol (1e-8), so two correct implementations differ by
 rounding-level amounts amplified by the local solves' conditioning and
 accumulated over the steps.  The reference is not reproducible below that
-level itself: the same march with 1 instead of 4 (config 2) / 2 (config 3)
-OpenBLAS threads differs from the fixture by up to 2.1e-10 / 3.7e-10
-(tests/golden/config{2,3}_selfspread.npz, tools/make_golden_full.py
+level itself: the same march with 1, 2 or 8 instead of 4 (config 2) / 1
+instead of 2 (config 3) OpenBLAS threads differs from the fixture by up to
+2.9e-10 / 3.7e-10 (tests/golden/config{2,3}_selfspread.npz: per step the
+largest difference over these reference runs; tools/make_golden_full.py
 spread).  The bound at step k is therefore max(1e-10, 2 x the reference's
 own largest thread-count difference up to step k): north_star's 1e-10
 wherever the reference itself holds it, its own noise envelope elsewhere.

@@ -95,28 +95,31 @@ def steady(index):
     mg.save(f"config4_full_{index}.npz", st)
 
 
-def spread(fname, other_dir):
+def spread(fname, other_dirs):
     """Self-reproducibility of the reference: the same march recorded with
-    another BLAS thread count (OPENBLAS_NUM_THREADS=1, T2S2_GOLDEN_OUT=
-    other_dir) compared state by state with the committed fixture.  Writes
-    tests/golden/<config>_selfspread.npz: per stored step the relative
-    difference (10^5 seeded sample points) and whether the raw ranks agree."""
+    other BLAS thread counts (OPENBLAS_NUM_THREADS=k, T2S2_GOLDEN_OUT=dir_k)
+    compared state by state with the committed fixture.  Writes
+    tests/golden/<config>_selfspread.npz: per stored step the largest relative
+    difference over the other runs (10^5 seeded sample points), the
+    per-run differences, and whether the raw ranks agree in all of them."""
     from golden_io import get_train, has_train
     from helpers import rel_diff
 
     a = dict(np.load(os.path.join(mg.OUT, fname)))
-    b = dict(np.load(os.path.join(other_dir, fname)))
     n = int(a["n_steps"])
-    steps, diffs, same = [], [], []
-    for k in range(1, n + 1):
-        same.append(bool(np.array_equal(a[f"ranks{k}"], b[f"ranks{k}"])))
-        if has_train(a, f"state{k}"):
-            steps.append(k)
-            diffs.append(rel_diff(get_train(b, f"state{k}"), get_train(a, f"state{k}")))
-    out = {"steps": np.array(steps), "rel_diff": np.array(diffs), "ranks_equal": np.array(same),
-           "threads": np.array([int(a["blas_threads"]), int(b["blas_threads"])])}
-    print(fname, "threads", out["threads"], "max rel diff", max(diffs), "rank mismatches",
-          n - sum(same))
+    steps = [k for k in range(1, n + 1) if has_train(a, f"state{k}")]
+    per_run, same, thr = [], np.ones(n, dtype=bool), [int(a["blas_threads"])]
+    for d in other_dirs:
+        b = dict(np.load(os.path.join(d, fname)))
+        thr.append(int(b["blas_threads"]))
+        same &= np.array([np.array_equal(a[f"ranks{k}"], b[f"ranks{k}"]) for k in range(1, n + 1)])
+        per_run.append([rel_diff(get_train(b, f"state{k}"), get_train(a, f"state{k}")) for k in steps])
+        print(fname, "threads", thr[0], "vs", thr[-1], "max rel diff", max(per_run[-1]), flush=True)
+    per_run = np.array(per_run)
+    out = {"steps": np.array(steps), "rel_diff": per_run.max(axis=0), "rel_diff_runs": per_run,
+           "ranks_equal": same, "threads": np.array(thr)}
+    print(fname, "threads", thr, "max rel diff", out["rel_diff"].max(), "rank mismatches",
+          n - int(same.sum()))
     mg.save(fname.replace("_full.npz", "_selfspread.npz"), out)
 
 
@@ -124,7 +127,8 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("what", choices=["cfg2", "cfg3", "cfg4", "spread"])
     ap.add_argument("--fixture", default="config2_full.npz")
-    ap.add_argument("--other", default="/tmp/selfref")
+    ap.add_argument("--other", default=["/tmp/selfref"], nargs="+",
+                    help="spread: directories holding the same fixture recorded with other thread counts")
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--index", type=int, default=0)
     ap.add_argument("--keep-every", type=int, default=1)
