@@ -118,6 +118,25 @@ __global__ void copy_scaled_kernel(double* dst, int ldd, const double* src, int 
   }
 }
 
+// blockIdx.y = 0: d1 = s1 (r1 x c1 block copy); 1: d2[i, j] = s2[i, j] * rs[i]
+__global__ void copy_and_scaled_kernel(double* d1, int ldd1, const double* s1, int lds1, int r1, int c1,
+                                       double* d2, int ldd2, const double* s2, int lds2, int r2, int c2,
+                                       const double* rs) {
+  if (blockIdx.y == 0) {
+    const int n = r1 * c1;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+      const int r = e / c1, c = e - r * c1;
+      d1[(long long)r * ldd1 + c] = s1[(long long)r * lds1 + c];
+    }
+  } else {
+    const int n = r2 * c2;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+      const int r = e / c2, c = e - r * c2;
+      d2[(long long)r * ldd2 + c] = s2[(long long)r * lds2 + c] * rs[r];
+    }
+  }
+}
+
 __global__ void copy2d_pair_kernel(double* dst, int ldd, const double* s1, int ld1, int c1,
                                    const double* s2, int ld2, int c2, int rows) {
   const int cols = c1 + c2, n = rows * cols;
@@ -568,6 +587,22 @@ void copy_scaled(double* dst, int ldd, const double* src, int lds, int rows, int
   {
     LaunchScope ls("vector", (double)n, 16.0 * n);
     copy_scaled_kernel<<<grid_for(n), 256, 0, stream()>>>(dst, ldd, src, lds, rows, cols, rs, cs);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+void copy_and_scaled(double* d1, int ldd1, const double* s1, int lds1, int r1, int c1, double* d2,
+                     int ldd2, const double* s2, int lds2, int r2, int c2, const double* rs) {
+  const long long n1 = (long long)r1 * c1, n2 = (long long)r2 * c2;
+  if (n1 <= 0 || n2 <= 0) {
+    copy2d(d1, ldd1, s1, lds1, r1, c1);
+    copy_scaled(d2, ldd2, s2, lds2, r2, c2, rs, nullptr);
+    return;
+  }
+  {
+    LaunchScope ls("vector", (double)n2, 16.0 * (n1 + n2));
+    copy_and_scaled_kernel<<<dim3(grid_for(n1 > n2 ? n1 : n2), 2), 256, 0, stream()>>>(
+        d1, ldd1, s1, lds1, r1, c1, d2, ldd2, s2, lds2, r2, c2, rs);
   }
   T2S2_CHECK_LAUNCH();
 }

@@ -121,6 +121,9 @@ void copy2d(double* dst, int ldd, const double* src, int lds, int rows, int cols
 // product is the single rounding of copy2d followed by scale_rows/scale_cols)
 void copy_scaled(double* dst, int ldd, const double* src, int lds, int rows, int cols,
                  const double* rs, const double* cs);
+// copy2d(d1 <- s1, r1 x c1) and copy_scaled(d2 <- s2 with row scales rs, r2 x c2) in one launch
+void copy_and_scaled(double* d1, int ldd1, const double* s1, int lds1, int r1, int c1, double* d2,
+                     int ldd2, const double* s2, int lds2, int r2, int c2, const double* rs);
 // dst[:, :c1] = s1, dst[:, c1:c1+c2] = s2 (rows x ...), one launch
 void copy2d_pair(double* dst, int ldd, const double* s1, int ld1, int c1, const double* s2, int ld2,
                  int c2, int rows);

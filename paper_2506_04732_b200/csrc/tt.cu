@@ -26,27 +26,37 @@ __global__ void scale_cols_kernel(double* X, int rows, int cols, int ld, const d
   }
 }
 
-// One core of a TT sum written in one pass: out (r0o, mid, r1o) holds
-// fa * a at offsets (0, 0), fb * b at offsets (ob0, ob1), zeros elsewhere
-// (the blocks are disjoint: block diagonal, or side by side in the first
-// and last cores).
-__global__ void sum_core_kernel(double* out, int r0o, int mid, int r1o, const double* a, int r0a,
-                                int r1a, double fa, const double* b, int r0b, int r1b, double fb,
-                                int ob0, int ob1) {
-  const long long n = (long long)r0o * mid * r1o;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(e % r1o);
-    const long long t = e / r1o;
-    const int m = (int)(t % mid), i = (int)(t / mid);
+// The cores of a TT sum written in one pass and ONE launch (blockIdx.y = the
+// core): out (r0o, mid, r1o) holds fa * a at offsets (0, 0), fb * b at offsets
+// (ob0, ob1), zeros elsewhere (the blocks are disjoint: block diagonal, or
+// side by side in the first and last cores).
+constexpr int kSumCores = 8;
+struct SumCore {
+  double* out;
+  const double* a;
+  const double* b;
+  double fa, fb;
+  int r0o, mid, r1o, r0a, r1a, r0b, r1b, ob0, ob1;
+};
+struct SumCores {
+  SumCore c[kSumCores];
+};
+__global__ void sum_cores_kernel(const __grid_constant__ SumCores args) {
+  const SumCore& k = args.c[blockIdx.y];
+  const int n = k.r0o * k.mid * k.r1o;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int j = e % k.r1o;
+    const int t = e / k.r1o;
+    const int m = t % k.mid, i = t / k.mid;
     double v = 0.0;
-    if (i < r0a && j < r1a) {
-      v = fa * a[((long long)i * mid + m) * r1a + j];
+    if (i < k.r0a && j < k.r1a) {
+      v = k.fa * k.a[((long long)i * k.mid + m) * k.r1a + j];
     } else {
-      const int ib = i - ob0, jb = j - ob1;
-      if (ib >= 0 && jb >= 0 && ib < r0b && jb < r1b) v = fb * b[((long long)ib * mid + m) * r1b + jb];
+      const int ib = i - k.ob0, jb = j - k.ob1;
+      if (ib >= 0 && jb >= 0 && ib < k.r0b && jb < k.r1b)
+        v = k.fb * k.b[((long long)ib * k.mid + m) * k.r1b + jb];
     }
-    out[e] = v;
+    k.out[e] = v;
   }
 }
 
@@ -118,8 +128,8 @@ void right_orthonormalize(std::vector<DTensor>& cores) {
     DTensor Q, R;
     qr_thin(rows, r0, c.p, Q, R, true);  // Q rows x k (column-major), R k x r0
     const int k = rows < r0 ? rows : r0;
-    DTensor nc(with_bonds(c, k, r1));
-    dcopy(nc.p, Q.p, (size_t)rows * k);
+    DTensor nc = std::move(Q);  // column-major rows x k = the new core (k, mid, r1) row-major
+    nc.view(with_bonds(c, k, r1));
     DTensor& p = cores[l - 1];
     const int pr = (int)((long long)p.size() / r0);
     DTensor np(with_bonds(p, p.dim(0), k));
@@ -186,9 +196,8 @@ Train tt_round(const Train& t, double tol, int max_rank) {
     int r = tail_keep(hs, delta);
     if (r > cap) r = (int)cap;
     DTensor nc(with_bonds(c, r0, r));
-    copy2d(nc.p, r, U.p, kk, m, r);
     DTensor carry({r, r1});
-    copy_scaled(carry.p, r1, Vt.p, r1, r, r1, s.p, nullptr);
+    copy_and_scaled(nc.p, r, U.p, kk, m, r, carry.p, r1, Vt.p, r1, r, r1, s.p);
     DTensor& nx = w[l + 1];
     const int rest = (int)((long long)nx.size() / r1);
     DTensor nn(with_bonds(nx, r, nx.dim(-1)));
@@ -207,32 +216,44 @@ Train tt_add(const Train& a, const Train& b, double sa, double sb) {
   Train out;
   out.rows = a.rows;
   out.cols = a.cols;
+  if (d == 1) {
+    const DTensor& ca = a.cores[0];
+    DTensor o(ca.shape);
+    dcopy(o.p, b.cores[0].p, o.size());
+    daxpby(sa, ca.p, sb, o.p, o.size());
+    out.cores.push_back(std::move(o));
+    return out;
+  }
+  SumCores args{};
+  int nb = 0;
+  long long largest = 0, bytes = 0;
+  auto flush = [&]() {
+    if (nb == 0) return;
+    {
+      LaunchScope ls("vector", 0, (double)bytes);
+      sum_cores_kernel<<<dim3(grid_of(largest), nb), 256, 0, stream()>>>(args);
+    }
+    T2S2_CHECK_LAUNCH();
+    nb = 0;
+    largest = bytes = 0;
+  };
   for (int l = 0; l < d; ++l) {
     const DTensor& ca = a.cores[l];
     const DTensor& cb = b.cores[l];
-    const int mid = (int)mid_size(ca);
-    const double fa = l == 0 ? sa : 1.0, fb = l == 0 ? sb : 1.0;
-    if (d == 1) {
-      DTensor o(ca.shape);
-      dcopy(o.p, cb.p, o.size());
-      daxpby(fa, ca.p, fb, o.p, o.size());
-      out.cores.push_back(std::move(o));
-      continue;
-    }
     const int r0 = l == 0 ? 1 : ca.dim(0) + cb.dim(0);
     const int r1 = l == d - 1 ? 1 : ca.dim(-1) + cb.dim(-1);
     DTensor o(with_bonds(ca, r0, r1));
-    const int ob0 = l == 0 ? 0 : ca.dim(0), ob1 = l == d - 1 ? 0 : ca.dim(-1);
     const long long no = (long long)o.size();
-    {
-      LaunchScope ls("vector", 0, 8.0 * (no + (long long)ca.size() + (long long)cb.size()));
-      sum_core_kernel<<<grid_of(no), 256, 0, stream()>>>(o.p, r0, mid, r1, ca.p, ca.dim(0),
-                                                         ca.dim(-1), fa, cb.p, cb.dim(0),
-                                                         cb.dim(-1), fb, ob0, ob1);
-    }
-    T2S2_CHECK_LAUNCH();
+    T2S2_REQUIRE(no < (1LL << 31), kErrShape, "tt_add: core too large");
+    args.c[nb++] = SumCore{o.p, ca.p, cb.p, l == 0 ? sa : 1.0, l == 0 ? sb : 1.0, r0, (int)mid_size(ca),
+                           r1, ca.dim(0), ca.dim(-1), cb.dim(0), cb.dim(-1),
+                           l == 0 ? 0 : ca.dim(0), l == d - 1 ? 0 : ca.dim(-1)};
+    largest = no > largest ? no : largest;
+    bytes += 8 * (no + (long long)ca.size() + (long long)cb.size());
     out.cores.push_back(std::move(o));
+    if (nb == kSumCores) flush();
   }
+  flush();
   return out;
 }
 
@@ -245,16 +266,28 @@ Train tt_scale(const Train& a, double s) {
 Train tt_apply(const Train& op, const Train& v) {
   T2S2_REQUIRE(op.is_op() && !v.is_op() && op.cols == v.rows, kErrShape,
                "tt_apply: operator columns do not match vector modes");
+  // out_l[(a,c), m, (b,e)] = sum_n op_l[a, m, n, b] v_l[c, n, e]: every core is
+  // one batched GEMM (batch c, rows (a, m, b), columns e) that reads the cores
+  // where they lie and writes the result core in place, all cores in ONE
+  // single-stage program — one launch instead of two permutations, a GEMM and
+  // a permutation per core, with the same contraction order over n.
   Train out;
   out.rows = op.rows;
+  GemmBatch gb;
   for (int l = 0; l < op.d(); ++l) {
     const DTensor& co = op.cores[l];  // (a, m, n, b)
     const DTensor& cv = v.cores[l];   // (c, n, e)
-    DTensor t = tensordot(co, {2}, cv, {1});  // (a, m, b, c, e)
-    DTensor p = permute(t, {0, 3, 1, 2, 4});   // (a, c, m, b, e)
-    p.view({co.dim(0) * cv.dim(0), co.dim(1), co.dim(3) * cv.dim(2)});
+    const int A = co.dim(0), M = co.dim(1), N = co.dim(2), B = co.dim(3);
+    const int C = cv.dim(0), E = cv.dim(2);
+    DTensor p({A * C, M, B * E});
+    // A(i = (a m, b), n) at (i / B) * N B + (i % B) + n B; B(n, e) of batch c;
+    // C(i = (a, m b), e) at (i / (M B)) * C M B E + (i % (M B)) * E + e, batch stride M B E
+    const GemmOperand a{co.p, B, (long long)N * B, 1, B, 0};
+    const GemmOperand c{p.p, M * B, (long long)C * M * B * E, E, 1, (long long)M * B * E};
+    gb.add_general(0, A * M * B, E, N, a, cv.p, E, 1, (long long)N * E, c, C);
     out.cores.push_back(std::move(p));
   }
+  gb.run();
   return out;
 }
 
