@@ -154,10 +154,15 @@ __global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
 // deterministic two-level reduction per candidate (tt_solver.py:332-334 and
 // the isfinite check at :370/:398), read back together with the LU info.
 // One launch: the last CTA to arrive (ticket) sums the per-CTA partials in
-// CTA order and re-arms the ticket.
+// CTA order and re-arms the ticket; when the host reads the probe buffer
+// next (rt open) that CTA also publishes the buffer.
 __global__ void probe_kernel(const double* __restrict__ u, const double* __restrict__ nu,
                              const double* __restrict__ c, int n, double* part,
-                             unsigned* ticket, double* out) {
+                             unsigned* ticket, double* out, const double* buf, ReadTicket rt,
+                             int* zero_info) {
+  // (zero_info: the solver flags behind the probe slots are cleared for the
+  // solve that follows this probe — no memset on the stream)
+  if (zero_info && blockIdx.x == 0 && threadIdx.x < 2) zero_info[threadIdx.x] = 0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double x = u[i];
@@ -196,6 +201,11 @@ __global__ void probe_kernel(const double* __restrict__ u, const double* __restr
     out[threadIdx.x] = t;
   }
   if (threadIdx.x == 0) *ticket = 0u;
+  if (rt.dst) {
+    // the host reads the whole probe buffer next: publish it from here
+    __syncthreads();
+    publish_words(rt, reinterpret_cast<const unsigned*>(buf), 32);
+  }
 }
 
 __global__ void nonfinite_kernel(const double* x, long long n, int* flag) {
@@ -582,14 +592,23 @@ struct Probe {
   unsigned* ticket() { return reinterpret_cast<unsigned*>(buf.p + 14); }
   // info()[0]: LU info; info()[1]: a pivoted solve interchanged rows
   void clear_info() { T2S2_CUDA(cudaMemsetAsync(info(), 0, 2 * sizeof(int), stream())); }
-  void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c) {
+  ReadTicket open;  // the last probe launch publishes the buffer itself
+  bool is_open = false;
+  // then_read: read() follows this launch with nothing that reads in between
+  void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c, bool then_read,
+           bool zero_info = false) {
     const int n = (int)u.size();
+    if (then_read) {
+      open = read_open(16 * sizeof(double));
+      is_open = true;
+    }
     int nb = (n + 255) / 256;
     if (nb > 148) nb = 148;
     double* part = allocator().alloc((size_t)nb * 3);
     {
       LaunchScope ls("reduce", 4.0 * n, 24.0 * n);
-      probe_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part, ticket(), buf.p + 3 * slot);
+      probe_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part, ticket(), buf.p + 3 * slot, buf.p,
+                                             then_read ? open : ReadTicket{}, zero_info ? info() : nullptr);
     }
     T2S2_CHECK_LAUNCH();
     allocator().release(part);
@@ -597,7 +616,12 @@ struct Probe {
   // one read-back: h[3*slot + {0,1,2}], info at h_info, interchange flag
   void read(double* h, int* h_info, int* h_swapped = nullptr) {
     double tmp[16];
-    host_read(tmp, buf.p, sizeof tmp);
+    if (is_open) {
+      read_close(tmp, sizeof tmp, open);
+      is_open = false;
+    } else {
+      host_read(tmp, buf.p, sizeof tmp);
+    }
     for (int i = 0; i < 12; ++i) h[i] = tmp[i];
     *h_info = reinterpret_cast<int*>(tmp + 12)[0];
     if (h_swapped) *h_swapped = reinterpret_cast<int*>(tmp + 12)[1];
@@ -675,16 +699,14 @@ struct SplitSync {
   // read keep, s and (optionally) zs together
   int read(const DTensor& s, const DTensor* zs, std::vector<double>& hz) {
     const int zk = zs ? zs->dim(0) : 0;
-    DTensor buf({1 + kk + zk});
-    pack(buf.p, {{keep_mask.p, 1}, {s.p, (size_t)kk}, {zk ? zs->p : nullptr, (size_t)zk}});
     std::vector<double> h(1 + kk + zk);
-    to_host(h.data(), buf.p, h.size());
+    host_read_gather(h.data(), {{keep_mask.p, 1}, {s.p, (size_t)kk}, {zk ? zs->p : nullptr, (size_t)zk}});
     hz.assign(h.begin() + 1 + kk, h.end());
     return (int)h[0];
   }
 };
 
-Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& cfg, int d) {
+Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
   DTensor U, s, Vt;
   svd_thin(m, r1, u.p, U, s, Vt);
@@ -697,7 +719,7 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
   if (enrich) {
     // z = g - U_keep U_keep^T g, with U_keep = U diag(mask)
     const int gc = (int)(grad->size() / m);
-    DTensor z = grad->clone();
+    DTensor z = std::move(*grad);  // the gradient is consumed here
     DTensor tmp({kk, gc});
     {
       GemmBatch gb;  // tmp = diag(mask) U^T z, then z -= U tmp: one launch
@@ -729,7 +751,7 @@ Split split_forward(const DTensor& u, const DTensor* grad, const SolverConfig& c
   return out;
 }
 
-Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& cfg, int d) {
+Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), cols = n * r1;
   DTensor U, s, Vt;
   svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
@@ -741,7 +763,7 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
   if (enrich) {
     // z = g - g Vt_keep^T Vt_keep, with Vt_keep = diag(mask) Vt
     const int gr = (int)(grad->size() / cols);
-    DTensor z = grad->clone();
+    DTensor z = std::move(*grad);  // the gradient is consumed here
     DTensor tmp({gr, kk});
     {
       GemmBatch gb;  // tmp = z Vt^T diag(mask), then z -= tmp Vt: one launch
@@ -771,8 +793,8 @@ Split split_backward(const DTensor& u, const DTensor* grad, const SolverConfig& 
 
 // -- residual (tt_solver.py:305-329) ----------------------------------------------
 
-double measure_residual(const Train& A, const std::vector<DTensor>& acg,
-                        const std::vector<DTensor>& x, const Train& rhs, double bnorm) {
+double measure_residual(const Train& A, const std::vector<DTensor>& acg, std::vector<DTensor>& x,
+                        const Train& rhs, double bnorm) {
   const int d = A.d();
   // both Gram chains in one program (4 stages per core for <Ax,Ax>, 3 for <Ax,b>)
   GemmBatch gb;
@@ -790,20 +812,22 @@ double measure_residual(const Train& A, const std::vector<DTensor>& acg,
   gb.run();
   keep.clear();
   double hv[2];
-  {
-    DTensor two({2});
-    dcopy(two.p, phi.p, 1);
-    dcopy(two.p + 1, psi.p, 1);
-    to_host(hv, two.p, 2);
-  }
+  host_read_gather(hv, {{phi.p, 1}, {psi.p, 1}});
   const double axax = hv[0], axb = hv[1];
   const double est_sq = axax - 2.0 * axb + bnorm * bnorm;
   const double est = std::sqrt(est_sq > 0.0 ? est_sq : 0.0) / bnorm;
   if (est_sq <= 0.0 || est < 1e-6) {
-    Train xt;
+    Train xt;  // the cores are lent to a train for the apply and taken back
     xt.rows = rhs.rows;
-    for (auto& c : x) xt.cores.push_back(c.clone());
-    Train diff = tt_add(tt_apply(A, xt), rhs, 1.0, -1.0);
+    xt.cores = std::move(x);
+    Train diff;
+    try {
+      diff = tt_add(tt_apply(A, xt), rhs, 1.0, -1.0);
+    } catch (...) {
+      x = std::move(xt.cores);
+      throw;
+    }
+    x = std::move(xt.cores);
     return tt_norm(diff) / bnorm;
   }
   return est;
@@ -849,8 +873,7 @@ struct Sweep {
       nop.add(gb, 0, u_old.p, nu_old.p);
       gb.run();
     }
-    probe.run(0, u_old, nu_old, c_ls);
-    probe.clear_info();
+    probe.run(0, u_old, nu_old, c_ls, false, true);  // and clears the solver flags
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
     const double inner_rtol = std::fmax(cfg.inner_tol_factor * current_res, 1e-12);
     const bool try_gal = gal_rejects < gal_cap;
@@ -870,7 +893,7 @@ struct Sweep {
       u_gal.view(u_old.shape);
       trace_buffer("update u_gal", u_gal.p, u_gal.size());
       nu_gal = nop.apply(u_gal);
-      probe.run(1, u_gal, nu_gal, c_ls);
+      probe.run(1, u_gal, nu_gal, c_ls, true);
     }
     double h[12];
     int info = 0, swapped = 0;
@@ -883,7 +906,7 @@ struct Sweep {
       dense_solve_pivoted(B, c_gal, u_gal, probe.info());
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
-      probe.run(1, u_gal, nu_gal, c_ls);
+      probe.run(1, u_gal, nu_gal, c_ls, true);
       probe.read(h, &info);
     }
     if (try_gal && direct && info != 0) {
@@ -893,7 +916,7 @@ struct Sweep {
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
       probe.clear_info();
-      probe.run(1, u_gal, nu_gal, c_ls);
+      probe.run(1, u_gal, nu_gal, c_ls, true);
       probe.read(h, &info);
     }
     const double q_old = h[0] - 2.0 * h[1];
@@ -931,7 +954,7 @@ struct Sweep {
       u_ls.view(u_old.shape);
       trace_buffer("update u_ls", u_ls.p, u_ls.size());
       DTensor nu_ls = nop.apply(u_ls);
-      probe.run(2, u_ls, nu_ls, c_ls);
+      probe.run(2, u_ls, nu_ls, c_ls, true);
       probe.read(h, &info, &swapped);
       if (direct) pol_ls.observe(info, swapped);
       if (direct && info == -1) {
@@ -941,7 +964,7 @@ struct Sweep {
         dense_solve_pivoted(Nm, c_ls, u_ls, probe.info());
         u_ls.view(u_old.shape);
         nu_ls = nop.apply(u_ls);
-        probe.run(2, u_ls, nu_ls, c_ls);
+        probe.run(2, u_ls, nu_ls, c_ls, true);
         probe.read(h, &info);
       }
       if (direct && info != 0) {
@@ -952,7 +975,7 @@ struct Sweep {
         u_ls.view(u_old.shape);
         nu_ls = nop.apply(u_ls);
         probe.clear_info();
-        probe.run(2, u_ls, nu_ls, c_ls);
+        probe.run(2, u_ls, nu_ls, c_ls, true);
         probe.read(h, &info);
       }
       if (info == 0 && h[8] == 0.0) {
@@ -1108,12 +1131,17 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
     }
     rep.ranks.push_back(mr);
     rep.compression.push_back(stored / dense);
+    const bool done = current_res <= cfg.residual_tol;
     if (current_res < best_res) {
       best_res = current_res;
-      best_cores.clear();
-      for (auto& c : cores) best_cores.push_back(c.clone());
+      if (done) {
+        best_cores = std::move(cores);  // the sweep loop ends here: no copy
+      } else {
+        best_cores.clear();
+        for (auto& c : cores) best_cores.push_back(c.clone());
+      }
     }
-    if (current_res <= cfg.residual_tol) {
+    if (done) {
       rep.converged = true;
       break;
     }

@@ -53,6 +53,10 @@ struct t2s2_context {
   void* pinned = nullptr;
   static constexpr size_t kPinnedBytes = 64 * 1024;
   unsigned read_ticket = 0;  // last ticket published into the word after the staging buffer
+  // zeroed device words for the counters of hand-off kernels (zero_words)
+  unsigned* zero_pool = nullptr;
+  size_t zero_cursor = 0;
+  static constexpr size_t kZeroWords = 1 << 16;
   // host_read trace: 0 off, 1 record, 2 replay
   int trace_mode = 0;
   std::vector<std::vector<unsigned char>> trace;
@@ -206,6 +210,105 @@ __global__ void publish_kernel(const unsigned* __restrict__ src, unsigned* dst, 
   if (threadIdx.x == 0) *ticket = value;
 }
 
+namespace {
+// trace bookkeeping of a completed read (record / compare modes)
+void trace_read(t2s2_context* c, const void* host, size_t bytes);
+}  // namespace
+
+// Zeroed words for a kernel's arrival counters without a memset per launch:
+// slices of a pool that is cleared as a whole when it has been handed out
+// once (stream-ordered after every earlier user).
+unsigned* zero_words(size_t n) {
+  t2s2_context* c = g_ctx;
+  T2S2_REQUIRE(n <= t2s2_context::kZeroWords, kErrArg, "zero_words: request too large");
+  const bool fresh = !c->zero_pool;
+  if (fresh) c->zero_pool = reinterpret_cast<unsigned*>(c->alloc.alloc(t2s2_context::kZeroWords / 2));
+  if (fresh || c->zero_cursor + n > t2s2_context::kZeroWords) {
+    T2S2_CUDA(cudaMemsetAsync(c->zero_pool, 0, t2s2_context::kZeroWords * sizeof(unsigned), c->stream));
+    c->zero_cursor = 0;
+  }
+  unsigned* p = c->zero_pool + c->zero_cursor;
+  c->zero_cursor += (n + 3) & ~size_t(3);
+  return p;
+}
+
+ReadTicket read_open(size_t bytes) {
+  t2s2_context* c = g_ctx;
+  ReadTicket t;
+  if (c->trace_mode == 2) return t;  // replay: nothing is published, read_close hands back the record
+  T2S2_REQUIRE(bytes && bytes <= t2s2_context::kPinnedBytes && bytes % 4 == 0, kErrArg,
+               "read_open: unsupported size");
+  if (!c->pinned) {
+    T2S2_CUDA(cudaHostAlloc(&c->pinned, t2s2_context::kPinnedBytes + 64, cudaHostAllocMapped));
+    std::memset(c->pinned, 0, t2s2_context::kPinnedBytes + 64);
+  }
+  t.dst = static_cast<unsigned*>(c->pinned);
+  t.flag = reinterpret_cast<unsigned*>(static_cast<char*>(c->pinned) + t2s2_context::kPinnedBytes);
+  t.value = ++c->read_ticket;
+  return t;
+}
+
+void read_close(void* host, size_t bytes, const ReadTicket& t) {
+  t2s2_context* c = g_ctx;
+  if (c->trace_mode == 2) {
+    T2S2_REQUIRE(c->trace_pos < c->trace.size() && c->trace[c->trace_pos].size() == bytes, kErrArg,
+                 "host_read replay: the run differs from the recorded one");
+    std::memcpy(host, c->trace[c->trace_pos++].data(), bytes);
+    return;
+  }
+  T2S2_CHECK_LAUNCH();
+  // spin on the ticket; a faulted or finished stream without the ticket is an error
+  volatile unsigned* ticket = t.flag;
+  for (unsigned long long spins = 0; *ticket != t.value; ++spins) {
+    if ((spins & 0xfffff) == 0xfffff) {
+      const cudaError_t q = cudaStreamQuery(c->stream);
+      if (q != cudaErrorNotReady && *ticket != t.value) {
+        T2S2_CUDA(q);
+        T2S2_REQUIRE(*ticket == t.value, kErrCuda, "host_read: the stream drained without the ticket");
+      }
+    }
+  }
+  std::memcpy(host, c->pinned, bytes);
+  trace_read(c, host, bytes);
+}
+
+// Up to four device segments gathered straight into the mapped buffer by ONE
+// kernel (instead of a pack kernel or copies followed by the publish kernel).
+struct GatherArgs {
+  const unsigned* src[4];
+  int words[4];
+  int k;
+};
+__global__ void gather_publish_kernel(GatherArgs a, ReadTicket t) {
+  int off = 0;
+  for (int q = 0; q < a.k; ++q) {
+    for (int i = threadIdx.x; i < a.words[q]; i += blockDim.x) t.dst[off + i] = a.src[q][i];
+    off += a.words[q];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *(volatile unsigned*)t.flag = t.value;
+}
+
+void host_read_gather(double* host, std::initializer_list<std::pair<const double*, size_t>> parts) {
+  GatherArgs a{};
+  size_t total = 0;
+  for (const auto& pr : parts) {
+    if (!pr.second) continue;
+    T2S2_REQUIRE(a.k < 4, kErrArg, "host_read_gather: at most four segments");
+    a.src[a.k] = reinterpret_cast<const unsigned*>(pr.first);
+    a.words[a.k++] = (int)(2 * pr.second);
+    total += pr.second;
+  }
+  if (!total) return;
+  const ReadTicket t = read_open(total * sizeof(double));
+  if (t.dst) {
+    LaunchScope ls("host_read", 0.0, 16.0 * total);
+    gather_publish_kernel<<<1, 2 * total < 256 ? 32 * (int)((2 * total + 31) / 32) : 256, 0, stream()>>>(a, t);
+  }
+  read_close(host, total * sizeof(double), t);
+}
+
 void host_read(void* host, const void* dev, size_t bytes) {
   t2s2_context* c = g_ctx;
   if (c->trace_mode == 2) {
@@ -216,35 +319,23 @@ void host_read(void* host, const void* dev, size_t bytes) {
   }
   if (bytes && bytes <= t2s2_context::kPinnedBytes && bytes % 4 == 0 &&
       reinterpret_cast<uintptr_t>(dev) % 4 == 0) {
-    if (!c->pinned) {
-      T2S2_CUDA(cudaHostAlloc(&c->pinned, t2s2_context::kPinnedBytes + 64, cudaHostAllocMapped));
-      std::memset(c->pinned, 0, t2s2_context::kPinnedBytes + 64);
-    }
-    volatile unsigned* ticket =
-        reinterpret_cast<volatile unsigned*>(static_cast<char*>(c->pinned) + t2s2_context::kPinnedBytes);
-    const unsigned value = ++c->read_ticket;
+    const ReadTicket t = read_open(bytes);
     const int words = (int)(bytes / 4);
     {
       LaunchScope ls("host_read", 0.0, 2.0 * bytes);
       publish_kernel<<<1, words < 256 ? 32 * ((words + 31) / 32) : 256, 0, c->stream>>>(
-          static_cast<const unsigned*>(dev), static_cast<unsigned*>(c->pinned), words, ticket, value);
+          static_cast<const unsigned*>(dev), t.dst, words, t.flag, t.value);
     }
-    T2S2_CHECK_LAUNCH();
-    // spin on the ticket; a faulted or finished stream without the ticket is an error
-    for (unsigned long long spins = 0; *ticket != value; ++spins) {
-      if ((spins & 0xfffff) == 0xfffff) {
-        const cudaError_t q = cudaStreamQuery(c->stream);
-        if (q != cudaErrorNotReady && *ticket != value) {
-          T2S2_CUDA(q);
-          T2S2_REQUIRE(*ticket == value, kErrCuda, "host_read: the stream drained without the ticket");
-        }
-      }
-    }
-    std::memcpy(host, c->pinned, bytes);
-  } else {
-    if (bytes) T2S2_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
-    T2S2_CUDA(cudaStreamSynchronize(c->stream));
+    read_close(host, bytes, t);
+    return;
   }
+  if (bytes) T2S2_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  T2S2_CUDA(cudaStreamSynchronize(c->stream));
+  trace_read(c, host, bytes);
+}
+
+namespace {
+void trace_read(t2s2_context* c, const void* host, size_t bytes) {
   if (c->trace_mode == 1) {
     const unsigned char* b = static_cast<const unsigned char*>(host);
     c->trace.emplace_back(b, b + bytes);
@@ -266,6 +357,7 @@ void host_read(void* host, const void* dev, size_t bytes) {
     }
   }
 }
+}  // namespace
 
 }  // namespace t2s2
 
@@ -427,6 +519,7 @@ void t2s2_context_destroy(t2s2_context* ctx) {
   else
     cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->zero_pool) ctx->alloc.release(reinterpret_cast<double*>(ctx->zero_pool));
   ctx->alloc.trim();
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->event_pool) cudaEventDestroy(e);

@@ -171,11 +171,16 @@ __global__ void dot_partial_kernel(const double* x, const double* y, long long n
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void sum_final_kernel(const double* part, int n, double* out) {
+// (an open read ticket: the sum is also published to the host, see common.h)
+__global__ void sum_final_kernel(const double* part, int n, double* out, ReadTicket t) {
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
   s = block_sum(s);
   if (threadIdx.x == 0) *out = s;
+  if (t.dst) {
+    __syncthreads();
+    publish_words(t, reinterpret_cast<const unsigned*>(out), 2);
+  }
 }
 
 __global__ void transpose_kernel(const double* in, double* out, int rows, int cols) {
@@ -660,7 +665,7 @@ void pack(double* dst, std::initializer_list<std::pair<const double*, size_t>> p
   run_segments(a, most);
 }
 
-void ddot_dev(const double* x, const double* y, size_t n, double* out) {
+static void ddot_launch(const double* x, const double* y, size_t n, double* out, const ReadTicket& t) {
   int g = grid_for((long long)n, 256, 296);
   double* part = allocator().alloc(g);
   {
@@ -669,10 +674,14 @@ void ddot_dev(const double* x, const double* y, size_t n, double* out) {
   }
   {
     LaunchScope ls("reduce", 0, 0);
-    sum_final_kernel<<<1, 256, 0, stream()>>>(part, g, out);
+    sum_final_kernel<<<1, 256, 0, stream()>>>(part, g, out, t);
   }
   T2S2_CHECK_LAUNCH();
   allocator().release(part);
+}
+
+void ddot_dev(const double* x, const double* y, size_t n, double* out) {
+  ddot_launch(x, y, n, out, ReadTicket{});
 }
 
 double scalar_to_host(const double* d) {
@@ -682,9 +691,12 @@ double scalar_to_host(const double* d) {
 }
 
 double ddot(const double* x, const double* y, size_t n) {
+  // the final sum publishes itself: no separate read launch
   double* o = allocator().alloc(1);
-  ddot_dev(x, y, n, o);
-  double h = scalar_to_host(o);
+  const ReadTicket t = read_open(sizeof(double));
+  ddot_launch(x, y, n, o, t);
+  double h = 0.0;
+  read_close(&h, sizeof(double), t);
   allocator().release(o);
   return h;
 }

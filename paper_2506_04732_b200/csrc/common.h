@@ -7,6 +7,9 @@
 // in HBM (or L2) between kernels.
 #pragma once
 
+#include <initializer_list>
+#include <utility>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -125,6 +128,37 @@ bool profiling();        // per-launch CUDA-event timing switched on (t2s2_stats
 // synchronising, to an identical run (t2s2_read_trace): the measurement of
 // what the synchronising reads cost.
 void host_read(void* host, const void* dev, size_t bytes);
+// n zeroed 32-bit device words that stay untouched by anyone else until the
+// context's pool of them has been handed out once (65536 words): arrival
+// counters of one kernel launch, no memset per launch
+unsigned* zero_words(size_t n);
+// A steering read published by its producer: read_open reserves the mapped
+// host buffer and the next ticket; the LAST kernel that computes the values
+// copies them there itself (publish_words: one CTA, after the values are
+// visible to it) instead of a separate publish launch; read_close waits for
+// the ticket and hands the bytes to the host (and to the read trace).
+// Nothing else may read between open and close.  While a trace is replayed
+// the ticket is empty (dst == null): kernels publish nothing and read_close
+// returns the recorded values.
+struct ReadTicket {
+  unsigned* dst = nullptr;   // mapped host buffer (device-visible)
+  unsigned* flag = nullptr;  // ticket word behind it
+  unsigned value = 0;
+};
+ReadTicket read_open(size_t bytes);
+void read_close(void* host, size_t bytes, const ReadTicket& t);
+// up to four device segments (pointer, doubles) read back as one array with one kernel
+void host_read_gather(double* host, std::initializer_list<std::pair<const double*, size_t>> parts);
+#ifdef __CUDACC__
+// every thread of ONE CTA, once the n words at src are visible to that CTA
+__device__ __forceinline__ void publish_words(const ReadTicket& t, const unsigned* src, int n) {
+  if (!t.dst) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) t.dst[i] = __ldcg(src + i);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *(volatile unsigned*)t.flag = t.value;
+}
+#endif
 bool replaying_reads();  // host_read returns recorded values, nothing synchronises
 // Determinism probe: while a trace is recorded (mode 1) or compared (mode 3)
 // the tagged device buffer joins the trace like a host read; otherwise a no-op.

@@ -829,8 +829,7 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   const int npan = (N + kP - 1) / kP;
   double* inv = allocator().alloc((size_t)npan * kInv);
   double* wbuf = allocator().alloc((size_t)3 * kP * (N + 1));
-  unsigned* sync = reinterpret_cast<unsigned*>(allocator().alloc((size_t)(npan + 3) / 2 + 1));
-  T2S2_CUDA(cudaMemsetAsync(sync, 0, sizeof(unsigned) * (size_t)(npan + 3), stream()));
+  unsigned* sync = zero_words((size_t)npan + 3);
   GjArgs a{N, A, b, inv, wbuf, info_dev, sync, nullptr};  // *info zeroed by the kernel
   void* params[] = {&a};
   {
@@ -844,7 +843,6 @@ bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev) {
   }
   allocator().release(inv);
   allocator().release(wbuf);
-  allocator().release(reinterpret_cast<double*>(sync));
   return true;
 }
 

@@ -116,10 +116,14 @@ int tail_keep(const std::vector<double>& s, double delta) {
   return r < 1 ? 1 : r;
 }
 
-void right_orthonormalize(std::vector<DTensor>& cores) {
-  const int d = (int)cores.size();
+// Right-to-left QR sweep: reads the cores of `in` (core l - 1 after it has
+// absorbed R_l), never writes them; returns the new cores.
+static std::vector<DTensor> right_orthonormalized(const std::vector<DTensor>& in) {
+  const int d = (int)in.size();
+  std::vector<DTensor> out(d);
+  DTensor absorbed;  // core l with R_{l+1} multiplied in
   for (int l = d - 1; l > 0; --l) {
-    DTensor& c = cores[l];
+    const DTensor& c = l == d - 1 ? in[l] : absorbed;
     const int r0 = c.dim(0), r1 = c.dim(-1);
     const long long mid = mid_size(c);
     const int rows = (int)(mid * r1);
@@ -128,15 +132,21 @@ void right_orthonormalize(std::vector<DTensor>& cores) {
     DTensor Q, R;
     qr_thin(rows, r0, c.p, Q, R, true);  // Q rows x k (column-major), R k x r0
     const int k = rows < r0 ? rows : r0;
-    DTensor nc = std::move(Q);  // column-major rows x k = the new core (k, mid, r1) row-major
+    DTensor nc = std::move(Q);
     nc.view(with_bonds(c, k, r1));
-    DTensor& p = cores[l - 1];
+    const DTensor& p = in[l - 1];
     const int pr = (int)((long long)p.size() / r0);
     DTensor np(with_bonds(p, p.dim(0), k));
     gemm(false, true, pr, k, r0, 1.0, p.p, r0, R.p, r0, 0.0, np.p, k);
-    cores[l] = std::move(nc);
-    cores[l - 1] = std::move(np);
+    out[l] = std::move(nc);
+    absorbed = std::move(np);
   }
+  out[0] = d == 1 ? in[0].clone() : std::move(absorbed);
+  return out;
+}
+
+void right_orthonormalize(std::vector<DTensor>& cores) {
+  if (cores.size() > 1) cores = right_orthonormalized(cores);
 }
 
 double tt_norm(const Train& t) {
@@ -170,9 +180,7 @@ Train tt_round(const Train& t, double tol, int max_rank) {
   if (d == 1) return t.clone();
   const long long cap_all = max_rank > 0 ? max_rank : 1000000000LL;
   std::vector<int> in_ranks = t.ranks();
-  std::vector<DTensor> w;
-  for (auto& c : t.cores) w.push_back(c.clone());
-  right_orthonormalize(w);
+  std::vector<DTensor> w = right_orthonormalized(t.cores);
   const double nrm = dnrm2(w[0].p, w[0].size());
   if (nrm == 0.0) {
     for (int l = 0; l < d; ++l) {
