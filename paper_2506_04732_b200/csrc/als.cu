@@ -632,6 +632,7 @@ struct Probe {
 
 struct Split {
   DTensor core, carry;
+  DTensor next;  // the neighbour core's new buffer (its enrichment part zeroed), if asked for
   int extra = 0;
 };
 
@@ -706,7 +707,11 @@ struct SplitSync {
   }
 };
 
-Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d) {
+// neighbour: the core the carry goes to; out.next is its new buffer
+// (keep + extra, n', r'), rows of the enrichment part zeroed.  Carry, core and
+// that zero fill are ONE launch (split_finish).
+Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d,
+                    const DTensor* neighbour = nullptr) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
   DTensor U, s, Vt;
   svd_thin(m, r1, u.p, U, s, Vt);
@@ -735,7 +740,6 @@ Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, in
   const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({keep, r1});
-  copy_scaled(out.carry.p, r1, Vt.p, r1, keep, r1, s.p, nullptr);
   if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
@@ -744,14 +748,22 @@ Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, in
     out.extra = extra > 0 ? extra : 0;
   }
   out.core = DTensor({r0, n, keep + out.extra});
-  if (out.extra > 0)
-    copy2d_pair(out.core.p, keep + out.extra, U.p, kk, keep, zu.p, zk, out.extra, m);
-  else
-    copy2d(out.core.p, keep, U.p, kk, m, keep);
+  SplitFinish f{};
+  f.d0 = out.carry.p, f.s0 = Vt.p, f.ldd0 = r1, f.lds0 = r1, f.rows0 = keep, f.cols0 = r1, f.rs = s.p;
+  f.d1 = out.core.p, f.a1 = U.p, f.b1 = zu.p, f.ldd1 = keep + out.extra, f.lda1 = kk, f.ldb1 = zk;
+  f.c1 = keep, f.c2 = out.extra, f.rows1 = m;
+  if (neighbour) {
+    const int rest = (int)(neighbour->size() / r1);
+    out.next = DTensor({keep + out.extra, neighbour->dim(1), neighbour->dim(2)});
+    f.d2 = out.next.p + (size_t)keep * rest;
+    f.n2 = (long long)out.extra * rest;
+  }
+  split_finish(f);
   return out;
 }
 
-Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d) {
+Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, int d,
+                     const DTensor* neighbour = nullptr) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), cols = n * r1;
   DTensor U, s, Vt;
   svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
@@ -778,7 +790,6 @@ Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, i
   const int keep = sync.read(s, enrich ? &zs : nullptr, hz);
   Split out;
   out.carry = DTensor({r0, keep});
-  copy_scaled(out.carry.p, keep, U.p, kk, r0, keep, nullptr, s.p);
   if (enrich && keep < cfg.max_rank) {
     int nz = count_significant(hz);
     int extra = cfg.enrichment_rank;
@@ -787,7 +798,19 @@ Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, i
     out.extra = extra > 0 ? extra : 0;
   }
   out.core = DTensor({keep + out.extra, n, r1});
-  pack(out.core.p, {{Vt.p, (size_t)keep * cols}, {zvt.p, (size_t)out.extra * cols}});
+  SplitFinish f{};
+  f.d0 = out.carry.p, f.s0 = U.p, f.ldd0 = keep, f.lds0 = kk, f.rows0 = r0, f.cols0 = keep, f.cs = s.p;
+  // the core: keep rows of Vt, then extra rows of the gradient's Vt — two contiguous pieces
+  f.d1 = out.core.p, f.a1 = Vt.p, f.b1 = zvt.p, f.rows1 = 1;
+  f.c1 = keep * cols, f.c2 = out.extra * cols;
+  if (neighbour) {
+    out.next = DTensor({neighbour->dim(0), neighbour->dim(1), keep + out.extra});
+    if (out.extra > 0) {
+      f.d2 = out.next.p;
+      f.n2 = (long long)out.next.size();
+    }
+  }
+  split_finish(f);
   return out;
 }
 
@@ -843,12 +866,24 @@ struct Sweep {
   int gal_rejects = 0;
   int gal_cap;
   std::vector<DTensor> la, ln, lg, lb, ra, rn, rg, rb;
-  std::vector<DTensor> acg;  // per-core operator layout (m, A, a, n)
+  const std::vector<DTensor>& acg;  // per-core operator layout (m, A, a, n), cached in the train
+  static const std::vector<DTensor>& layout_of(const Train& a) {
+    bool valid = a.layout_of.size() == a.cores.size() && !a.cores.empty();
+    for (size_t l = 0; valid && l < a.cores.size(); ++l) valid = a.layout_of[l] == a.cores[l].p;
+    if (!valid) {
+      a.solver_layout.clear();
+      a.layout_of.clear();
+      for (const DTensor& ac : a.cores) {
+        a.solver_layout.push_back(op_layout(ac));
+        a.layout_of.push_back(ac.p);
+      }
+    }
+    return a.solver_layout;
+  }
   Sweep(const Train& a, const Train& b, const SolverConfig& c)
       : A(a), rhs(b), cfg(c), d(a.d()), gal_cap(2 * a.d()),
-        la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1) {
-    for (const DTensor& ac : a.cores) acg.push_back(op_layout(ac));
-  }
+        la(d + 1), ln(d + 1), lg(d + 1), lb(d + 1), ra(d + 1), rn(d + 1), rg(d + 1), rb(d + 1),
+        acg(layout_of(a)) {}
 
   Probe probe;
   PivotPolicy pol_gal, pol_ls;  // Galerkin / normal-equation systems
@@ -1057,13 +1092,12 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
         end_direct = sw.gal_direct;
         break;
       }
-      Split sp = split_forward(u, &grad, cfg, d);
+      Split sp = split_forward(u, &grad, cfg, d, &cores[l + 1]);
       cores[l] = std::move(sp.core);
       const DTensor& nx = cores[l + 1];
       const int keep = sp.carry.dim(0), r1 = sp.carry.dim(1);
       const int rest = (int)(nx.size() / r1);
-      DTensor nn({keep + sp.extra, nx.dim(1), nx.dim(2)});
-      if (sp.extra > 0) dfill(nn.p + (size_t)keep * rest, 0.0, (size_t)sp.extra * rest);
+      DTensor nn = std::move(sp.next);  // rows of the enrichment part already zero
       {
         // the carry product (next core) and the four interface recurrences
         // of the moved bond are independent: one program
@@ -1099,14 +1133,13 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
         cores[l] = std::move(u);
         break;
       }
-      Split sp = split_backward(u, &grad, cfg, d);
+      Split sp = split_backward(u, &grad, cfg, d, &cores[l - 1]);
       cores[l] = std::move(sp.core);
       const DTensor& pv = cores[l - 1];
       const int r0 = sp.carry.dim(0), keep = sp.carry.dim(1);
       const int rows = (int)(pv.size() / r0);
       const int nk = keep + sp.extra;
-      DTensor np({pv.dim(0), pv.dim(1), nk});
-      if (sp.extra > 0) dfill(np.p, 0.0, np.size());
+      DTensor np = std::move(sp.next);  // zeroed when it has enrichment columns
       {
         // the carry product (previous core) and the four interface
         // recurrences of the moved bond are independent: one program

@@ -248,6 +248,16 @@ ReadTicket read_open(size_t bytes) {
   return t;
 }
 
+void read_publish(const void* dev, size_t bytes, const ReadTicket& t) {
+  if (!t.dst) return;
+  const int words = (int)(bytes / 4);
+  {
+    LaunchScope ls("host_read", 0.0, 2.0 * bytes);
+    publish_kernel<<<1, words < 256 ? 32 * ((words + 31) / 32) : 256, 0, g_ctx->stream>>>(
+        static_cast<const unsigned*>(dev), t.dst, words, t.flag, t.value);
+  }
+}
+
 void read_close(void* host, size_t bytes, const ReadTicket& t) {
   t2s2_context* c = g_ctx;
   if (c->trace_mode == 2) {
@@ -320,12 +330,7 @@ void host_read(void* host, const void* dev, size_t bytes) {
   if (bytes && bytes <= t2s2_context::kPinnedBytes && bytes % 4 == 0 &&
       reinterpret_cast<uintptr_t>(dev) % 4 == 0) {
     const ReadTicket t = read_open(bytes);
-    const int words = (int)(bytes / 4);
-    {
-      LaunchScope ls("host_read", 0.0, 2.0 * bytes);
-      publish_kernel<<<1, words < 256 ? 32 * ((words + 31) / 32) : 256, 0, c->stream>>>(
-          static_cast<const unsigned*>(dev), t.dst, words, t.flag, t.value);
-    }
+    read_publish(dev, bytes, t);
     read_close(host, bytes, t);
     return;
   }

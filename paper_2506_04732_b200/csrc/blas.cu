@@ -137,6 +137,32 @@ __global__ void copy_and_scaled_kernel(double* d1, int ldd1, const double* s1, i
   }
 }
 
+// The three data movements that finish a split, blockIdx.y = 0, 1, 2 (see
+// SplitFinish in blas.h); each element gets the arithmetic of copy_scaled /
+// copy2d_pair / fill.
+__global__ void split_finish_kernel(const __grid_constant__ SplitFinish a) {
+  const int stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.y == 0) {
+    const int n = a.rows0 * a.cols0;
+    for (int e = t0; e < n; e += stride) {
+      const int r = e / a.cols0, c = e - r * a.cols0;
+      double v = a.s0[(long long)r * a.lds0 + c];
+      if (a.rs) v *= a.rs[r];
+      if (a.cs) v *= a.cs[c];
+      a.d0[(long long)r * a.ldd0 + c] = v;
+    }
+  } else if (blockIdx.y == 1) {
+    const int cols = a.c1 + a.c2, n = a.rows1 * cols;
+    for (int e = t0; e < n; e += stride) {
+      const int r = e / cols, c = e - r * cols;
+      a.d1[(long long)r * a.ldd1 + c] =
+          c < a.c1 ? a.a1[(long long)r * a.lda1 + c] : a.b1[(long long)r * a.ldb1 + c - a.c1];
+    }
+  } else {
+    for (long long e = t0; e < a.n2; e += stride) a.d2[e] = 0.0;
+  }
+}
+
 __global__ void copy2d_pair_kernel(double* dst, int ldd, const double* s1, int ld1, int c1,
                                    const double* s2, int ld2, int c2, int rows) {
   const int cols = c1 + c2, n = rows * cols;
@@ -608,6 +634,19 @@ void copy_and_scaled(double* d1, int ldd1, const double* s1, int lds1, int r1, i
     LaunchScope ls("vector", (double)n2, 16.0 * (n1 + n2));
     copy_and_scaled_kernel<<<dim3(grid_for(n1 > n2 ? n1 : n2), 2), 256, 0, stream()>>>(
         d1, ldd1, s1, lds1, r1, c1, d2, ldd2, s2, lds2, r2, c2, rs);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+void split_finish(const SplitFinish& a) {
+  const long long n0 = (long long)a.rows0 * a.cols0, n1 = (long long)a.rows1 * (a.c1 + a.c2);
+  long long most = n0 > n1 ? n0 : n1;
+  most = a.n2 > most ? a.n2 : most;
+  if (most <= 0) return;
+  T2S2_REQUIRE(n0 < (1LL << 31) && n1 < (1LL << 31), kErrShape, "split_finish: block too large");
+  {
+    LaunchScope ls("vector", (double)n0, 16.0 * (n0 + n1) + 8.0 * a.n2);
+    split_finish_kernel<<<dim3(grid_for(most), a.n2 > 0 ? 3 : 2), 256, 0, stream()>>>(a);
   }
   T2S2_CHECK_LAUNCH();
 }

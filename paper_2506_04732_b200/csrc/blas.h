@@ -124,6 +124,24 @@ void copy_scaled(double* dst, int ldd, const double* src, int lds, int rows, int
 // copy2d(d1 <- s1, r1 x c1) and copy_scaled(d2 <- s2 with row scales rs, r2 x c2) in one launch
 void copy_and_scaled(double* d1, int ldd1, const double* s1, int lds1, int r1, int c1, double* d2,
                      int ldd2, const double* s2, int lds2, int r2, int c2, const double* rs);
+// The data movements that finish a split of a solved core, in ONE launch:
+//   0: d0[i, j] = s0[i, j] * rs[i] * cs[j]   (rows0 x cols0; a null scale is 1)
+//   1: d1[r, :c1] = a1[r, :c1], d1[r, c1:c1+c2] = b1[r, :c2]   (rows1 rows)
+//   2: d2[0 .. n2) = 0
+struct SplitFinish {
+  double* d0;
+  const double* s0;
+  int ldd0, lds0, rows0, cols0;
+  const double* rs;
+  const double* cs;
+  double* d1;
+  const double* a1;
+  const double* b1;
+  int ldd1, lda1, ldb1, c1, c2, rows1;
+  double* d2;
+  long long n2;
+};
+void split_finish(const SplitFinish& a);
 // dst[:, :c1] = s1, dst[:, c1:c1+c2] = s2 (rows x ...), one launch
 void copy2d_pair(double* dst, int ldd, const double* s1, int ld1, int c1, const double* s2, int ld2,
                  int c2, int rows);

@@ -146,6 +146,7 @@ struct ReadTicket {
   unsigned value = 0;
 };
 ReadTicket read_open(size_t bytes);
+void read_publish(const void* dev, size_t bytes, const ReadTicket& t);  // a separate publish launch
 void read_close(void* host, size_t bytes, const ReadTicket& t);
 // up to four device segments (pointer, doubles) read back as one array with one kernel
 void host_read_gather(double* host, std::initializer_list<std::pair<const double*, size_t>> parts);
@@ -226,6 +227,12 @@ struct Train {
     return m;
   }
   Train clone() const;
+  // The solver's (m, A, a, n) layout of an operator's cores (als.cu), kept
+  // with the train so that a march permutes its left operator once, not once
+  // per step; valid while layout_of[l] == cores[l].p (trains are not edited
+  // in place).  Not copied by clone().
+  mutable std::vector<DTensor> solver_layout;
+  mutable std::vector<const double*> layout_of;
 };
 
 }  // namespace t2s2

@@ -455,7 +455,8 @@ __global__ void __launch_bounds__(kQrThreads)
 //          barriers); U' = Q Ur through shared memory.
 template <int RPL, int NPX>
 __global__ void __launch_bounds__(512)
-    svd_warp_kernel(int m, int n, const double* __restrict__ A, double* U, double* s, double* Vt) {
+    svd_warp_kernel(int m, int n, const double* __restrict__ A, double* U, double* s, double* Vt,
+                    ReadTicket pub) {
   extern __shared__ double wsm[];
   const bool tr = m < n;
   const int mp = tr ? n : m, np = tr ? m : n;
@@ -649,6 +650,13 @@ __global__ void __launch_bounds__(512)
   __syncthreads();
   SVD_T(3)
   for (int j = tid; j < np; j += blockDim.x) s[j] = ssv[j];
+  if (pub.dst) {
+    // the host decides the rank from s: publish it now, U and Vt follow
+    if (tid < 2 * np) pub.dst[tid] = reinterpret_cast<const unsigned*>(ssv)[tid];
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) *(volatile unsigned*)pub.flag = pub.value;
+  }
   // U' = Q Ur (mp x np); V' = V[:, perm]
   if (!tr) {
     for (int e = tid; e < m * n; e += blockDim.x) {
@@ -678,9 +686,9 @@ __global__ void __launch_bounds__(512)
 
 template <int RPL, int NPX>
 void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double* Vt, size_t smem,
-                     int thr) {
+                     int thr, const ReadTicket& pub) {
   max_dynamic_smem((const void*)svd_warp_kernel<RPL, NPX>, (int)kSmemCap);
-  svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt);
+  svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt, pub);
 }
 
 // Householder QR of a tall block (m rows <= 32 * RPL, n <= 32 * CPW columns,
@@ -1062,7 +1070,9 @@ void svd_tall(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
 
 }  // namespace
 
-void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt) {
+namespace {
+void svd_thin_run(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt, const ReadTicket* pub,
+                  bool& published) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
   {
     const int mp = m >= n ? m : n, np = m >= n ? n : m;
@@ -1075,12 +1085,14 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
       {
         LaunchScope ls("svd_jacobi", 4.0 * mp * (double)np * np, 8.0 * m * (double)n);
         const int thr = 32 * (np < 2 ? 2 : np);
+        const ReadTicket tk = pub ? *pub : ReadTicket{};
+        published = pub != nullptr;
         const int rpl = (mp + 31) / 32;
 #define T2S2_SVD_WARP(NPX)                                                            \
   do {                                                                            \
-    if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);   \
-    else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr); \
-    else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr);           \
+    if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk);   \
+    else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk); \
+    else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk);           \
   } while (0)
         if (np <= 4) T2S2_SVD_WARP(4);
         else if (np <= 8) T2S2_SVD_WARP(8);
@@ -1119,6 +1131,13 @@ void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
   transpose(Vt2.p, U.p, m, m);
   Vt = DTensor({m, n});
   transpose(U2.p, Vt.p, n, m);
+}
+}  // namespace
+
+void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt, const ReadTicket* pub) {
+  bool published = false;
+  svd_thin_run(m, n, A, U, s, Vt, pub, published);
+  if (pub && !published) read_publish(s.p, s.size() * sizeof(double), *pub);
 }
 
 }  // namespace t2s2

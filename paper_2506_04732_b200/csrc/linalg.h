@@ -19,7 +19,11 @@ void qr_r(int m, int n, const double* A, DTensor& R, bool cm = false);
 
 // Thin SVD A = U diag(s) Vt of a row-major m x n matrix, k = min(m, n),
 // singular values descending.  Tall case: QR, then one-sided Jacobi on R.
-void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt);
+// pub: an open read ticket (common.h) for the min(m, n) singular values —
+// the kernel that finishes s publishes it (as soon as s is known, before U
+// and Vt are written), other paths with a publish launch.
+void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt,
+              const ReadTicket* pub = nullptr);
 
 // In-place LU with partial pivoting of a column-major N x N matrix (ld=N);
 // ipiv 0-based row swaps; *info_dev = 0 or 1 + first zero pivot column.

@@ -196,10 +196,14 @@ Train tt_round(const Train& t, double tol, int max_rank) {
     const int r0 = c.dim(0), r1 = c.dim(-1);
     const int m = (int)((long long)c.size() / r1);
     DTensor U, s, Vt;
-    svd_thin(m, r1, c.p, U, s, Vt);
-    const int kk = s.dim(0);
+    const int kk = m < r1 ? m : r1;
     std::vector<double> hs(kk);
-    to_host(hs.data(), s.p, kk);
+    {
+      // the SVD kernel publishes the singular values itself
+      const ReadTicket tk = read_open(kk * sizeof(double));
+      svd_thin(m, r1, c.p, U, s, Vt, &tk);
+      read_close(hs.data(), kk * sizeof(double), tk);
+    }
     long long cap = cap_all < in_ranks[l + 1] ? cap_all : in_ranks[l + 1];
     int r = tail_keep(hs, delta);
     if (r > cap) r = (int)cap;
