@@ -5,10 +5,10 @@
 // The local systems of an implicit step (I + dt L projected on orthonormal
 // interface bases, tt_solver.py:350-362 solves them with numpy.linalg.solve)
 // are well conditioned and their diagonal pivots are large.  Every
-// multiplier is checked against kPivThresh = 1 (below): partial pivoting
-// makes no interchange exactly when all |l| <= 1, and then these are GEPP's
-// factors; if one exceeds it, or a pivot is zero, the kernel declines
-// (*info = -1) and the caller runs the partial-pivoting kernel.
+// multiplier is checked against kPivThresh (below, threshold partial
+// pivoting: no interchange while |l| <= 8); if one exceeds it, or a pivot is
+// zero, the kernel declines (*info = -1) and the caller runs the
+// partial-pivoting kernel.
 //
 // Panel p (rows/columns [k0, k1), k1 = k0 + 32), normalised block
 // Gauss-Jordan:
@@ -59,14 +59,20 @@ constexpr int kT = 64;         // tile rows / columns
 constexpr int kLdT = kT + 4;   // smem stride of 64-long columns
 constexpr int kLdP = kP + 4;   // smem stride of 32-long columns
 constexpr int kInv = 2 * kP * kP;  // per panel: D^{-1} then U^{-1}, column-major
-// Multiplier bound: kPivThresh = 1 is exactly "partial pivoting makes no
-// interchange", so an accepted solve has GEPP's factors (numpy.linalg.solve
-// is GEPP).  A threshold-pivoting bound (e.g. 10, u = 0.1 as sparse LU codes
-// use) would accept every config-2 system (max |l| <= 4 measured where GEPP
-// interchanges) and drop the ~3% fallbacks, but it moves the march onto a
-// different noise-level trajectory (measured: 27 -> 32 sweeps per 20 steps),
-// so the GEPP-equivalent bound is kept.
-constexpr double kPivThresh = 1.0;
+// Multiplier bound: threshold partial pivoting.  Elimination proceeds without
+// an interchange while every multiplier satisfies |l| <= kPivThresh (the
+// bound sparse LU codes use with u = 1 / kPivThresh); kPivThresh = 1 would be
+// exactly "GEPP makes no interchange".  Where GEPP does interchange on the
+// local systems of configs 2 and 3, the multipliers are <= 4 (measured), so
+// 8 accepts those solves here instead of sending ~3% of them to the pivoting
+// kernel at 3-4x the cost; a larger multiplier or a zero pivot still
+// declines.  Every candidate is scored by the solver afterwards
+// (tt_solver.py:383-399: a local solution that does not lower the residual
+// functional is discarded), and the full-length parity runs against ttss hold
+// with it: config 2 max 2.9e-10 (GEPP-equivalent bound: 3.3e-10), config 3
+// 1.4e-10 (2.0e-10), identical ranks at every step, 125 / 202 sweeps against
+// the reference's 132 / 200 (profiles/r02i_parity_full_*.json).
+constexpr double kPivThresh = 8.0;
 
 struct GjArgs {
   int N;
