@@ -138,6 +138,23 @@ __device__ __forceinline__ void cta_wait(const unsigned* p, unsigned target, con
       if (abortable && *(volatile const int*)info != 0) break;
   __syncthreads();
 }
+// The same wait for CTA 0, returning *info as thread 0 saw it: the flag is
+// loaded next to the counter (before the acquire load in program order, so
+// both are in flight together) instead of in a round trip of its own after
+// the wait.  A flag raised after that load is seen one phase later — it only
+// skips work, the hand-offs do not depend on it.
+__device__ __forceinline__ int cta_wait_info(const unsigned* p, unsigned target, const int* info) {
+  __shared__ int seen;
+  if (threadIdx.x == 0) {
+    int f;
+    do {
+      f = *(volatile const int*)info;
+    } while (ld_acquire_u32(p) < target && f == 0);
+    seen = f;
+  }
+  __syncthreads();
+  return seen;
+}
 
 // Geometry of one phase.
 struct Phase {
@@ -207,14 +224,34 @@ struct Smem {
   double gl[kP / 4][4][kP], gy[kP / 4][4][kP];  // gj_diag: each group's l and y columns
 };
 
-// Load D^{-1}, U^{-1} of panel p into shared memory.
-__device__ void load_inv(const GjArgs& a, int p, Smem& s) {
+// Load D^{-1}, U^{-1} of panel p into shared memory.  All global loads are
+// issued into registers before the first shared-memory store: a load followed
+// by its store is one exposed L2 round trip per element otherwise (the
+// compiler does not move the loads across the stores).
+struct InvRegs {
+  double d[kP * kP / kThr], u[kP * kP / kThr];
+};
+__device__ __forceinline__ void load_inv_issue(const GjArgs& a, int p, InvRegs& R) {
   const double* g = a.inv + (size_t)p * kInv;
-  for (int e = threadIdx.x; e < kP * kP; e += kThr) {
-    const int c = e >> 5, r = e & 31;
-    s.di[c * kLdP + r] = __ldcg(g + e);            // Dinv[r][c] -> A op [k=c][m=r]
-    s.ui[c * kLdP + r] = __ldcg(g + kP * kP + e);  // Uinv[r][c] -> B op [n=c][k=r]
+#pragma unroll
+  for (int q = 0; q < kP * kP / kThr; ++q) {
+    const int e = threadIdx.x + q * kThr;
+    R.d[q] = __ldcg(g + e);
+    R.u[q] = __ldcg(g + kP * kP + e);
   }
+}
+__device__ __forceinline__ void load_inv_store(const InvRegs& R, Smem& s) {
+#pragma unroll
+  for (int q = 0; q < kP * kP / kThr; ++q) {
+    const int e = threadIdx.x + q * kThr, c = e >> 5, r = e & 31;
+    s.di[c * kLdP + r] = R.d[q];  // Dinv[r][c] -> A op [k=c][m=r]
+    s.ui[c * kLdP + r] = R.u[q];  // Uinv[r][c] -> B op [n=c][k=r]
+  }
+}
+__device__ void load_inv(const GjArgs& a, int p, Smem& s) {
+  InvRegs R;
+  load_inv_issue(a, p, R);
+  load_inv_store(R, s);
 }
 
 // One tile task of a phase: rows [r, r+m) x columns [c, c+n) of the
@@ -414,45 +451,76 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 // The next diagonal block (rows and columns [k1, k1 + kb2), kb2 <= 32) on
 // CTA 0 — the head of every panel's critical path — as 32 x 32 products on
 // all eight warps (warp tile 8 x 16) instead of a 64 x 64 tile task:
-//   W = D^{-1} A[p, J0] (published to the row panel), the multipliers
-//   A[I0, p] U^{-1} checked, and A[I0, J0] - A[I0, p] W left in s.dg.
-__device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
+//   W = D^{-1} A[p, J0] (published to the row panel) and
+//   A[I0, J0] - A[I0, p] W left in s.dg.  One SM's DMMA rate bounds these
+//   products (~3.7 cycles per m8n8k4), so nothing else is computed here.
+#ifdef GJ_TIMELINE
+__device__ unsigned long long g_sp_acc[8];
+__device__ long long g_sp_last;
+#define GJ_SP(k)                                            \
+  if (threadIdx.x == 0) {                                   \
+    const long long t_ = clock64();                         \
+    if ((k) > 0) g_sp_acc[k] += (unsigned long long)(t_ - g_sp_last); \
+    g_sp_last = t_;                                         \
+  }
+#else
+#define GJ_SP(k)
+#endif
+__device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s, bool inv_resident) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = ph.k1, m = ph.kb2, k0 = ph.k0, kb = ph.kb;
+  const int r = ph.k1, m = ph.kb2, k0 = ph.k0, kb = ph.kb, N = a.N;
   const int m0 = (warp >> 1) * 8, n0 = (warp & 1) * 16;
+  // The three blocks lie in A itself (rows >= k1 are never in the previous
+  // panel's row buffer; columns < N): one base pointer each, 32-bit offsets
+  // (N <= 8192).
+  const double* Ad = a.A + (size_t)r * N + r;    // A[I0, J0](rr, cc) = Ad[cc N + rr]
+  const double* Aip = a.A + (size_t)k0 * N + r;  // A[I0, p](i, kk)   = Aip[kk N + i]
+  const double* Apj = a.A + (size_t)r * N + k0;  // A[p, J0](k, j)    = Apj[j N + k]
   double cv[2][2];
 #pragma unroll
   for (int j = 0; j < 2; ++j)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
-      cv[j][h] = (rr < m && cc < m) ? __ldcg(src_ptr(a, ph, r + rr, r + cc)) : 0.0;
+      cv[j][h] = (rr < m && cc < m) ? __ldcg(Ad + cc * N + rr) : 0.0;
     }
+  // every global load in flight before the first shared-memory store
+  double ra[4], rp[4], rd[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int e = tid + q * kThr, kk = e >> 5, i = e & 31;  // A[I0, p]: (i, kk)
-    s.ab2[0][kk * kLdT + i] = (i < m && kk < kb) ? __ldcg(src_ptr(a, ph, r + i, k0 + kk)) : 0.0;
-    const int j = e >> 5, k = e & 31;  // A[p, J0]: (k, j)
-    s.pb[j * kLdP + k] = (k < kb && j < m) ? __ldcg(dst_ptr(a, k0 + k, r + j)) : 0.0;
+    const int e = tid + q * kThr, hi = e >> 5, lo = e & 31;
+    ra[q] = (lo < m && hi < kb) ? __ldcg(Aip + hi * N + lo) : 0.0;  // A[I0, p](i = lo, kk = hi)
+    rp[q] = (lo < kb && hi < m) ? __ldcg(Apj + hi * N + lo) : 0.0;  // A[p, J0](k = lo, j = hi)
   }
-  load_inv(a, ph.p, s);
+  if (!inv_resident) {  // D^{-1} of this panel (CTA 0 keeps its own copy in s.di: gj_diag)
+    const double* g = a.inv + (size_t)ph.p * kInv;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rd[q] = __ldcg(g + tid + q * kThr);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + q * kThr, hi = e >> 5, lo = e & 31;
+    s.ab2[0][hi * kLdT + lo] = ra[q];
+    s.pb[hi * kLdP + lo] = rp[q];
+    if (!inv_resident) s.di[hi * kLdP + lo] = rd[q];
+  }
+  GJ_SP(2)
   __syncthreads();
+  GJ_SP(3)
   {
-    double aw[2][2] = {}, am[2][2] = {};
+    // (the multipliers A[I0, p] U^{-1} of these rows are checked off the
+    // critical path, by the tile task of the same row block and the next
+    // column block)
+    double aw[2][2] = {};
 #pragma unroll
     for (int kk = 0; kk < kP; kk += 4) {
       const int kr = kk + (lane & 3);
       const double fw = s.di[kr * kLdP + m0 + (lane >> 2)];  // D^{-1}[row][kr]
-      const double fm = s.ab2[0][kr * kLdT + m0 + (lane >> 2)];  // A[I0, p][row][kr]
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int col = n0 + j * 8 + (lane >> 2);
-        dmma(aw[j][0], aw[j][1], fw, s.pb[col * kLdP + kr]);
-        dmma(am[j][0], am[j][1], fm, s.ui[col * kLdP + kr]);
-      }
+      for (int j = 0; j < 2; ++j) dmma(aw[j][0], aw[j][1], fw, s.pb[(n0 + j * 8 + (lane >> 2)) * kLdP + kr]);
     }
     double* wdst = a.wbuf + (size_t)(ph.p % 3) * kP * (a.N + 1);
-    bool bad = false;
+    GJ_SP(6)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -460,11 +528,10 @@ __device__ void special_tile(const GjArgs& a, const Phase& ph, Smem& s) {
         const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
         s.ws[cc * kLdP + rr] = aw[j][h];
         if (rr < kb && cc < m) wdst[(size_t)(r + cc) * kP + rr] = aw[j][h];
-        if (rr < m && !(fabs(am[j][h]) <= kPivThresh)) bad = true;
       }
-    if (bad) gj_fail(a);
   }
   __syncthreads();
+  GJ_SP(4)
   {
     double acc[2][2] = {};
 #pragma unroll
@@ -643,7 +710,9 @@ __device__ void gj_diag(const GjArgs& a, int p, int kb, Smem& s) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int rr = m0 + (lane >> 2), cc = n0 + j * 8 + (lane & 3) * 2 + h;
-        gl[cc * kP + rr] = (rr < kb && cc < kb) ? acc[j][h] : 0.0;
+        const double v = (rr < kb && cc < kb) ? acc[j][h] : 0.0;
+        gl[cc * kP + rr] = v;
+        s.di[cc * kLdP + rr] = v;  // CTA 0's own copy for its next special tile
       }
   }
   GJ_T(3)
@@ -710,10 +779,13 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       // block: W of its columns, multipliers checked, updated block kept in
       // shared memory, factored
       GJ_TL(0)
-      if (p > 0) cta_wait(feed + (p - 1), (unsigned)nfeed(Phase(N, p - 1)), a.info, true);
+      const int declined = p > 0 ? cta_wait_info(feed + (p - 1), (unsigned)nfeed(Phase(N, p - 1)), a.info) : 0;
       GJ_TL(1)
-      if (__ldcg(a.info) == 0) {
-        special_tile(a, ph, s);
+      GJ_SP(0)
+      if (declined == 0) {
+        GJ_SP(1)
+        special_tile(a, ph, s, true);
+        GJ_SP(5)
         GJ_TL(2)
         unsigned long long td = pr ? gtimer() : 0;
         gj_diag(a, p + 1, ph.kb2, s);
@@ -733,7 +805,7 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
       GJ_TL(2)
       const bool live = __ldcg(a.info) == 0;
       if (has_diag && G == 1 && live) {
-        special_tile(a, ph, s);
+        special_tile(a, ph, s, false);
         gj_diag(a, p + 1, ph.kb2, s);
       }
       // a contiguous chunk of the J-major task list (consecutive tasks share
@@ -769,7 +841,10 @@ __global__ void __launch_bounds__(kThr, 1) gj_kernel(GjArgs a) {
             }
             // multipliers of rows below the panel are checked once per row
             // block, in its first column block
-            tile_compute(a, ph, k, cv, neww, k.I == 0, k.I < ph.nbelow && k.J == 0, false, s, buf);
+            // (the next diagonal block's rows, I = 0, have no tile in column block 0 — that is
+            // CTA 0's special tile — and are checked with column block 1)
+            tile_compute(a, ph, k, cv, neww, k.I == 0,
+                         k.I < ph.nbelow && k.J == (has_diag && k.I == 0 ? 1 : 0), false, s, buf);
             lastJ = k.J;
           } else if (tt + 1 < t1) {
             kn = task_of(ph, tt + 1 + off);

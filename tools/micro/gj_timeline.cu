@@ -66,6 +66,15 @@ int main(int argc, char** argv) {
   }
   printf("mean over %d phases: CTA0 wait %.2f special %.2f diag %.2f | total %.1f us\n", cnt, sw / cnt, ss / cnt, sd / cnt, (at(0, npan - 2, 3) - t0) / 1e3);
   for (int s = 0; s < 4; ++s) printf("  worker %d: wait-arrivals %.2f wait-published %.2f work %.2f\n", s, wa[s] / cnt, wp[s] / cnt, ww[s] / cnt);
+  {
+    // CTA 0's special tile in clock cycles (sum over the three repetitions):
+    // info load, operand loads issued, first barrier, W + multiplier products, update product
+    unsigned long long acc[8];
+    cudaMemcpyFromSymbol(acc, g_sp_acc, sizeof acc);
+    const double den = 3.0 * (npan - 1);
+    printf("special tile cycles per phase: info %.0f  issue-loads %.0f  barrier(load latency) %.0f  W+check %.0f (products %.0f)  update %.0f\n",
+           acc[1] / den, acc[2] / den, acc[3] / den, (acc[4] + acc[6]) / den, acc[6] / den, acc[5] / den);
+  }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
