@@ -295,6 +295,7 @@ __device__ __forceinline__ const double* elem(const GjArgs& a, const RowSrc& rs,
 __device__ __forceinline__ void tile_load(const GjArgs& a, const Phase& ph, const Task& k, bool want_p,
                                           TileRegs& R) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
   const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
