@@ -40,10 +40,17 @@ constexpr int kGemmSmemWide = ring_bytes(64, kWideN, 16, kStages) > kGemmSmem
                                   ? ring_bytes(64, kWideN, 16, kStages)
                                   : kGemmSmem;
 
+// 8-byte async copy; !pred: the source is ignored and zeros are written
+// (the ignore-src predicate form: one LDGSTS.ZFILL, no size arithmetic)
 __device__ __forceinline__ void cp_async8(unsigned dst, const double* src, bool pred) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
-               "r"(pred ? 8 : 0)
-               : "memory");
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " setp.eq.u32 p, %2, 0;\n"
+      " cp.async.ca.shared.global [%0], [%1], 8, p;\n"
+      "}\n" ::"r"(dst),
+      "l"(src), "r"((unsigned)pred)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -110,6 +117,25 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
     bdst[t] = sbase + 8u * (unsigned)(SA + bkk[t] * LB + bj);
   }
   const int nk = (K + TK - 1) / TK;
+  // issue() runs for kt = 0, 1, 2, ... in order: each element keeps a running
+  // source pointer (advanced by one K-tile per call) and the number of
+  // K-tiles' worth of k it may still read, so a copy costs a compare, the
+  // copy and a pointer increment instead of a 64-bit multiply-add per call.
+  const double* ap[PA];
+  int alim[PA];
+#pragma unroll
+  for (int t = 0; t < PA; ++t) {
+    ap[t] = A + aoff[t];
+    alim[t] = (aval[t] && arow[t]) ? K - akk[t] : 0;  // copy while k0 < alim
+  }
+  const double* bp[PB];
+  int blim[PB];
+#pragma unroll
+  for (int t = 0; t < PB; ++t) {
+    bp[t] = B + boff[t];
+    blim[t] = (bval[t] && bcol[t]) ? K - bkk[t] : 0;
+  }
+  const long long astep = (long long)TK * g.ak, bstep = (long long)TK * g.bk;
   auto issue = [&](int kt) {  // K-tile kt into ring slot kt % ST (always commits a group)
     if (kt < nk) {
       const int k0 = kt * TK;
@@ -117,14 +143,16 @@ __device__ __forceinline__ void gemm_tile(const GemmProb& g, int bx, int by, int
 #pragma unroll
       for (int t = 0; t < PA; ++t) {
         if (!aval[t]) continue;
-        const bool ok = arow[t] && k0 + akk[t] < K;
-        cp_async8(adst[t] + so, ok ? A + aoff[t] + (long long)k0 * g.ak : A, ok);
+        const bool ok = k0 < alim[t];
+        cp_async8(adst[t] + so, ok ? ap[t] : A, ok);
+        ap[t] += astep;
       }
 #pragma unroll
       for (int t = 0; t < PB; ++t) {
         if (!bval[t]) continue;
-        const bool ok = bcol[t] && k0 + bkk[t] < K;
-        cp_async8(bdst[t] + so, ok ? B + boff[t] + (long long)k0 * g.bk : B, ok);
+        const bool ok = k0 < blim[t];
+        cp_async8(bdst[t] + so, ok ? bp[t] : B, ok);
+        bp[t] += bstep;
       }
     }
     cp_async_commit();

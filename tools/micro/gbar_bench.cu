@@ -57,6 +57,23 @@ __global__ void k_bar(int reps, long long* cyc, unsigned* ctr, unsigned* data, i
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / (2 * reps);
 }
 
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// one thread-block cluster = the whole grid; the hardware cluster barrier with release/acquire
+__global__ void k_cluster(int reps, long long* cyc, unsigned* data, int* bad) {
+  const unsigned G = gridDim.x, me = blockIdx.x;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (threadIdx.x == 0) data[me] = r + 1;
+    cluster_sync();
+    if (threadIdx.x == 32 && data[(me + 1) % G] != (unsigned)(r + 1)) atomicAdd(bad, 1);
+    cluster_sync();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (t1 - t0) / (2 * reps);
+}
+
 int main() {
   long long* cyc;
   unsigned *ctr, *data;
@@ -66,6 +83,27 @@ int main() {
   cudaMalloc(&data, 4 * 1024);
   cudaMalloc(&bad, 4);
   cudaMemset(bad, 0, 4);
+  cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int G : {2, 4, 8, 16}) {
+    int reps = 500;
+    long long hc = 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(256);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster, reps, cyc, data, bad);
+    cudaMemcpy(&hc, cyc, 8, cudaMemcpyDeviceToHost);
+    int hbad = 0;
+    cudaMemcpy(&hbad, bad, 4, cudaMemcpyDeviceToHost);
+    printf("cluster of %2d CTAs: barrier.cluster %5lld cycles   stale reads %d (%s / %s)\n", G, hc, hbad,
+           cudaGetErrorString(e), cudaGetErrorString(cudaGetLastError()));
+  }
   for (int G : {2, 6, 16, 40, 75, 148, 296}) {
     int reps = 500;
     long long hc = 0, hb = 0;

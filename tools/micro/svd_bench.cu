@@ -41,7 +41,7 @@ static void check(int m, int n, const std::vector<double>& A, double* dU, double
 int main(int argc, char** argv) {
   using namespace t2s2;
   const int shapes[][2] = {{66, 4}, {132, 8}, {264, 8}, {198, 11}, {231, 11}, {264, 16}, {8, 264},
-                           {33, 1}, {1, 33}, {4, 33}, {12, 66}, {100, 3}, {384, 16}, {16, 384}, {2, 50}, {33, 16}};
+                           {33, 1}, {1, 33}, {4, 33}, {12, 66}, {100, 3}, {384, 16}, {16, 384}, {2, 50}, {33, 16}, {132, 12}, {396, 12}, {627, 12}};
   for (auto& sh : shapes) {
     const int m = sh[0], n = sh[1];
     std::vector<double> h((size_t)m * n);
@@ -89,9 +89,9 @@ int main(int argc, char** argv) {
                       : (mp <= 128 ? svd_warp_kernel<4, 16> : mp <= 256 ? svd_warp_kernel<8, 16> : svd_warp_kernel<12, 16>);
     cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
     const int thr = 32 * (np < 2 ? 2 : np);
-    for (int w = 0; w < 3; ++w) wk<<<1, thr, wneed>>>(m, n, A, U, s, Vt);
+    for (int w = 0; w < 3; ++w) wk<<<1, thr, wneed>>>(m, n, A, U, s, Vt, t2s2::ReadTicket{});
     cudaEventRecord(e0);
-    for (int w = 0; w < reps; ++w) wk<<<1, thr, wneed>>>(m, n, A, U, s, Vt);
+    for (int w = 0; w < reps; ++w) wk<<<1, thr, wneed>>>(m, n, A, U, s, Vt, t2s2::ReadTicket{});
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms2;
