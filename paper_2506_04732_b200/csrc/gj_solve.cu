@@ -292,11 +292,37 @@ __device__ __forceinline__ const double* elem(const GjArgs& a, const RowSrc& rs,
   return (c == a.N && !rs.buf) ? a.b + r : rs.base + (size_t)c * rs.stride;
 }
 
+// A full 64 x 64 tile of matrix columns whose rows are not in the previous
+// panel's row buffer, under a full panel: every address is tile origin +
+// per-thread constant (+ a multiple of N), no predicates — the path of almost
+// every task of a large system (the general path spends ~19 instructions of
+// address arithmetic, predicates and reconvergence per DMMA,
+// profiles/r02i_gj_sizes.ncu-rep).
+__device__ __forceinline__ bool task_interior(const GjArgs& a, const Phase& ph, const Task& k) {
+  return k.m == kT && k.n == kT && k.c + kT <= a.N && ph.kb == kP &&
+         (ph.kprev < 0 || k.r >= ph.k0 || k.r + kT <= ph.kprev);
+}
+
 __device__ __forceinline__ void tile_load(const GjArgs& a, const Phase& ph, const Task& k, bool want_p,
                                           TileRegs& R) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
   const int wm0 = (warp >> 2) * 32, wn0 = (warp & 3) * 16;
+  if (!want_p && task_interior(a, ph, k)) {
+    const int N = a.N;
+    const double* ct = a.A + (size_t)k.c * N + k.r + (wn0 + (lane & 3) * 2) * N + wm0 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* pc = ct + (j * 8 + h) * N;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) R.cv[i][j][h] = __ldcg(pc + i * 8);
+      }
+    const double* ap = a.A + (size_t)ph.k0 * N + k.r + (tid >> 6) * N + (tid & 63);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) R.ab[q] = __ldcg(ap + q * 4 * N);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int rr = wm0 + i * 8 + (lane >> 2);
@@ -428,21 +454,34 @@ __device__ void tile_compute(const GjArgs& a, const Phase& ph, const Task& k, co
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
+    if (!to_diag && task_interior(a, ph, k)) {
+      const int N = a.N;
+      double* ct = a.A + (size_t)k.c * N + k.r + (wn0 + (lane & 3) * 2) * N + wm0 + (lane >> 2);
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int rr = wm0 + i * 8 + (lane >> 2), cc = wn0 + j * 8 + (lane & 3) * 2 + h;
-          if (rr < k.m && cc < k.n) {
-            const double v = cv[i][j][h] - acc[i][j][h];
-            if (to_diag)
-              s.dg[cc * 33 + rr] = v;
-            else
-              *dst_ptr(a, k.r + rr, k.c + cc) = v;
-          }
+          double* pc = ct + (j * 8 + h) * N;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pc[i * 8] = cv[i][j][h] - acc[i][j][h];
         }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int rr = wm0 + i * 8 + (lane >> 2), cc = wn0 + j * 8 + (lane & 3) * 2 + h;
+            if (rr < k.m && cc < k.n) {
+              const double v = cv[i][j][h] - acc[i][j][h];
+              if (to_diag)
+                s.dg[cc * 33 + rr] = v;
+              else
+                *dst_ptr(a, k.r + rr, k.c + cc) = v;
+            }
+          }
+    }
   }
   // no closing barrier: the next task stages into the other s.ab2 buffer,
   // and s.pb / s.ws are rewritten only after the next staging barrier, which

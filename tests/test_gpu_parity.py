@@ -249,6 +249,33 @@ def test_dense_local_solve_late_interchange(pk):
     assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
 
 
+@pytest.mark.parametrize("row", [201, 230, 290])
+@pytest.mark.parametrize("mult,pivots", [(3.0, False), (20.0, True)])
+def test_dense_local_solve_threshold_pivoting(pk, row, mult, pivots):
+    """Threshold partial pivoting of the Gauss-Jordan kernel (|l| <= 8): one
+    sub-diagonal entry of column 200 is `mult` times the diagonal, in the same
+    32-row diagonal block (row 201), in the next diagonal block's rows (230 —
+    checked by a worker's tile task) or further below (290).  A multiplier of 3
+    is eliminated without an interchange on the Gauss-Jordan kernel alone, 20
+    declines to the pivoting kernel; both to LAPACK's accuracy."""
+    from paper_2506_04732_b200 import _native
+
+    rng = np.random.default_rng(11)
+    n = 420
+    a = rng.standard_normal((n, n))
+    a += np.diag(np.abs(a).sum(0))
+    a[row, 200] = mult * a[200, 200]
+    b = rng.standard_normal(n)
+    _native.stats_reset()
+    x = _native.dense_solve(a, b)
+    st = _native.stats_read()
+    assert st["gj_nopivot"]["launches"] == 1
+    assert st.get("lu_fused", {}).get("launches", 0) == (1 if pivots else 0)
+    want = np.linalg.solve(a, b)
+    assert np.linalg.norm(x - want) <= 1e-14 * np.linalg.cond(a) * np.linalg.norm(want)
+    assert np.linalg.norm(a @ x - b) <= 1e-13 * np.linalg.norm(a) * np.linalg.norm(x)
+
+
 @pytest.mark.parametrize("ta,tb,m,n,k", [
     (0, 0, 37, 29, 13), (1, 0, 64, 65, 70), (0, 1, 130, 64, 132), (1, 1, 33, 40, 9),
     (0, 0, 2112, 64, 1024),  # split-K with a reduce stage
