@@ -702,7 +702,8 @@ void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double
 // [b*n, (b+1)*n) of the output.  A, Q column-major when cm, else row-major.
 template <int RPL, int CPW, bool WANTQ>
 __global__ void __launch_bounds__(512)
-    wqr_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Q, double* R, int cm) {
+    wqr_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Q, double* R, int cm,
+               const double* __restrict__ P, int pr, double* NP) {
   extern __shared__ double qsm2[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int r0 = blockIdx.x * chunk;
@@ -860,20 +861,46 @@ __global__ void __launch_bounds__(512)
       }
     }
   }
+  // Absorb R into the neighbouring core, NP (pr x k) = P (pr x n) R^T (one
+  // block, m >= n): the GEMM that followed this kernel in the
+  // orthonormalisation sweep, with its arithmetic — each 8 x 8 block of NP
+  // is the DMMA m8n8k4 chain over k = 0, 4, 8, ... from a zero accumulator
+  // (trailing k zero filled), exactly the GEMM tile engine's sequence.
+  if (P) {
+    const int rb = (pr + 7) / 8, cb = (k + 7) / 8;
+    for (int blk = warp; blk < rb * cb; blk += nw) {
+      const int i = (blk / cb) * 8 + (lane >> 2), j = (blk % cb) * 8 + (lane >> 2);
+      double d0 = 0.0, d1 = 0.0;
+      for (int kk = 0; kk < n; kk += 4) {
+        const int kc = kk + (lane & 3);
+        const double av = (i < pr && kc < n) ? P[(size_t)i * n + kc] : 0.0;
+        const double bv = (j < k && kc < n && kc >= j) ? Rs[(size_t)kc * n + j] : 0.0;  // R[j][kc]
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                     : "+d"(d0), "+d"(d1)
+                     : "d"(av), "d"(bv));
+      }
+      const int oc = (blk % cb) * 8 + (lane & 3) * 2;
+      if (i < pr) {
+        if (oc < k) NP[(size_t)i * k + oc] = d0;
+        if (oc + 1 < k) NP[(size_t)i * k + oc + 1] = d1;
+      }
+    }
+  }
 }
 
 template <int RPL, int CPW, bool WANTQ>
 void launch_wqr(int blocks, int thr, size_t smem, int m, int n, int chunk, const double* A, double* Q,
-                double* R, int cm) {
+                double* R, int cm, const double* P, int pr, double* NP) {
   max_dynamic_smem((const void*)wqr_kernel<RPL, CPW, WANTQ>, (int)kSmemCap);
-  wqr_kernel<RPL, CPW, WANTQ><<<blocks, thr, smem, stream()>>>(m, n, chunk, A, Q, R, cm);
+  wqr_kernel<RPL, CPW, WANTQ><<<blocks, thr, smem, stream()>>>(m, n, chunk, A, Q, R, cm, P, pr, NP);
 }
 
 // Dispatch: at most 16 warps, CPW = ceil(n / 16) columns each (1, 2 or 4);
 // rows per block <= 384 (<= 256 with four columns per warp, registers);
 // false if not applicable.
 template <bool WANTQ>
-bool wqr(int blocks, int m, int n, int chunk, const double* A, double* Q, double* R, int cm) {
+bool wqr(int blocks, int m, int n, int chunk, const double* A, double* Q, double* R, int cm,
+         const double* P = nullptr, int pr = 0, double* NP = nullptr) {
   const int rows = chunk < m ? chunk : m;
   const int cpw = n <= 16 ? 1 : (n <= 32 ? 2 : 4);
   if (n < 1 || n > 64 || rows > (cpw == 4 ? 256 : 384)) return false;
@@ -882,7 +909,7 @@ bool wqr(int blocks, int m, int n, int chunk, const double* A, double* Q, double
   const int thr = 32 * (nw < 2 ? 2 : nw);
   const size_t smem = ((size_t)rows * n + (size_t)n * n + n) * sizeof(double);
   if (smem > kSmemCap) return false;
-#define T2S2_WQR(R_, C_) launch_wqr<R_, C_, WANTQ>(blocks, thr, smem, m, n, chunk, A, Q, R, cm)
+#define T2S2_WQR(R_, C_) launch_wqr<R_, C_, WANTQ>(blocks, thr, smem, m, n, chunk, A, Q, R, cm, P, pr, NP)
   if (cpw == 1) {
     if (rpl <= 4) T2S2_WQR(4, 1);
     else if (rpl <= 8) T2S2_WQR(8, 1);
@@ -961,6 +988,11 @@ void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
 }
 
 void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
+  qr_thin_absorb(m, n, A, Q, R, cm, nullptr, 0, nullptr);
+}
+
+bool qr_thin_absorb(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm, const double* P, int pr,
+                    double* NP) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "qr_thin: empty matrix");
   const int k = m < n ? m : n;
   Q = DTensor({m, k});
@@ -968,14 +1000,20 @@ void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm) {
   if (m >= n && m <= (n > 32 ? 256 : 384) && n <= 64) {
     bool ok;
     {
-      LaunchScope ls("qr", 4.0 * m * (double)n * k, 16.0 * m * (double)n);
-      ok = wqr<true>(1, m, n, m, A, Q.p, R.p, cm ? 1 : 0);
+      LaunchScope ls("qr", 4.0 * m * (double)n * k + 2.0 * pr * (double)n * k, 16.0 * m * (double)n);
+      ok = wqr<true>(1, m, n, m, A, Q.p, R.p, cm ? 1 : 0, P, pr, NP);
     }
     if (ok) {
       T2S2_CHECK_LAUNCH();
-      return;
+      return P != nullptr;
     }
   }
+  qr_thin_general(m, n, A, Q, R, cm, k);
+  return false;
+}
+
+// the paths beyond the one-CTA warp kernel (Q and R allocated by the caller)
+void qr_thin_general(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm, int k) {
   // tall blocks that do not fit the one-CTA shared-memory kernel (config-4
   // cores, 33*64 x 64): TSQR with Q — warp-level leaves, the stacked leaf
   // R factors factored recursively (Q2, R), Q = diag(Q_leaf) Q2 as one

@@ -12,6 +12,13 @@ namespace t2s2 {
 // the LAPACK dgeqrf/dorgqr convention.
 // cm: A (m x n) and Q (m x k) column-major instead.
 void qr_thin(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm = false);
+// The same, and NP (pr x k, row-major) = P (pr x n, row-major) R^T from the
+// QR kernel itself when the one-CTA warp kernel applies (m >= n): returns
+// whether NP was written — otherwise the caller multiplies.  The product has
+// the GEMM engine's arithmetic (DMMA chain over k from a zero accumulator).
+bool qr_thin_absorb(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm, const double* P, int pr,
+                    double* NP);
+void qr_thin_general(int m, int n, const double* A, DTensor& Q, DTensor& R, bool cm, int k);
 
 // R factor only (k x n, k = min(m, n)) of a row-major m x n matrix; tall
 // inputs are reduced by a TSQR tree of shared-memory Householder leaves.

@@ -130,14 +130,16 @@ static std::vector<DTensor> right_orthonormalized(const std::vector<DTensor>& in
     // the row-major r0 x rows unfolding is the column-major rows x r0 matrix
     // whose QR we need; Q comes back column-major = the new core row-major
     DTensor Q, R;
-    qr_thin(rows, r0, c.p, Q, R, true);  // Q rows x k (column-major), R k x r0
     const int k = rows < r0 ? rows : r0;
-    DTensor nc = std::move(Q);
-    nc.view(with_bonds(c, k, r1));
     const DTensor& p = in[l - 1];
     const int pr = (int)((long long)p.size() / r0);
     DTensor np(with_bonds(p, p.dim(0), k));
-    gemm(false, true, pr, k, r0, 1.0, p.p, r0, R.p, r0, 0.0, np.p, k);
+    // Q rows x k (column-major), R k x r0; the QR kernel multiplies R into
+    // the neighbouring core itself when it is the one-CTA warp kernel
+    if (!qr_thin_absorb(rows, r0, c.p, Q, R, true, p.p, pr, np.p))
+      gemm(false, true, pr, k, r0, 1.0, p.p, r0, R.p, r0, 0.0, np.p, k);
+    DTensor nc = std::move(Q);
+    nc.view(with_bonds(c, k, r1));
     out[l] = std::move(nc);
     absorbed = std::move(np);
   }
