@@ -159,16 +159,17 @@ __global__ void normal_diag_kernel(int rx, int ra, int n, int ry, int rb,
 __global__ void probe_kernel(const double* __restrict__ u, const double* __restrict__ nu,
                              const double* __restrict__ c, int n, double* part,
                              unsigned* ticket, double* out, const double* buf, ReadTicket rt,
-                             int* zero_info) {
+                             int* zero_info, double* gout) {
   // (zero_info: the solver flags behind the probe slots are cleared for the
   // solve that follows this probe — no memset on the stream)
   if (zero_info && blockIdx.x == 0 && threadIdx.x < 2) zero_info[threadIdx.x] = 0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const double x = u[i];
-    s0 = fma(x, nu[i], s0);
-    s1 = fma(c[i], x, s1);
+    const double x = u[i], v = nu[i], ci = c[i];
+    s0 = fma(x, v, s0);
+    s1 = fma(ci, x, s1);
     s2 += isfinite(x) ? 0.0 : 1.0;
+    if (gout) gout[i] = v - ci;  // the candidate's residual gradient N u - c (update())
   }
   __shared__ double red[3][32];
   for (int o = 16; o > 0; o >>= 1) {
@@ -595,9 +596,11 @@ struct Probe {
   ReadTicket open;  // the last probe launch publishes the buffer itself
   bool is_open = false;
   // then_read: read() follows this launch with nothing that reads in between
+  // grad: also write N u - c (the projected residual gradient of this candidate)
   void run(int slot, const DTensor& u, const DTensor& nu, const DTensor& c, bool then_read,
-           bool zero_info = false) {
+           bool zero_info = false, DTensor* grad = nullptr) {
     const int n = (int)u.size();
+    if (grad) *grad = DTensor(u.shape);
     if (then_read) {
       open = read_open(16 * sizeof(double));
       is_open = true;
@@ -608,7 +611,8 @@ struct Probe {
     {
       LaunchScope ls("reduce", 4.0 * n, 24.0 * n);
       probe_kernel<<<nb, 256, 0, stream()>>>(u.p, nu.p, c.p, n, part, ticket(), buf.p + 3 * slot, buf.p,
-                                             then_read ? open : ReadTicket{}, zero_info ? info() : nullptr);
+                                             then_read ? open : ReadTicket{}, zero_info ? info() : nullptr,
+                                             grad ? grad->p : nullptr);
     }
     T2S2_CHECK_LAUNCH();
     allocator().release(part);
@@ -656,31 +660,6 @@ int count_significant(const std::vector<double>& zs) {
   return nz;
 }
 
-// Truncation rank of a split on the device (tt_solver.py:249-258, 268-270):
-// delta = rounding_tol * ||s|| / sqrt(max(d-1, 1)), keep = first k with
-// ||s[k:]|| <= delta (at least 1), capped at max_rank; mask[j] = j < keep.
-// Products and sums are rounded separately, in the reference's order.  One
-// thread: s has at most a few dozen entries.
-__global__ void split_keep_kernel(const double* s, int n, double tol, double rootd, int max_rank,
-                                  double* keep_out, double* mask) {
-  if (threadIdx.x != 0) return;
-  double nrm = 0.0;
-  for (int k = 0; k < n; ++k) nrm = __dadd_rn(nrm, __dmul_rn(s[k], s[k]));
-  const double delta = tol * sqrt(nrm) / rootd;
-  int r = n;
-  double acc = 0.0;
-  // tails from the back; keep the FIRST k with tail <= delta
-  for (int k = n - 1; k >= 0; --k) {
-    acc = __dadd_rn(acc, __dmul_rn(s[k], s[k]));
-    if (sqrt(acc) <= delta) r = k;
-  }
-  if (n == 0) r = 1;
-  if (r < 1) r = 1;
-  if (r > max_rank) r = max_rank;
-  keep_out[0] = (double)r;
-  for (int j = 0; j < n; ++j) mask[j] = j < r ? 1.0 : 0.0;
-}
-
 // Split of a solved core with enrichment from the residual gradient
 // (tt_solver.py:261-302).  The truncation rank is decided on the device and
 // the projection of the gradient is masked with it, so the core's singular
@@ -689,12 +668,11 @@ __global__ void split_keep_kernel(const double* s, int n, double tol, double roo
 struct SplitSync {
   DTensor keep_mask;  // [0] = keep, [1..kk] = mask
   int kk;
-  SplitSync(const DTensor& s, const SolverConfig& cfg, int d) : keep_mask({1 + s.dim(0)}), kk(s.dim(0)) {
-    LaunchScope ls("reduce", 0, 0);
-    split_keep_kernel<<<1, 32, 0, stream()>>>(s.p, kk, cfg.rounding_tol,
-                                              std::sqrt((double)(d - 1 > 1 ? d - 1 : 1)),
-                                              cfg.max_rank, keep_mask.p, keep_mask.p + 1);
-    T2S2_CHECK_LAUNCH();
+  KeepArgs args;
+  // kk = min(m, n) of the core's unfolding; the SVD kernel fills keep_mask (svd_thin's keep argument)
+  SplitSync(int kk_, const SolverConfig& cfg, int d) : keep_mask({1 + kk_}), kk(kk_) {
+    args = KeepArgs{cfg.rounding_tol, std::sqrt((double)(d - 1 > 1 ? d - 1 : 1)), cfg.max_rank, keep_mask.p,
+                    keep_mask.p + 1};
   }
   const double* mask() const { return keep_mask.p + 1; }
   // read keep, s and (optionally) zs together
@@ -714,10 +692,10 @@ Split split_forward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, in
                     const DTensor* neighbour = nullptr) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), m = r0 * n;
   DTensor U, s, Vt;
-  svd_thin(m, r1, u.p, U, s, Vt);
+  const int kk = m < r1 ? m : r1;
+  SplitSync sync(kk, cfg, d);
+  svd_thin(m, r1, u.p, U, s, Vt, nullptr, &sync.args);  // and the truncation rank
   trace_buffer("split_forward s", s.p, s.size());
-  const int kk = s.dim(0);
-  SplitSync sync(s, cfg, d);
   const bool enrich = cfg.enrichment_rank > 0 && grad;
   DTensor zu, zs, zvt;
   int zk = 0;
@@ -766,10 +744,10 @@ Split split_backward(const DTensor& u, DTensor* grad, const SolverConfig& cfg, i
                      const DTensor* neighbour = nullptr) {
   const int r0 = u.dim(0), n = u.dim(1), r1 = u.dim(2), cols = n * r1;
   DTensor U, s, Vt;
-  svd_thin(r0, cols, u.p, U, s, Vt);  // U r0 x kk, Vt kk x cols
+  const int kk = r0 < cols ? r0 : cols;
+  SplitSync sync(kk, cfg, d);
+  svd_thin(r0, cols, u.p, U, s, Vt, nullptr, &sync.args);  // U r0 x kk, Vt kk x cols; and the rank
   trace_buffer("split_backward s", s.p, s.size());
-  const int kk = s.dim(0);
-  SplitSync sync(s, cfg, d);
   const bool enrich = cfg.enrichment_rank > 0 && grad;
   DTensor zu, zs, zvt;
   if (enrich) {
@@ -914,6 +892,7 @@ struct Sweep {
     const bool try_gal = gal_rejects < gal_cap;
     gal_direct = try_gal && direct;
     DTensor u_gal, nu_gal;
+    DTensor g_gal;  // N u_gal - c_ls, written by the Galerkin candidate's probe
     if (try_gal) {
       if (direct) {
         DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
@@ -928,7 +907,7 @@ struct Sweep {
       u_gal.view(u_old.shape);
       trace_buffer("update u_gal", u_gal.p, u_gal.size());
       nu_gal = nop.apply(u_gal);
-      probe.run(1, u_gal, nu_gal, c_ls, true);
+      probe.run(1, u_gal, nu_gal, c_ls, true, false, &g_gal);
     }
     double h[12];
     int info = 0, swapped = 0;
@@ -941,7 +920,7 @@ struct Sweep {
       dense_solve_pivoted(B, c_gal, u_gal, probe.info());
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
-      probe.run(1, u_gal, nu_gal, c_ls, true);
+      probe.run(1, u_gal, nu_gal, c_ls, true, false, &g_gal);
       probe.read(h, &info);
     }
     if (try_gal && direct && info != 0) {
@@ -951,7 +930,7 @@ struct Sweep {
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
       probe.clear_info();
-      probe.run(1, u_gal, nu_gal, c_ls, true);
+      probe.run(1, u_gal, nu_gal, c_ls, true, false, &g_gal);
       probe.read(h, &info);
     }
     const double q_old = h[0] - 2.0 * h[1];
@@ -1027,9 +1006,14 @@ struct Sweep {
       best = u_old.clone();
       nu_best = std::move(nu_old);
     }
-    // projected residual gradient N u - c steers the enrichment
-    grad = std::move(nu_best);
-    daxpy(-1.0, c_ls.p, grad.p, grad.size());
+    // projected residual gradient N u - c steers the enrichment (for the
+    // Galerkin candidate its probe has written it already)
+    if (choice == 1) {
+      grad = std::move(g_gal);
+    } else {
+      grad = std::move(nu_best);
+      daxpy(-1.0, c_ls.p, grad.p, grad.size());
+    }
   }
 };
 

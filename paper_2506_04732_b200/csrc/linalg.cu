@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kQrThreads)
 template <int RPL, int NPX>
 __global__ void __launch_bounds__(512)
     svd_warp_kernel(int m, int n, const double* __restrict__ A, double* U, double* s, double* Vt,
-                    ReadTicket pub) {
+                    ReadTicket pub, KeepArgs keep) {
   extern __shared__ double wsm[];
   const bool tr = m < n;
   const int mp = tr ? n : m, np = tr ? m : n;
@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(512)
   __syncthreads();
   SVD_T(3)
   for (int j = tid; j < np; j += blockDim.x) s[j] = ssv[j];
+  if (keep.keep_out && tid == 32) split_keep_device(ssv, np, keep);  // the split's rank (one thread)
   if (pub.dst) {
     // the host decides the rank from s: publish it now, U and Vt follow
     if (tid < 2 * np) pub.dst[tid] = reinterpret_cast<const unsigned*>(ssv)[tid];
@@ -686,9 +687,13 @@ __global__ void __launch_bounds__(512)
 
 template <int RPL, int NPX>
 void launch_svd_warp(int m, int n, const double* A, double* U, double* s, double* Vt, size_t smem,
-                     int thr, const ReadTicket& pub) {
+                     int thr, const ReadTicket& pub, const KeepArgs& keep) {
   max_dynamic_smem((const void*)svd_warp_kernel<RPL, NPX>, (int)kSmemCap);
-  svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt, pub);
+  svd_warp_kernel<RPL, NPX><<<1, thr, smem, stream()>>>(m, n, A, U, s, Vt, pub, keep);
+}
+
+__global__ void split_keep_kernel(const double* s, int n, KeepArgs a) {
+  if (threadIdx.x == 0) split_keep_device(s, n, a);
 }
 
 // Householder QR of a tall block (m rows <= 32 * RPL, n <= 32 * CPW columns,
@@ -1110,7 +1115,7 @@ void svd_tall(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt
 
 namespace {
 void svd_thin_run(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt, const ReadTicket* pub,
-                  bool& published) {
+                  const KeepArgs* keep, bool& published) {
   T2S2_REQUIRE(m > 0 && n > 0, kErrShape, "svd_thin: empty matrix");
   {
     const int mp = m >= n ? m : n, np = m >= n ? n : m;
@@ -1124,13 +1129,14 @@ void svd_thin_run(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor
         LaunchScope ls("svd_jacobi", 4.0 * mp * (double)np * np, 8.0 * m * (double)n);
         const int thr = 32 * (np < 2 ? 2 : np);
         const ReadTicket tk = pub ? *pub : ReadTicket{};
-        published = pub != nullptr;
+        const KeepArgs kp = keep ? *keep : KeepArgs{};
+        published = true;
         const int rpl = (mp + 31) / 32;
 #define T2S2_SVD_WARP(NPX)                                                            \
   do {                                                                            \
-    if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk);   \
-    else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk); \
-    else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk);           \
+    if (rpl <= 4) launch_svd_warp<4, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk, kp);   \
+    else if (rpl <= 8) launch_svd_warp<8, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk, kp); \
+    else launch_svd_warp<12, NPX>(m, n, A, U.p, s.p, Vt.p, wneed, thr, tk, kp);           \
   } while (0)
         if (np <= 4) T2S2_SVD_WARP(4);
         else if (np <= 8) T2S2_SVD_WARP(8);
@@ -1172,10 +1178,20 @@ void svd_thin_run(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor
 }
 }  // namespace
 
-void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt, const ReadTicket* pub) {
-  bool published = false;
-  svd_thin_run(m, n, A, U, s, Vt, pub, published);
-  if (pub && !published) read_publish(s.p, s.size() * sizeof(double), *pub);
+void split_keep(const double* s, int n, const KeepArgs& a) {
+  {
+    LaunchScope ls("reduce", 0, 0);
+    split_keep_kernel<<<1, 32, 0, stream()>>>(s, n, a);
+  }
+  T2S2_CHECK_LAUNCH();
+}
+
+void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt, const ReadTicket* pub,
+              const KeepArgs* keep) {
+  bool fused = false;  // the warp kernel published s / decided the rank itself
+  svd_thin_run(m, n, A, U, s, Vt, pub, keep, fused);
+  if (keep && !fused) split_keep(s.p, s.dim(0), *keep);
+  if (pub && !fused) read_publish(s.p, s.size() * sizeof(double), *pub);
 }
 
 }  // namespace t2s2

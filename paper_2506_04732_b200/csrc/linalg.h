@@ -26,11 +26,45 @@ void qr_r(int m, int n, const double* A, DTensor& R, bool cm = false);
 
 // Thin SVD A = U diag(s) Vt of a row-major m x n matrix, k = min(m, n),
 // singular values descending.  Tall case: QR, then one-sided Jacobi on R.
+// Truncation rank of a split decided on the device (tt_solver.py:249-258,
+// 268-270): delta = tol * ||s|| / rootd, keep = first k with ||s[k:]|| <= delta
+// (at least 1), capped at max_rank; keep_out[0] = keep, mask[j] = j < keep.
+// Products and sums are rounded separately, in the reference's order.
+struct KeepArgs {
+  double tol, rootd;
+  int max_rank;
+  double* keep_out;
+  double* mask;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ void split_keep_device(const double* s, int n, const KeepArgs& a) {
+  double nrm = 0.0;
+  for (int k = 0; k < n; ++k) nrm = __dadd_rn(nrm, __dmul_rn(s[k], s[k]));
+  const double delta = a.tol * sqrt(nrm) / a.rootd;
+  int r = n;
+  double acc = 0.0;
+  // tails from the back; keep the FIRST k with tail <= delta
+  for (int k = n - 1; k >= 0; --k) {
+    acc = __dadd_rn(acc, __dmul_rn(s[k], s[k]));
+    if (sqrt(acc) <= delta) r = k;
+  }
+  if (n == 0) r = 1;
+  if (r < 1) r = 1;
+  if (r > a.max_rank) r = a.max_rank;
+  a.keep_out[0] = (double)r;
+  for (int j = 0; j < n; ++j) a.mask[j] = j < r ? 1.0 : 0.0;
+}
+#endif
+// One-thread kernel around split_keep_device (s in device memory).
+void split_keep(const double* s, int n, const KeepArgs& a);
+
 // pub: an open read ticket (common.h) for the min(m, n) singular values —
 // the kernel that finishes s publishes it (as soon as s is known, before U
 // and Vt are written), other paths with a publish launch.
+// keep: the truncation rank of the split is decided by the same kernel
+// (one launch less; other paths run the one-thread kernel).
 void svd_thin(int m, int n, const double* A, DTensor& U, DTensor& s, DTensor& Vt,
-              const ReadTicket* pub = nullptr);
+              const ReadTicket* pub = nullptr, const KeepArgs* keep = nullptr);
 
 // In-place LU with partial pivoting of a column-major N x N matrix (ld=N);
 // ipiv 0-based row swaps; *info_dev = 0 or 1 + first zero pivot column.
