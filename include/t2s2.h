@@ -187,9 +187,9 @@ int t2s2_solve(t2s2_context* ctx, const t2s2_train* a, const t2s2_train* rhs,
                t2s2_solve_report* report);
 /* Dense solve of one local system (column-major n x n) — the kernels behind
  * the direct local solves (tt_solver.py:357-366, 392-397), exposed for
- * testing: the verified no-pivot block Gauss-Jordan kernel (GEPP's factors
- * whenever partial pivoting would make no interchange), else the
- * partial-pivoting kernel; returns T2S2_ERR_VALUE on an exactly singular
+ * testing: the verified block Gauss-Jordan kernel (threshold partial
+ * pivoting: no interchange while every multiplier is <= 8 in magnitude;
+ * GEPP's factors when none exceeds 1), else the partial-pivoting kernel; returns T2S2_ERR_VALUE on an exactly singular
  * matrix (numpy.linalg.solve's LinAlgError). */
 int t2s2_dense_solve(t2s2_context* ctx, int n, const double* a_colmajor, const double* b,
                      double* x);

@@ -74,14 +74,15 @@ void lu_solve(int N, const double* LU, const int* ipiv, double* b);
 // One cooperative launch: factor A (clobbered) and overwrite b with the
 // solution.  Returns false when N is too large for the smem panel.
 // *swapped (optional, not cleared here) is set to 1 if any row was
-// interchanged, i.e. when the no-pivot kernel would have declined.
+// interchanged.
 bool lu_solve_fused(int N, double* A, double* b, int* piv, int* info_dev, int* swapped = nullptr);
-// Verified no-pivot dense solve by blocked Gauss-Jordan (one cooperative
-// launch, gj_solve.cu): when partial pivoting would make no interchange —
-// every multiplier |l| <= 1 — it computes GEPP's factors without a pivot
-// search and overwrites b with the solution.  Otherwise (or on a zero
-// pivot) it sets *info_dev = -1 and leaves A, b clobbered: rebuild and use
-// the pivoting kernel.  Returns false when not applicable (nothing launched).
+// Verified dense solve by blocked Gauss-Jordan without interchanges (one
+// cooperative launch, gj_solve.cu): threshold partial pivoting — while every
+// multiplier satisfies |l| <= 8 it eliminates without a pivot search
+// (|l| <= 1 throughout means these are GEPP's factors) and overwrites b with
+// the solution.  Otherwise (or on a zero pivot) it sets *info_dev = -1 and
+// leaves A, b clobbered: rebuild and use the pivoting kernel.  Returns false
+// when not applicable (nothing launched).
 bool gj_solve_nopivot(int N, double* A, double* b, int* info_dev);
 
 }  // namespace t2s2
