@@ -705,6 +705,19 @@ __global__ void split_keep_kernel(const double* s, int n, KeepArgs a) {
 // H_0 ... H_{n-1} [I; 0], no barriers) and R; mode R (TSQR leaf): CTA b
 // factors rows [b*chunk, b*chunk + rows) and writes its n x n R at rows
 // [b*n, (b+1)*n) of the output.  A, Q column-major when cm, else row-major.
+#ifdef WQR_MICRO
+__device__ unsigned long long g_wqr_t[4];  // owner: form; everyone (warp 1): barrier wait, apply
+#define WQR_T0 long long wq_t = clock64();
+#define WQR_T(k, cond)                                    \
+  if ((cond) && lane == 0) {                              \
+    const long long t_ = clock64();                       \
+    atomicAdd(&g_wqr_t[k], (unsigned long long)(t_ - wq_t)); \
+  }                                                       \
+  wq_t = clock64();
+#else
+#define WQR_T0
+#define WQR_T(k, cond)
+#endif
 template <int RPL, int CPW, bool WANTQ>
 __global__ void __launch_bounds__(512)
     wqr_kernel(int m, int n, int chunk, const double* __restrict__ A, double* Q, double* R, int cm,
@@ -727,8 +740,10 @@ __global__ void __launch_bounds__(512)
       a[q][r] = (c < n && i < mr) ? (cm ? A[(size_t)c * m + r0 + i] : A[(size_t)(r0 + i) * n + c]) : 0.0;
     }
   }
+  WQR_T0
   for (int j = 0; j < k; ++j) {
     const int ow = j % nw, oq = j / nw;
+    WQR_T(3, false)
     if (warp == ow) {
       double ss = 0.0, alpha = 0.0;
 #pragma unroll
@@ -768,7 +783,9 @@ __global__ void __launch_bounds__(512)
           }
       if (lane == 0) tau[j] = t;
     }
+    WQR_T(0, warp == ow && blockIdx.x == 0)
     __syncthreads();
+    WQR_T(1, warp == (ow + 1) % nw && blockIdx.x == 0)
     const double t = tau[j];
     if (t != 0.0) {
       const double* v = vb + (size_t)j * mr;
@@ -801,6 +818,7 @@ __global__ void __launch_bounds__(512)
         }
       }
     }
+    WQR_T(2, warp == (ow + 1) % nw && blockIdx.x == 0)
   }
   // columns j >= k (wide leaf, mr < n): their R rows < k are the updated values
 #pragma unroll
@@ -956,8 +974,8 @@ void qr_r(int m, int n, const double* A, DTensor& R, bool cm) {
       if (ok) {
         T2S2_CHECK_LAUNCH();
         if (blocks == 1) {
-          R = DTensor({k, n});
-          dcopy(R.p, stacked.p, (size_t)k * n);
+          R = std::move(stacked);  // k == n here (m >= n): the leaf's factor is R
+          R.view({k, n});
           return;
         }
         qr_r(blocks * n, n, stacked.p, R);
