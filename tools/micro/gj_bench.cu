@@ -55,7 +55,7 @@ __global__ void special_loop(GjArgs a, int reps, long long* cyc) {
   long long tt = 0, td = 0;
   for (int r = 0; r < reps; ++r) {
     long long t0 = clock64();
-    special_tile(a, ph, s);
+    special_tile(a, ph, s, false);
     __syncthreads();
     long long t1 = clock64();
     for (int e = threadIdx.x; e < kP * 33; e += kThr) s.dg[e] += (e % 34 == 0) ? 40.0 : 0.0;
