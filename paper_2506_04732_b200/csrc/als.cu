@@ -515,10 +515,16 @@ DTensor galerkin_matrix(const DTensor& pal, const DTensor& ac, const DTensor& pa
 // 1 + first zero pivot) lands in *info_dev and is read back by the caller.
 // Partial-pivoting dense solve (the reference's numpy.linalg.solve).
 // info_dev[1] (set to 1, never cleared here) records a row interchange.
-void dense_solve_pivoted(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
+// consume: the right-hand side is not needed afterwards — it becomes the
+// solution buffer instead of being copied (the caller recomputes it in the
+// rare case it solves the same system again).
+void dense_solve_pivoted(DTensor& M, DTensor& rhs, DTensor& out, int* info_dev, bool consume = false) {
   const int N = M.dim(0);
   int* ipiv = reinterpret_cast<int*>(allocator().alloc((N + 1) / 2 + 1));
-  out = rhs.clone();
+  if (consume)
+    out = std::move(rhs);
+  else
+    out = rhs.clone();
   if (!lu_solve_fused(N, M.p, out.p, ipiv, info_dev, info_dev + 1)) {
     lu_factor(N, M.p, ipiv, info_dev);
     lu_solve(N, M.p, ipiv, out.p);
@@ -530,10 +536,15 @@ void dense_solve_pivoted(DTensor& M, const DTensor& rhs, DTensor& out, int* info
 // partial pivoting would not interchange rows); *info_dev == -1 afterwards
 // means it declined and the caller must rebuild M and call
 // dense_solve_pivoted.
-void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
-  out = rhs.clone();
+void dense_solve(DTensor& M, DTensor& rhs, DTensor& out, int* info_dev, bool consume = false) {
+  if (consume)
+    out = std::move(rhs);
+  else
+    out = rhs.clone();
   if (gj_solve_nopivot(M.dim(0), M.p, out.p, info_dev)) return;
-  dense_solve_pivoted(M, rhs, out, info_dev);
+  // not applicable (nothing launched, the buffer is untouched): the pivoting kernel
+  DTensor again = std::move(out);
+  dense_solve_pivoted(M, again, out, info_dev, true);
 }
 
 // Which dense kernel a kind of local system tries first.  The no-pivot
@@ -546,11 +557,11 @@ void dense_solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) {
 struct PivotPolicy {
   int declines = 0;
   bool pivot_first = false;
-  void solve(DTensor& M, const DTensor& rhs, DTensor& out, int* info_dev) const {
+  void solve(DTensor& M, DTensor& rhs, DTensor& out, int* info_dev, bool consume = false) const {
     if (pivot_first)
-      dense_solve_pivoted(M, rhs, out, info_dev);
+      dense_solve_pivoted(M, rhs, out, info_dev, consume);
     else
-      dense_solve(M, rhs, out, info_dev);
+      dense_solve(M, rhs, out, info_dev, consume);
   }
   void observe(int info, int swapped) {  // after the first attempt of a system
     if (pivot_first) {
@@ -886,6 +897,13 @@ struct Sweep {
       nop.add(gb, 0, u_old.p, nu_old.p);
       gb.run();
     }
+    // the Galerkin right-hand side again (the direct solve consumes it): same program, same bits
+    auto regal = [&]() {
+      GemmBatch gb;
+      DTensor c = galerkin_rhs(gb, 0, lb[l], bc, rb[l + 1]);
+      gb.run();
+      return c;
+    };
     probe.run(0, u_old, nu_old, c_ls, false, true);  // and clears the solver flags
     const bool direct = cfg.local_solver == 1 || (cfg.local_solver == 0 && size <= cfg.local_direct_size);
     const double inner_rtol = std::fmax(cfg.inner_tol_factor * current_res, 1e-12);
@@ -896,7 +914,7 @@ struct Sweep {
     if (try_gal) {
       if (direct) {
         DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
-        pol_gal.solve(B, c_gal, u_gal, probe.info());
+        pol_gal.solve(B, c_gal, u_gal, probe.info(), true);  // c_gal becomes u_gal
       } else {
         // scipy gmres(x0=u_old, rtol, atol=0, restart=40, maxiter=10)
         u_gal = u_old.clone();
@@ -916,8 +934,9 @@ struct Sweep {
     if (try_gal && direct && info == -1) {
       // the block needs row interchanges: rebuild it, partial pivoting
       DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+      c_gal = regal();
       probe.clear_info();
-      dense_solve_pivoted(B, c_gal, u_gal, probe.info());
+      dense_solve_pivoted(B, c_gal, u_gal, probe.info(), true);
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
       probe.run(1, u_gal, nu_gal, c_ls, true, false, &g_gal);
@@ -926,6 +945,7 @@ struct Sweep {
     if (try_gal && direct && info != 0) {
       // singular Galerkin block: numpy.linalg.lstsq fallback (tt_solver.py:362)
       DTensor B = galerkin_matrix(la[l], ac, ra[l + 1]);
+      c_gal = regal();
       lstsq_dense(B, c_gal, u_gal);
       u_gal.view(u_old.shape);
       nu_gal = nop.apply(u_gal);
@@ -1031,8 +1051,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
   const int d = x.d();
   std::vector<DTensor> cores = std::move(x.cores);
   double best_res = INFINITY;
-  std::vector<DTensor> best_cores;
-  for (auto& c : cores) best_cores.push_back(c.clone());
+  std::vector<DTensor> best_cores = clone_all(cores);
   double current_res = 1.0;
   Sweep sw(A, rhs, cfg);
 
@@ -1106,7 +1125,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
         // it.  Not for a GMRES candidate: the reference restarts GMRES from
         // the new core (x0 = u_old), which iterates on unless the forward run
         // reached its tolerance (tt_solver.py:367-377), so that case re-solves.
-        u = cores[l].clone();
+        u = std::move(cores[l]);  // cores[l] is replaced by the split below
         grad = std::move(end_grad);
         choice = 1;
       } else {
@@ -1154,8 +1173,7 @@ Train als_solve(const Train& A, const Train& rhs, const Train& x0, const SolverC
       if (done) {
         best_cores = std::move(cores);  // the sweep loop ends here: no copy
       } else {
-        best_cores.clear();
-        for (auto& c : cores) best_cores.push_back(c.clone());
+        best_cores = clone_all(cores);
       }
     }
     if (done) {

@@ -778,11 +778,16 @@ int t2s2_march(t2s2_context* ctx, const t2s2_train* left, const t2s2_train* righ
     T2S2_REQUIRE(step_tol > 0, kErrValue, "step rounding tolerance must be positive");
     const SolverConfig sc = to_cfg(cfg);
     if (failed_step) *failed_step = 0;
-    Train state = state0->t.clone();
+    // the current state: the caller's initial train (read only) in step 1, then
+    // this loop's own; a state that is stored is handed over when its
+    // successor exists (no copies)
+    Train own;
+    const Train* cur = &state0->t;
     if (states_out)
       for (int k = 0; k < n_steps; ++k) states_out[k] = nullptr;
     for (int k = 1; k <= n_steps; ++k) {
       const int f = n_forcing == 1 ? 0 : k - 1;
+      const Train& state = *cur;
       Train rhs = tt_apply(right->t, state);
       if (bc && bc[f]) rhs = tt_add(rhs, bc[f]->t);
       if (src && src[f]) rhs = tt_add(rhs, src[f]->t);
@@ -798,17 +803,21 @@ int t2s2_march(t2s2_context* ctx, const t2s2_train* left, const t2s2_train* righ
                  achieved);
         throw Error(kErrStagnation, msg);
       }
-      state = tt_round(nxt, step_tol, 0);
+      Train next = tt_round(nxt, step_tol, 0);
       if (reports) {
         reports[k - 1].step = k;
-        reports[k - 1].max_rank = state.max_rank();
-        reports[k - 1].compression = compression_ratio(state);
+        reports[k - 1].max_rank = next.max_rank();
+        reports[k - 1].compression = compression_ratio(next);
         reports[k - 1].residual = rep.residuals.back();
         reports[k - 1].sweeps = (int)rep.residuals.size();
       }
-      if (states_out && store_stride > 0 && (k % store_stride == 0 || k == n_steps))
-        states_out[k - 1] = wrap(state.clone());
+      // the previous state of this loop is no longer read: store it or drop it
+      if (k >= 2 && states_out && store_stride > 0 && (k - 1) % store_stride == 0)
+        states_out[k - 2] = wrap(std::move(own));
+      own = std::move(next);
+      cur = &own;
     }
+    if (states_out && store_stride > 0) states_out[n_steps - 1] = wrap(std::move(own));
   });
 }
 

@@ -569,7 +569,9 @@ void transpose(const double* in, double* out, int rows, int cols) {
 }
 
 void dcopy(double* dst, const double* src, size_t n) {
-  if (n) T2S2_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  if (!n) return;
+  LaunchScope ls("copy", 0, 16.0 * n);  // a copy-engine node on the stream, counted like a launch
+  T2S2_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
 }
 
 void dfill(double* dst, double v, size_t n) {
@@ -746,6 +748,29 @@ void to_host(double* h, const double* d, size_t n) { host_read(h, d, n * sizeof(
 
 void to_device(double* d, const double* h, size_t n) {
   if (n) T2S2_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, stream()));
+}
+
+std::vector<DTensor> clone_all(const std::vector<DTensor>& v) {
+  std::vector<DTensor> out;
+  out.reserve(v.size());
+  Segments a{};
+  long long most = 0;
+  for (const DTensor& t : v) {
+    out.emplace_back(t.shape);
+    if (!t.size()) continue;
+    if (a.k == 8) {
+      run_segments(a, most);
+      a.k = 0;
+      most = 0;
+    }
+    a.dst[a.k] = out.back().p;
+    a.src[a.k] = t.p;
+    a.n[a.k] = (long long)t.size();
+    most = a.n[a.k] > most ? a.n[a.k] : most;
+    a.k++;
+  }
+  run_segments(a, most);
+  return out;
 }
 
 DTensor DTensor::clone() const {

@@ -162,13 +162,15 @@ double tt_norm(const Train& t) {
     const int r0 = c.dim(0), r1 = c.dim(-1);
     const int mid = (int)(c.size() / ((size_t)r0 * r1));
     const int k = l == t.d() - 1 ? r1 : Rp.dim(0);
-    DTensor Y({r0 * mid, k});
-    if (l == t.d() - 1)
-      dcopy(Y.p, c.p, c.size());
-    else
+    DTensor Y;
+    const double* Yp = c.p;  // the last core is its own Y (r1 = k = 1 column block), read only
+    if (l < t.d() - 1) {
+      Y = DTensor({r0 * mid, k});
       gemm(false, true, r0 * mid, k, r1, 1.0, c.p, r1, Rp.p, r1, 0.0, Y.p, k);
-    if (l == 0) return dnrm2(Y.p, Y.size());
-    qr_r(mid * k, r0, Y.p, Rp, true);  // Y row-major r0 x (mid k) = column-major (mid k) x r0
+      Yp = Y.p;
+    }
+    if (l == 0) return dnrm2(Yp, (size_t)r0 * mid * k);
+    qr_r(mid * k, r0, Yp, Rp, true);  // Y row-major r0 x (mid k) = column-major (mid k) x r0
   }
   return 0.0;
 }
