@@ -444,7 +444,7 @@ def run_b200_march(args, torch, dd):
             state = nxt
         t_wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
-    gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
+    gpu_launches = sum(v["launches"] for k, v in _native.stats_read().items() if k != "copy")  # kernels; "copy" = copy-engine nodes
     elapsed = dd.max(total_ms / 1e3)
     dd.barrier()
     value = dd.world * K / elapsed
@@ -674,7 +674,7 @@ def run_b200_sweep(args, torch, dd):
             sweeps += len(rep.residual_history)
             reports.append((i, rep.residual_history[-1], rep.rank_history[-1]))
             h.free()
-    gpu_launches = sum(v["launches"] for v in _native.stats_read().values())
+    gpu_launches = sum(v["launches"] for k, v in _native.stats_read().items() if k != "copy")  # kernels; "copy" = copy-engine nodes
     elapsed = dd.max(total_ms / 1e3)
     value = dd.world * K / elapsed
     serial = None
